@@ -1,0 +1,383 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// extern "C" shim over the UNMODIFIED reference sources
+// (/root/reference/proj/src/{tensor,network,car_following,node_model,
+// observation,engine,optimization}.cpp), compiled by oracle/Makefile into
+// oracle/_ref/libdtsim_ref.so.  It only builds reference objects
+// (Scenario, LinkParams, RngStream, LossBuilder) and calls the reference's
+// own entry points:
+//   simulate_forward   include/dtsim/engine.hpp:76-78  (src/engine.cpp:227-254)
+//   simulate_gradient  include/dtsim/engine.hpp:105-107 (src/engine.cpp:303-429)
+// so the outputs ARE the reference's outputs.  Used by tests/ (golden
+// generation, oracle pinning) and by bench.py's `--impl reference` arm.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dtsim/engine.hpp"
+#include "dtsim/network.hpp"
+#include "dtsim/optimization.hpp"
+
+using namespace dtsim;
+
+namespace {
+thread_local std::string g_err;
+
+struct RefScn {
+  Scenario s;
+};
+
+LinkParams make_params(int L, const double* u, const double* k,
+                       const double* b, const double* a, const double* c) {
+  LinkParams p;
+  p.u.assign(u, u + L);
+  p.kappa.assign(k, k + L);
+  p.beta.assign(b, b + L);
+  p.alpha.assign(a, a + L);
+  p.cost.assign(c, c + L);
+  return p;
+}
+
+// Compact (link, pos) of a dense N x L row-major state; exactly the
+// reference's compact_state rule (src/engine.cpp:267-285).
+void compact(const std::vector<double>& X, int N, int L, double M, int* link,
+             double* pos) {
+  for (int i = 0; i < N; ++i) {
+    link[i] = -1;
+    pos[i] = 0.0;
+    for (int j = 0; j < L; ++j) {
+      const double x = X[static_cast<std::size_t>(i) * L + j];
+      if (x != -M) {
+        link[i] = j;
+        pos[i] = x;
+        break;
+      }
+    }
+  }
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ---- RNG (include/dtsim/rng.hpp) -------------------------------------------
+uint64_t ref_rng_fork(uint64_t seed, uint64_t label) {
+  return RngStream(seed).fork(label).seed();
+}
+uint64_t ref_rng_bits(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  return RngStream(seed).bits(a, b, c);
+}
+double ref_rng_uniform(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  return RngStream(seed).uniform(a, b, c);
+}
+/// One Gumbel draw exactly as gumbel_sample_keys computes it
+/// (src/tensor.cpp:682-699): stream `seed`, key, row key, column key.
+double ref_gumbel(uint64_t seed, uint64_t key, int row, int col) {
+  std::vector<int> rk{row}, ck{col};
+  return gumbel_sample_keys({1, 1}, RngStream(seed), key, &rk, &ck).vals()[0];
+}
+
+// ---- scenarios ---------------------------------------------------------------
+/// Explicit-link scenario (make_network, network.cpp:238-247).  kind: 0 physical,
+/// 1 virtual inflow, 2 virtual outflow.  n_custom > 0 sets custom_init.
+void* ref_scenario_links(int n_nodes, int n_links, const int* from,
+                         const int* to, const double* len, const int* kind) {
+  auto* r = new RefScn;
+  std::vector<Link> links(n_links);
+  for (int i = 0; i < n_links; ++i) {
+    links[i].id = i;
+    links[i].from_node = from[i];
+    links[i].to_node = to[i];
+    links[i].length = len[i];
+    links[i].kind = static_cast<LinkKind>(kind[i]);
+  }
+  r->s.net = make_network(n_nodes, std::move(links));
+  return r;
+}
+
+/// Synthetic grid (SURVEY §8d generator) + attach_virtual_links
+/// (network.cpp:151-201) with RngStream(net_seed).
+void* ref_scenario_grid(int n, double len, uint64_t net_seed, double virt_len) {
+  void* out = nullptr;
+  if (guarded([&] {
+        std::vector<Link> links;
+        auto push = [&](int a, int b) {
+          Link l;
+          l.from_node = a;
+          l.to_node = b;
+          l.length = len;
+          l.kind = LinkKind::Physical;
+          links.push_back(l);
+        };
+        for (int r = 0; r < n; ++r)
+          for (int c = 0; c < n; ++c) {
+            if (c + 1 < n) {
+              push(r * n + c, r * n + c + 1);
+              push(r * n + c + 1, r * n + c);
+            }
+            if (r + 1 < n) {
+              push(r * n + c, (r + 1) * n + c);
+              push((r + 1) * n + c, r * n + c);
+            }
+          }
+        Network phys = make_network(n * n, std::move(links));
+        auto* rs = new RefScn;
+        rs->s.net = attach_virtual_links(phys, RngStream(net_seed), virt_len);
+        out = rs;
+      }))
+    return nullptr;
+  return out;
+}
+
+void ref_scenario_free(void* h) { delete static_cast<RefScn*>(h); }
+
+void ref_scenario_config(void* h, int n_vehicles, int delta_n, double tau,
+                         double gumbel_tau, int trajectory_grafting,
+                         int horizon_steps, int obs_interval_s) {
+  auto& s = static_cast<RefScn*>(h)->s;
+  s.n_vehicles = n_vehicles;
+  s.cfg.delta_n = delta_n;
+  s.cfg.tau = tau;
+  s.cfg.gumbel_tau = gumbel_tau;
+  s.cfg.trajectory_grafting = trajectory_grafting != 0;
+  s.horizon_steps = horizon_steps;
+  s.obs_interval_s = obs_interval_s;
+}
+
+void ref_scenario_custom_init(void* h, int n, const int* link,
+                              const double* pos) {
+  auto& s = static_cast<RefScn*>(h)->s;
+  s.custom_init.clear();
+  for (int i = 0; i < n; ++i) s.custom_init.push_back({link[i], pos[i]});
+}
+
+int ref_fit_inflow_queues(void* h) {
+  return guarded([&] { fit_inflow_queues(static_cast<RefScn*>(h)->s); });
+}
+
+int ref_n_links(void* h) { return static_cast<RefScn*>(h)->s.net.n_links(); }
+int ref_n_nodes(void* h) { return static_cast<RefScn*>(h)->s.net.n_nodes; }
+int ref_n_agents(void* h) {
+  int n = -1;
+  if (guarded([&] { n = static_cast<RefScn*>(h)->s.n_agents(); })) return -1;
+  return n;
+}
+
+void ref_links(void* h, int* from, int* to, double* len, int* kind) {
+  const auto& net = static_cast<RefScn*>(h)->s.net;
+  for (int i = 0; i < net.n_links(); ++i) {
+    from[i] = net.links[i].from_node;
+    to[i] = net.links[i].to_node;
+    len[i] = net.links[i].length;
+    kind[i] = static_cast<int>(net.links[i].kind);
+  }
+}
+
+void ref_adjacency(void* h, double* adj) {
+  const auto& a = static_cast<RefScn*>(h)->s.net.adjacency;
+  std::memcpy(adj, a.data(), a.size() * sizeof(double));
+}
+
+int ref_sample_parameters(void* h, uint64_t seed, int mean_mode, double* u,
+                          double* k, double* b, double* a, double* c) {
+  return guarded([&] {
+    const auto& net = static_cast<RefScn*>(h)->s.net;
+    LinkParams p =
+        sample_parameters(net, ParamRanges{}, RngStream(seed), mean_mode != 0);
+    const std::size_t L = p.u.size();
+    std::memcpy(u, p.u.data(), L * 8);
+    std::memcpy(k, p.kappa.data(), L * 8);
+    std::memcpy(b, p.beta.data(), L * 8);
+    std::memcpy(a, p.alpha.data(), L * 8);
+    std::memcpy(c, p.cost.data(), L * 8);
+  });
+}
+
+int ref_seed_agents(void* h, int* link, double* pos) {
+  return guarded([&] {
+    InitialState init = seed_agents(static_cast<RefScn*>(h)->s);
+    for (std::size_t i = 0; i < init.link.size(); ++i) {
+      link[i] = init.link[i];
+      pos[i] = init.pos[i];
+    }
+  });
+}
+
+int ref_steps_for_minutes(int delta_n, double tau, double minutes) {
+  int out = -1;
+  SimConfig c;
+  c.delta_n = delta_n;
+  c.tau = tau;
+  if (guarded([&] { out = steps_for_minutes(c, minutes); })) return -1;
+  return out;
+}
+
+// ---- hot path ------------------------------------------------------------------
+/// simulate_forward (src/engine.cpp:227-254).  cum_per_step: T x L.
+/// link_final/pos_final: compact final state per agent.  If states_link is
+/// non-null, record_states is set and every step's compact state (T x N) is
+/// returned.  wall: the reference's own wall_seconds.
+int ref_forward(void* h, const double* u, const double* k, const double* b,
+                const double* a, const double* c, uint64_t seed,
+                uint64_t noise_iteration, double* cum_per_step, int* link_final,
+                double* pos_final, int* states_link, double* states_pos,
+                double* wall) {
+  return guarded([&] {
+    const auto& s = static_cast<RefScn*>(h)->s;
+    const int L = s.net.n_links();
+    const int N = s.n_agents();
+    ForwardOptions opt;
+    opt.noise_iteration = noise_iteration;
+    opt.record_states = states_link != nullptr;
+    const Trajectory tr =
+        simulate_forward(s, make_params(L, u, k, b, a, c), RngStream(seed), opt);
+    for (int t = 0; t < tr.steps; ++t)
+      std::memcpy(cum_per_step + static_cast<std::size_t>(t) * L,
+                  tr.cum_per_step[t].data(), L * 8);
+    compact(tr.X_final, N, L, s.cfg.sentinel, link_final, pos_final);
+    if (states_link)
+      for (int t = 0; t < tr.steps; ++t)
+        compact(tr.states[t], N, L, s.cfg.sentinel,
+                states_link + static_cast<std::size_t>(t) * N,
+                states_pos + static_cast<std::size_t>(t) * N);
+    if (wall) *wall = tr.wall_seconds;
+  });
+}
+
+/// simulate_gradient (src/engine.cpp:303-429) with a linear+quadratic loss
+///   loss = sum_k sum_j (ws[k,j] s_kj + 0.5 qs[k,j] s_kj^2)
+///        + sum_j (wc[j] c_j + 0.5 qc[j] c_j^2) + sum_n wx[n] X_final[n, link_n]
+/// over the snapshot leaves s_k, cum_final c and the valid cells of X_final,
+/// built from reference tape ops (it is a LossBuilder like any caller's).
+/// Any of ws/qs/wc/qc/wx may be null.  mode: 0 FullTape, 1 Checkpointed.
+/// grads: 5 x L (u, kappa, beta, alpha, cost).  snaps: n_snap x L.
+int ref_gradient(void* h, const double* u, const double* k, const double* b,
+                 const double* a, const double* c, uint64_t seed,
+                 uint64_t noise_iteration, int mode, const double* ws,
+                 const double* qs, const double* wc, const double* qc,
+                 const double* wx, double* loss, double* grads, double* snaps,
+                 int* n_snaps, double* cum_final, int* link_final,
+                 double* pos_final, double* wall) {
+  return guarded([&] {
+    const auto& s = static_cast<RefScn*>(h)->s;
+    const int L = s.net.n_links();
+    const int N = s.n_agents();
+    const double M = s.cfg.sentinel;
+    LossBuilder builder = [=](Tape&, const LossInputs& li) -> Tensor {
+      Tensor acc = Tensor::zeros({1, 1});
+      const int K = static_cast<int>(li.snapshots.size());
+      for (int kk = 0; kk < K; ++kk) {
+        const Tensor& sk = li.snapshots[kk];
+        if (ws)
+          acc = add(acc, reduce_sum(mul(sk, Tensor::from(std::vector<double>(
+                                                 ws + kk * L, ws + kk * L + L),
+                                                 {L, 1})),
+                                    kAxisAll));
+        if (qs)
+          acc = add(acc,
+                    reduce_sum(mul(mul(sk, sk),
+                                   scale(Tensor::from(std::vector<double>(
+                                                          qs + kk * L,
+                                                          qs + kk * L + L),
+                                                      {L, 1}),
+                                         0.5)),
+                               kAxisAll));
+      }
+      if (wc)
+        acc = add(acc, reduce_sum(mul(li.cum_final,
+                                      Tensor::from(std::vector<double>(wc, wc + L),
+                                                   {L, 1})),
+                                  kAxisAll));
+      if (qc)
+        acc = add(acc,
+                  reduce_sum(mul(mul(li.cum_final, li.cum_final),
+                                 scale(Tensor::from(
+                                           std::vector<double>(qc, qc + L), {L, 1}),
+                                       0.5)),
+                             kAxisAll));
+      if (wx) {
+        const auto& xv = li.X_final.vals();
+        std::vector<int> idx;
+        std::vector<double> w;
+        for (int i = 0; i < N; ++i)
+          for (int j = 0; j < L; ++j)
+            if (xv[static_cast<std::size_t>(i) * L + j] != -M) {
+              idx.push_back(i * L + j);
+              w.push_back(wx[i]);
+              break;
+            }
+        if (!idx.empty()) {
+          const int m = static_cast<int>(idx.size());
+          acc = add(acc, reduce_sum(mul(gather(li.X_final, idx),
+                                        Tensor::from(std::move(w), {m, 1})),
+                                    kAxisAll));
+        }
+      }
+      return acc;
+    };
+    ForwardOptions opt;
+    opt.noise_iteration = noise_iteration;
+    const GradResult g = simulate_gradient(
+        s, make_params(L, u, k, b, a, c), RngStream(seed), builder,
+        mode == 0 ? GradMode::FullTape : GradMode::Checkpointed, opt);
+    *loss = g.loss;
+    std::memcpy(grads + 0 * L, g.grads.u.data(), L * 8);
+    std::memcpy(grads + 1 * L, g.grads.kappa.data(), L * 8);
+    std::memcpy(grads + 2 * L, g.grads.beta.data(), L * 8);
+    std::memcpy(grads + 3 * L, g.grads.alpha.data(), L * 8);
+    std::memcpy(grads + 4 * L, g.grads.cost.data(), L * 8);
+    if (n_snaps) *n_snaps = static_cast<int>(g.snapshot_values.size());
+    if (snaps)
+      for (std::size_t kk = 0; kk < g.snapshot_values.size(); ++kk)
+        std::memcpy(snaps + kk * L, g.snapshot_values[kk].data(), L * 8);
+    if (cum_final) std::memcpy(cum_final, g.cum_final_values.data(), L * 8);
+    if (link_final) compact(g.X_final_values, N, L, M, link_final, pos_final);
+    if (wall) *wall = g.wall_seconds;
+  });
+}
+
+/// Calibration loss: the reference's own mse_loss_builder
+/// (src/optimization.cpp:84-101) over observed links `obs_ids` (n_obs) and
+/// observations obs_vals (K x n_obs).
+int ref_gradient_mse(void* h, const double* u, const double* k,
+                     const double* b, const double* a, const double* c,
+                     uint64_t seed, uint64_t noise_iteration, int n_obs,
+                     const int* obs_ids, int K, const double* obs_vals,
+                     double* loss, double* grads) {
+  return guarded([&] {
+    const auto& s = static_cast<RefScn*>(h)->s;
+    const int L = s.net.n_links();
+    CountSeries obs;
+    obs.link_ids.assign(obs_ids, obs_ids + n_obs);
+    obs.interval_s = s.obs_interval_s;
+    for (int kk = 0; kk < K; ++kk)
+      obs.values.emplace_back(obs_vals + kk * n_obs, obs_vals + (kk + 1) * n_obs);
+    ForwardOptions opt;
+    opt.noise_iteration = noise_iteration;
+    const GradResult g = simulate_gradient(
+        s, make_params(L, u, k, b, a, c), RngStream(seed),
+        mse_loss_builder(obs, s.cfg.delta_n), GradMode::Checkpointed, opt);
+    *loss = g.loss;
+    std::memcpy(grads + 0 * L, g.grads.u.data(), L * 8);
+    std::memcpy(grads + 1 * L, g.grads.kappa.data(), L * 8);
+    std::memcpy(grads + 2 * L, g.grads.beta.data(), L * 8);
+    std::memcpy(grads + 3 * L, g.grads.alpha.data(), L * 8);
+    std::memcpy(grads + 4 * L, g.grads.cost.data(), L * 8);
+  });
+}
+
+}  // extern "C"
