@@ -1,0 +1,243 @@
+/* dtg — B200-native hot path of the differentiable traffic simulator.
+ *
+ * C-ABI drop-in boundary.  Plain pointers and sizes only; every entry point
+ * returns a status code and never throws.  Status codes follow the
+ * reference's C API (include/dtsim.h:17-20 — 0 ok, 1 runtime error,
+ * 2 configuration error, 3 divergence) plus DTG_ERR_CUDA / DTG_ERR_UNSUPPORTED.
+ *
+ * Two levels:
+ *
+ *  Level 1 — the device engine (dtg_ctx).  Replaces the reference's T-step
+ *  loops and reverse sweep inside
+ *     simulate_forward   /root/reference/proj/src/engine.cpp:227-254
+ *     simulate_gradient  /root/reference/proj/src/engine.cpp:303-429
+ *  i.e. engine_step (engine.cpp:70-125) and the checkpointed per-step VJP
+ *  (engine.cpp:388-415).  The host keeps the Scenario / LinkParams / LossBuilder
+ *  logic and hands the device a CSR network, parameters, an initial compact
+ *  state and noise seeds; it gets back counts, states and loss-seeded
+ *  gradients.  One context owns device memory for B independent scenarios
+ *  (stochastic draws) on one GPU and one CUDA stream.
+ *
+ *  Level 2 — scenario API (dtg_scenario).  The reference's host surface for
+ *  this path (Network / Scenario construction, seed_agents,
+ *  fit_inflow_queues, sample_parameters, simulate_forward,
+ *  simulate_gradient; include/dtsim/engine.hpp, network.hpp) as flat C calls
+ *  for ctypes / cgo / JNI-style bindings.  Implemented in C++ over level 1.
+ */
+#ifndef DTG_H
+#define DTG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DTG_OK = 0,
+  DTG_ERR_RUNTIME = 1,     /* std::runtime_error in the reference       */
+  DTG_ERR_CONFIG = 2,      /* ConfigError                               */
+  DTG_ERR_DIVERGENCE = 3,  /* DivergenceError (non-finite loss/grads)   */
+  DTG_ERR_CUDA = 4,        /* CUDA runtime / launch failure             */
+  DTG_ERR_UNSUPPORTED = 5  /* input outside the device path's contract  */
+};
+
+/* SimConfig (include/dtsim/car_following.hpp:31-40). */
+typedef struct {
+  int delta_n;             /* vehicles per agent (platoon size)           */
+  double tau;              /* reaction time, s;  dt = tau * delta_n       */
+  double sentinel;         /* M = 99999: "not on this link" marker        */
+  double gumbel_tau;       /* choice relaxation temperature (0.01)        */
+  int trajectory_grafting; /* TG on (1) / off (0)                         */
+} dtg_sim_config;
+
+/* Network as CSR: j is a successor of i iff i != j and
+ * to_node(i) == from_node(j) (network.cpp:28-35).  Successors of each link
+ * in ascending link id.  length[L] in meters. */
+typedef struct {
+  int n_links;
+  const int* succ_off; /* L + 1 */
+  const int* succ;     /* succ_off[L] */
+  const double* length;
+} dtg_net_desc;
+
+typedef struct dtg_ctx dtg_ctx;
+
+/* ---- Level 1: device engine ------------------------------------------------- */
+
+/* Allocate a context for n_scenarios (B) scenarios of n_agents (N) agents on
+ * the current CUDA device.  max_steps bounds the horizon kept in the
+ * checkpoint history (grown on demand).  Replaces the per-call setup of
+ * make_ctx (engine.cpp:40-59). */
+int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg,
+               int n_agents, int n_scenarios, int max_steps, dtg_ctx** out);
+void dtg_destroy(dtg_ctx* ctx);
+/* Last error message of this context (or of the failed dtg_create when
+ * ctx == NULL). */
+const char* dtg_last_error(const dtg_ctx* ctx);
+/* Run on this cudaStream_t (default: a stream owned by the context). */
+int dtg_set_stream(dtg_ctx* ctx, void* cuda_stream);
+/* Use CUDA graphs for the per-step launch sequence (default on). */
+int dtg_set_graphs(dtg_ctx* ctx, int enabled);
+
+/* Per-link parameter vectors (LinkParams, network.hpp:22-28) for one
+ * scenario, or all scenarios when scenario < 0. Host pointers, L each. */
+int dtg_set_params(dtg_ctx* ctx, int scenario, const double* u,
+                   const double* kappa, const double* beta, const double* alpha,
+                   const double* cost);
+/* Initial compact state per agent (seed_agents / custom_init output:
+ * engine.cpp:156-189), for one scenario or all (scenario < 0).  Positions
+ * below the validity threshold (-0.01) are rejected. */
+int dtg_set_state(dtg_ctx* ctx, int scenario, const int* link,
+                  const double* pos);
+/* Noise of one scenario (or all): the reference's
+ * rng.fork(kIteration).fork(noise_iteration) (engine.cpp:49). */
+int dtg_set_noise(dtg_ctx* ctx, int scenario, uint64_t root_seed,
+                  uint64_t noise_iteration);
+
+/* Run n_steps engine steps for every scenario from the state set by
+ * dtg_set_state.  checkpoint != 0 keeps every step's compact state on the
+ * device (required by dtg_backward and per-step dtg_read_state).
+ * steps_per_interval: observation interval in steps (snapshot boundaries
+ * (t + 1) % spi == 0, engine.cpp:321-323). */
+int dtg_forward(dtg_ctx* ctx, int n_steps, int steps_per_interval,
+                int checkpoint);
+
+/* Wait for the context's stream and report device-side errors of the last
+ * forward / backward (reads below do this implicitly). */
+int dtg_sync(dtg_ctx* ctx);
+/* Test hook: always take the exact ordered-sum path for the rows routed to
+ * the first arrived agent (normally used only on near ties). */
+int dtg_debug_force_slow_path(dtg_ctx* ctx, int on);
+
+/* Results of the last dtg_forward.
+ * cum_per_step: n_steps x L cumulative counts (Trajectory::cum_per_step).
+ * state: compact (link, pos) per agent after `step` steps (step in
+ * [0, n_steps]; any step needs checkpoint, n_steps works always). */
+int dtg_read_cum(dtg_ctx* ctx, int scenario, double* cum_per_step);
+int dtg_read_state(dtg_ctx* ctx, int scenario, int step, int* link,
+                   double* pos);
+/* Number of observation snapshots of the last forward. */
+int dtg_n_snapshots(const dtg_ctx* ctx);
+
+/* Checkpointed reverse sweep of the last dtg_forward(checkpoint=1).
+ * Seeds (host pointers, per scenario, scenario-major):
+ *   snap_seeds [B][K][L]  dLoss/dsnapshot_k (K = dtg_n_snapshots)
+ *   cum_seeds  [B][L]     dLoss/dcum_final
+ *   x_seeds    [B][N]     dLoss/dX_final at each agent's final valid cell
+ * Any seed pointer may be NULL (zero).  grads [B][5][L] (u, kappa, beta,
+ * alpha, cost) receives each scenario's parameter gradient. */
+int dtg_backward(dtg_ctx* ctx, const double* snap_seeds,
+                 const double* cum_seeds, const double* x_seeds,
+                 double* grads);
+/* Same with device pointers for seeds and output (the stream-ordered path
+ * used for NCCL reductions without a host round trip). */
+int dtg_backward_device(dtg_ctx* ctx, const double* d_snap_seeds,
+                        const double* d_cum_seeds, const double* d_x_seeds,
+                        double* d_grads);
+
+/* Device pointer to the cumulative-count history [n_steps + 1][B][L]
+ * (row 0 = zeros) of the last forward, valid until the next forward. */
+const double* dtg_device_cum(const dtg_ctx* ctx);
+/* Number of kernels the last forward / backward launched. */
+int64_t dtg_last_launches(const dtg_ctx* ctx);
+
+/* ---- Level 2: scenario API ---------------------------------------------------
+ * Mirrors include/dtsim/network.hpp + engine.hpp.  kind: 0 physical,
+ * 1 virtual inflow, 2 virtual outflow (LinkKind). */
+typedef struct dtg_scenario dtg_scenario;
+
+/* make_network (network.cpp:238-247) from explicit links. */
+dtg_scenario* dtg_scenario_from_links(int n_nodes, int n_links,
+                                      const int* from_node, const int* to_node,
+                                      const double* length, const int* kind);
+/* Synthetic n x n grid (east pair then south pair per node, row-major),
+ * then attach_virtual_links(RngStream(net_seed), virtual_length)
+ * (network.cpp:151-201).  NULL on error (see dtg_last_error(NULL)). */
+dtg_scenario* dtg_scenario_grid(int n, double length, uint64_t net_seed,
+                                double virtual_length);
+/* parse_tntp_text (network.cpp:58-118) + attach_virtual_links. */
+dtg_scenario* dtg_scenario_tntp(const char* text, double length_unit_scale,
+                                uint64_t net_seed, double virtual_length);
+void dtg_scenario_free(dtg_scenario* sc);
+/* Scenario fields + SimConfig; fit_queues != 0 runs fit_inflow_queues
+ * (engine.cpp:191-213). */
+int dtg_scenario_configure(dtg_scenario* sc, int n_vehicles, int delta_n,
+                           double tau, double gumbel_tau,
+                           int trajectory_grafting, int horizon_steps,
+                           int obs_interval_s, int fit_queues);
+/* Scenario::custom_init (engine.hpp:28-32); n == 0 clears it. */
+int dtg_scenario_custom_init(dtg_scenario* sc, int n, const int* link,
+                             const double* pos);
+int dtg_scenario_n_links(const dtg_scenario* sc);
+int dtg_scenario_n_nodes(const dtg_scenario* sc);
+/* Scenario::n_agents (engine.cpp:139-147); -1 on error. */
+int dtg_scenario_n_agents(const dtg_scenario* sc);
+int dtg_scenario_links(const dtg_scenario* sc, int* from_node, int* to_node,
+                       double* length, int* kind);
+/* Successor CSR (succ_off: L + 1, succ: dtg_scenario_n_edges). */
+int dtg_scenario_n_edges(const dtg_scenario* sc);
+int dtg_scenario_csr(const dtg_scenario* sc, int* succ_off, int* succ);
+/* sample_parameters (network.cpp:203-236) with the default ParamRanges. */
+int dtg_scenario_sample_parameters(const dtg_scenario* sc, uint64_t seed,
+                                   int mean_mode, double* u, double* kappa,
+                                   double* beta, double* alpha, double* cost);
+/* seed_agents (engine.cpp:156-189). */
+int dtg_scenario_seed_agents(const dtg_scenario* sc, int* link, double* pos);
+/* steps_for_minutes (engine.cpp:149-154); -1 on error. */
+int dtg_steps_for_minutes(int delta_n, double tau, double minutes);
+
+/* simulate_forward for n_draws noise iterations of one scenario (draw d uses
+ * noise_iterations[d]; scenario-major outputs).  cum_per_step [D][T][L],
+ * link_final/pos_final [D][N]; states_link/states_pos [D][T][N] optional
+ * (ForwardOptions::record_states).  wall_seconds (optional): wall time. */
+int dtg_simulate_forward(dtg_scenario* sc, const double* u,
+                         const double* kappa, const double* beta,
+                         const double* alpha, const double* cost,
+                         uint64_t root_seed, int n_draws,
+                         const uint64_t* noise_iterations,
+                         double* cum_per_step, int* link_final,
+                         double* pos_final, int* states_link,
+                         double* states_pos, double* wall_seconds);
+
+/* simulate_gradient (Checkpointed) for n_draws draws with the linear +
+ * quadratic loss
+ *   loss = sum_k sum_j (ws[k,j] s_kj + qs[k,j] s_kj^2 / 2)
+ *        + sum_j (wc[j] c_j + qc[j] c_j^2 / 2) + sum_n wx[n] x_n(final)
+ * over snapshots s_k, cum_final c and final positions (any coefficient array
+ * may be NULL; ws/qs are K x L, shared by all draws).  Outputs per draw:
+ * loss[D], grads[D][5][L], snapshots[D][K][L], cum_final[D][L],
+ * link_final/pos_final[D][N] (optional). */
+int dtg_simulate_gradient(dtg_scenario* sc, const double* u,
+                          const double* kappa, const double* beta,
+                          const double* alpha, const double* cost,
+                          uint64_t root_seed, int n_draws,
+                          const uint64_t* noise_iterations, const double* ws,
+                          const double* qs, const double* wc, const double* qc,
+                          const double* wx, double* loss, double* grads,
+                          double* snapshots, double* cum_final,
+                          int* link_final, double* pos_final,
+                          double* wall_seconds);
+
+/* simulate_gradient with the calibration loss mse_loss_builder
+ * (optimization.cpp:84-101): observed link ids obs_ids[n_obs], observations
+ * obs_values [K_obs][n_obs] in vehicles. */
+int dtg_simulate_gradient_mse(dtg_scenario* sc, const double* u,
+                              const double* kappa, const double* beta,
+                              const double* alpha, const double* cost,
+                              uint64_t root_seed, int n_draws,
+                              const uint64_t* noise_iterations, int n_obs,
+                              const int* obs_ids, int k_obs,
+                              const double* obs_values, double* loss,
+                              double* grads);
+
+/* Device context a scenario uses (for dtg_set_stream / dtg_last_launches);
+ * NULL before the first simulate call. */
+dtg_ctx* dtg_scenario_ctx(dtg_scenario* sc);
+const char* dtg_scenario_last_error(const dtg_scenario* sc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DTG_H */

@@ -1,0 +1,127 @@
+"""ctypes bindings of the C-ABI in include/dtg.h (libdtg.so, built in-tree).
+
+Loading fails loudly when the native library is missing: there is no CPU
+fallback for the hot path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdtg.so")
+
+DTG_OK = 0
+DTG_ERR_RUNTIME = 1
+DTG_ERR_CONFIG = 2
+DTG_ERR_DIVERGENCE = 3
+DTG_ERR_CUDA = 4
+DTG_ERR_UNSUPPORTED = 5
+
+
+class DtgError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[dtg code {code}] {msg}")
+        self.code = code
+
+
+class UnsupportedError(DtgError):
+    pass
+
+
+class ConfigError(DtgError):
+    pass
+
+
+def raise_for(code: int, msg: str):
+    if code == DTG_OK:
+        return
+    cls = {DTG_ERR_UNSUPPORTED: UnsupportedError, DTG_ERR_CONFIG: ConfigError}.get(code, DtgError)
+    raise cls(code, msg)
+
+
+class SimConfig(C.Structure):
+    _fields_ = [("delta_n", C.c_int), ("tau", C.c_double), ("sentinel", C.c_double),
+                ("gumbel_tau", C.c_double), ("trajectory_grafting", C.c_int)]
+
+
+class NetDesc(C.Structure):
+    _fields_ = [("n_links", C.c_int), ("succ_off", C.c_void_p), ("succ", C.c_void_p), ("length", C.c_void_p)]
+
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
+vp = C.c_void_p
+u64 = C.c_uint64
+i32 = C.c_int
+
+# (name, restype, argtypes) for every symbol declared in include/dtg.h
+SIGNATURES = [
+    ("dtg_create", i32, [C.POINTER(NetDesc), C.POINTER(SimConfig), i32, i32, i32, C.POINTER(vp)]),
+    ("dtg_destroy", None, [vp]),
+    ("dtg_last_error", C.c_char_p, [vp]),
+    ("dtg_set_stream", i32, [vp, vp]),
+    ("dtg_set_graphs", i32, [vp, i32]),
+    ("dtg_set_params", i32, [vp, i32, _dp, _dp, _dp, _dp, _dp]),
+    ("dtg_set_state", i32, [vp, i32, _ip, _dp]),
+    ("dtg_set_noise", i32, [vp, i32, u64, u64]),
+    ("dtg_forward", i32, [vp, i32, i32, i32]),
+    ("dtg_sync", i32, [vp]),
+    ("dtg_debug_force_slow_path", i32, [vp, i32]),
+    ("dtg_read_cum", i32, [vp, i32, _dp]),
+    ("dtg_read_state", i32, [vp, i32, i32, _ip, _dp]),
+    ("dtg_n_snapshots", i32, [vp]),
+    ("dtg_backward", i32, [vp, vp, vp, vp, _dp]),
+    ("dtg_backward_device", i32, [vp, vp, vp, vp, vp]),
+    ("dtg_device_cum", vp, [vp]),
+    ("dtg_last_launches", C.c_int64, [vp]),
+    ("dtg_scenario_from_links", vp, [i32, i32, _ip, _ip, _dp, _ip]),
+    ("dtg_scenario_grid", vp, [i32, C.c_double, u64, C.c_double]),
+    ("dtg_scenario_tntp", vp, [C.c_char_p, C.c_double, u64, C.c_double]),
+    ("dtg_scenario_free", None, [vp]),
+    ("dtg_scenario_configure", i32, [vp, i32, i32, C.c_double, C.c_double, i32, i32, i32, i32]),
+    ("dtg_scenario_custom_init", i32, [vp, i32, _ip, _dp]),
+    ("dtg_scenario_n_links", i32, [vp]),
+    ("dtg_scenario_n_nodes", i32, [vp]),
+    ("dtg_scenario_n_agents", i32, [vp]),
+    ("dtg_scenario_links", i32, [vp, _ip, _ip, _dp, _ip]),
+    ("dtg_scenario_n_edges", i32, [vp]),
+    ("dtg_scenario_csr", i32, [vp, _ip, _ip]),
+    ("dtg_scenario_sample_parameters", i32, [vp, u64, i32, _dp, _dp, _dp, _dp, _dp]),
+    ("dtg_scenario_seed_agents", i32, [vp, _ip, _dp]),
+    ("dtg_steps_for_minutes", i32, [i32, C.c_double, C.c_double]),
+    ("dtg_simulate_forward", i32, [vp, _dp, _dp, _dp, _dp, _dp, u64, i32, _u64p, vp, vp, vp, vp, vp, vp]),
+    ("dtg_simulate_gradient", i32, [vp, _dp, _dp, _dp, _dp, _dp, u64, i32, _u64p,
+                                    vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    ("dtg_simulate_gradient_mse", i32, [vp, _dp, _dp, _dp, _dp, _dp, u64, i32, _u64p,
+                                        i32, _ip, i32, _dp, vp, vp]),
+    ("dtg_scenario_ctx", vp, [vp]),
+    ("dtg_scenario_last_error", C.c_char_p, [vp]),
+]
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libdtg.so (raises if it was not built: no silent fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"native library {LIB_PATH} is missing; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (nvcc, sm_100a)")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def ptr(a):
+    """ctypes void* of a numpy array (or None)."""
+    return None if a is None else a.ctypes.data_as(C.c_void_p)

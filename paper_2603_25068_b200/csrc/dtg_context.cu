@@ -1,0 +1,668 @@
+// Level-1 C-ABI: the device engine context (include/dtg.h).
+//
+// Owns all device memory for B scenarios, the CUDA stream and the cached
+// CUDA graphs of the whole T-step forward and reverse sweeps (one graph launch
+// per simulate call instead of 4T / 8T kernel launches).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dtg.h"
+#include "dtg_kernels.h"
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Unsupported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                  \
+  do {                                                                         \
+    cudaError_t e_ = (x);                                                      \
+    if (e_ != cudaSuccess)                                                     \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  std::size_t n = 0;
+  void alloc(std::size_t count) {
+    release();
+    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  bool ensure(std::size_t count) {
+    if (count <= n) return false;
+    alloc(count);
+    return true;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+}  // namespace
+
+struct dtg_ctx {
+  int L = 0, N = 0, B = 0, maxdeg = 1;
+  dtg_sim_config cfg{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool graphs = true;
+  int force_slow = 0;
+  std::string err;
+  // static network
+  DevBuf<int> succ_off, succ, pred_off, pred, pred_pos;
+  DevBuf<double> len, thr, ctr, sc;
+  // parameters / seeds
+  DevBuf<double> params;  // [5][B][L]
+  DevBuf<double> derived; // [3][B][L]
+  DevBuf<std::uint64_t> seeds;  // [2][B]
+  std::vector<std::uint64_t> h_seeds;
+  std::vector<char> have_params, have_state;
+  // initial state
+  DevBuf<double> pos0, q0;
+  DevBuf<int> aid0, lnk0, off0;
+  // history
+  int S = 0, H = 0;
+  DevBuf<double> pos, qh, cumh;
+  DevBuf<int> aid, lnk, off;
+  // scratch
+  DevBuf<double> x1, tail;
+  DevBuf<int> choice, won, qn, nA, win, dep, newcnt, a0, errf;
+  DevBuf<unsigned char> vac;
+  // adjoint
+  DevBuf<double> cbar, qbar, qtot, lbar_row, prio_bar, vbar, lbar_a0, cu, cg,
+      grads, xbar;
+  DevBuf<double> snap_seed, cum_seed, x_seed;
+  DevBuf<unsigned long long> sort_scratch;
+  DevBuf<int> tmp_link;
+  DevBuf<double> tmp_pos;
+  // last run
+  int last_T = -1, last_spi = 1, last_ckpt = 0, last_K = 0;
+  bool pending = false;
+  std::int64_t launches = 0;
+  // graphs
+  cudaGraphExec_t fwd_exec = nullptr, bwd_exec = nullptr;
+  long long fwd_key = -1, bwd_key = -1;
+
+  dtg::DevView view() const {
+    dtg::DevView d{};
+    d.L = L;
+    d.N = N;
+    d.B = B;
+    d.S = S;
+    d.maxdeg = maxdeg;
+    d.delta_n = cfg.delta_n;
+    d.tg = cfg.trajectory_grafting ? 1 : 0;
+    d.M = cfg.sentinel;
+    d.dt = cfg.tau * cfg.delta_n;
+    d.kinv = 1.0 / cfg.gumbel_tau;
+    d.succ_off = succ_off.p;
+    d.succ = succ.p;
+    d.pred_off = pred_off.p;
+    d.pred = pred.p;
+    d.pred_pos = pred_pos.p;
+    d.len = len.p;
+    d.thr = thr.p;
+    d.ctr = ctr.p;
+    d.sc = sc.p;
+    const std::size_t BL = static_cast<std::size_t>(B) * L;
+    d.u = params.p;
+    d.kappa = params.p + BL;
+    d.beta = params.p + 2 * BL;
+    d.alpha = params.p + 3 * BL;
+    d.cost = params.p + 4 * BL;
+    d.jam = derived.p;
+    d.dxf = derived.p + BL;
+    d.pref = derived.p + 2 * BL;
+    d.seed_link = seeds.p;
+    d.seed_merge = seeds.p + B;
+    d.pos = pos.p;
+    d.aid = aid.p;
+    d.lnk = lnk.p;
+    d.off = off.p;
+    d.qh = qh.p;
+    d.cumh = cumh.p;
+    d.x1 = x1.p;
+    d.choice = choice.p;
+    d.won = won.p;
+    d.qn = qn.p;
+    d.nA = nA.p;
+    d.tail = tail.p;
+    d.win = win.p;
+    d.vac = vac.p;
+    d.dep = dep.p;
+    d.newcnt = newcnt.p;
+    d.a0 = a0.p;
+    d.err = errf.p;
+    d.cbar = cbar.p;
+    d.qbar = qbar.p;
+    d.qtot = qtot.p;
+    d.lbar_row = lbar_row.p;
+    d.prio_bar = prio_bar.p;
+    d.vbar = vbar.p;
+    d.lbar_a0 = lbar_a0.p;
+    d.cu = cu.p;
+    d.cg = cg.p;
+    d.grads = grads.p;
+    return d;
+  }
+
+  void drop_graphs() {
+    if (fwd_exec) cudaGraphExecDestroy(fwd_exec);
+    if (bwd_exec) cudaGraphExecDestroy(bwd_exec);
+    fwd_exec = bwd_exec = nullptr;
+    fwd_key = bwd_key = -1;
+  }
+
+  ~dtg_ctx() {
+    drop_graphs();
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  void ensure_history(int T, int ckpt) {
+    const int s_need = ckpt ? T + 1 : 2;
+    const int h_need = T + 1;
+    bool realloc = false;
+    if (s_need > S) {
+      const std::size_t BN = static_cast<std::size_t>(B) * N;
+      pos.alloc(BN * s_need);
+      aid.alloc(BN * s_need);
+      lnk.alloc(BN * s_need);
+      off.alloc(static_cast<std::size_t>(B) * (L + 1) * s_need);
+      S = s_need;
+      realloc = true;
+    }
+    if (h_need > H) {
+      qh.alloc(static_cast<std::size_t>(B) * L * h_need);
+      cumh.alloc(static_cast<std::size_t>(B) * L * h_need);
+      H = h_need;
+      realloc = true;
+    }
+    if (realloc) drop_graphs();
+  }
+
+  // Wait for the stream and turn device error flags into exceptions.
+  void sync_check() {
+    CK(cudaStreamSynchronize(stream));
+    if (!pending) return;
+    pending = false;
+    std::vector<int> e(B);
+    CK(cudaMemcpy(e.data(), errf.p, sizeof(int) * B, cudaMemcpyDeviceToHost));
+    for (int b = 0; b < B; ++b) {
+      if (e[b] & dtg::kErrCandOverflow)
+        throw Unsupported("more than 32 merge candidates for one link in one step (scenario " +
+                          std::to_string(b) + ")");
+      if (e[b] & dtg::kErrZeroAlpha)
+        throw Unsupported("zero merge priority (alpha) on a candidate link is not supported");
+      if (e[b] & dtg::kErrConservation)
+        throw std::runtime_error("agent conservation violated on the device (scenario " +
+                                 std::to_string(b) + ")");
+    }
+  }
+};
+
+namespace {
+
+int fail(dtg_ctx* c, int code, const std::string& msg) {
+  if (c)
+    c->err = msg;
+  else
+    g_create_error = msg;
+  return code;
+}
+
+template <class F>
+int guarded(dtg_ctx* c, F&& f) {
+  try {
+    f();
+    return DTG_OK;
+  } catch (const CudaError& e) {
+    return fail(c, DTG_ERR_CUDA, e.what());
+  } catch (const Unsupported& e) {
+    return fail(c, DTG_ERR_UNSUPPORTED, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(c, DTG_ERR_CONFIG, e.what());
+  } catch (const std::exception& e) {
+    return fail(c, DTG_ERR_RUNTIME, e.what());
+  }
+}
+
+template <class T>
+void h2d(DevBuf<T>& dst, const std::vector<T>& src, cudaStream_t st) {
+  dst.alloc(src.size());
+  if (!src.empty())
+    CK(cudaMemcpyAsync(dst.p, src.data(), src.size() * sizeof(T),
+                       cudaMemcpyHostToDevice, st));
+}
+
+// Link-segmented slot layout of one compact state (see dtg_device.cuh).
+void build_layout(int N, int L, const int* link, const double* pos,
+                  const std::vector<double>& length, std::vector<double>& ps,
+                  std::vector<int>& aid, std::vector<int>& lnk,
+                  std::vector<int>& off, std::vector<double>& q0) {
+  std::vector<int> cnt(L, 0);
+  for (int i = 0; i < N; ++i) {
+    if (link[i] < 0 || link[i] >= L)
+      throw std::runtime_error("agent placed on a link that does not exist");
+    if (!(pos[i] >= dtg::kValidThr))
+      throw Unsupported("agent " + std::to_string(i) + " position " +
+                        std::to_string(pos[i]) +
+                        " is below the validity threshold -0.01");
+    ++cnt[link[i]];
+  }
+  off.assign(L + 1, 0);
+  for (int j = 0; j < L; ++j) off[j + 1] = off[j] + cnt[j];
+  std::vector<int> cur(off.begin(), off.end() - 1);
+  aid.assign(N, 0);
+  for (int i = 0; i < N; ++i) aid[cur[link[i]]++] = i;  // ascending id per link
+  for (int j = 0; j < L; ++j) {
+    auto b = aid.begin() + off[j], e = aid.begin() + off[j + 1];
+    const bool sorted = std::is_sorted(b, e, [&](int x, int y) { return pos[x] > pos[y]; });
+    if (!sorted)  // stable: ties keep ascending id (argsort_desc, tensor.cpp:672-680)
+      std::stable_sort(b, e, [&](int x, int y) { return pos[x] > pos[y]; });
+  }
+  ps.resize(N);
+  lnk.resize(N);
+  q0.assign(L, 0.0);
+  for (int j = 0; j < L; ++j)
+    for (int k = off[j]; k < off[j + 1]; ++k) {
+      ps[k] = pos[aid[k]];
+      lnk[k] = j;
+      if (ps[k] >= 0.5 * length[j]) q0[j] += 1.0;  // initial_counts, engine.cpp:127-135
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
+               int n_scenarios, int max_steps, dtg_ctx** out) {
+  *out = nullptr;
+  dtg_ctx* c = new dtg_ctx;
+  const int rc = guarded(nullptr, [&] {
+    if (!net || !cfg) throw std::invalid_argument("dtg_create: null network or config");
+    const int L = net->n_links;
+    if (L <= 0) throw std::invalid_argument("network has no links");
+    if (n_agents <= 0) throw std::invalid_argument("no agents");
+    if (n_scenarios <= 0) throw std::invalid_argument("n_scenarios must be >= 1");
+    if (cfg->delta_n < 1) throw std::invalid_argument("platoon size must be >= 1");
+    if (!(cfg->gumbel_tau > 0.0)) throw std::invalid_argument("gumbel_tau must be > 0");
+    c->L = L;
+    c->N = n_agents;
+    c->B = n_scenarios;
+    c->cfg = *cfg;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    // CSR + predecessor CSR with the successor position of each edge
+    std::vector<int> so(net->succ_off, net->succ_off + L + 1);
+    const int E = so[L];
+    if (so[0] != 0) throw std::invalid_argument("succ_off[0] must be 0");
+    std::vector<int> su(net->succ, net->succ + E);
+    std::vector<int> pcnt(L + 1, 0);
+    for (int i = 0; i < L; ++i) {
+      if (so[i + 1] < so[i]) throw std::invalid_argument("succ_off not monotone");
+      const int deg = so[i + 1] - so[i];
+      c->maxdeg = std::max(c->maxdeg, deg);
+      for (int e = so[i]; e < so[i + 1]; ++e) {
+        if (su[e] < 0 || su[e] >= L || su[e] == i)
+          throw std::invalid_argument("successor out of range or self loop");
+        if (e > so[i] && su[e] <= su[e - 1])
+          throw std::invalid_argument("successors must be strictly ascending");
+        ++pcnt[su[e] + 1];
+      }
+    }
+    if (c->maxdeg > dtg::kMaxDeg)
+      throw Unsupported("link out-degree " + std::to_string(c->maxdeg) + " exceeds " +
+                        std::to_string(dtg::kMaxDeg));
+    for (int j = 0; j < L; ++j) pcnt[j + 1] += pcnt[j];
+    std::vector<int> pr(E), pp(E), fill(pcnt.begin(), pcnt.end() - 1);
+    for (int i = 0; i < L; ++i)  // ascending predecessor id per link
+      for (int e = so[i]; e < so[i + 1]; ++e) {
+        const int q = fill[su[e]]++;
+        pr[q] = i;
+        pp[q] = e - so[i];
+      }
+    std::vector<double> ln(net->length, net->length + L), th(L), ct(L), sc(L);
+    for (int j = 0; j < L; ++j) {
+      if (!(0.5 * ln[j] > 0.0 && 0.5 * ln[j] < ln[j]))  // observation.cpp:194-195
+        throw std::runtime_error("midpoint_count: counter position outside (0, L)");
+      th[j] = ln[j] - dtg::kArrivalTol;  // node_model.cpp:69-70
+      ct[j] = 0.5 * ln[j];               // engine.cpp:46-47
+      sc[j] = 5.0 / ln[j];               // observation.cpp:199
+    }
+    cudaStream_t st = c->stream;
+    h2d(c->succ_off, so, st);
+    h2d(c->succ, su, st);
+    h2d(c->pred_off, pcnt, st);
+    h2d(c->pred, pr, st);
+    h2d(c->pred_pos, pp, st);
+    h2d(c->len, ln, st);
+    h2d(c->thr, th, st);
+    h2d(c->ctr, ct, st);
+    h2d(c->sc, sc, st);
+    const std::size_t B = c->B, N = c->N, BL = B * L, BN = B * N;
+    c->params.alloc(5 * BL);
+    c->derived.alloc(3 * BL);
+    c->seeds.alloc(2 * B);
+    c->h_seeds.assign(2 * B, 0);
+    c->have_params.assign(B, 0);
+    c->have_state.assign(B, 0);
+    for (int b = 0; b < c->B; ++b) {  // default noise: RngStream(0), iteration 0
+      const std::uint64_t it = dtg::rng_fork(dtg::rng_fork(0, dtg::lane::kIteration), 0);
+      c->h_seeds[b] = dtg::rng_fork(it, dtg::lane::kGumbelLink);
+      c->h_seeds[B + b] = dtg::rng_fork(it, dtg::lane::kGumbelMerge);
+    }
+    c->pos0.alloc(BN);
+    c->aid0.alloc(BN);
+    c->lnk0.alloc(BN);
+    c->off0.alloc(B * (L + 1));
+    c->q0.alloc(BL);
+    c->x1.alloc(BN);
+    c->choice.alloc(BN);
+    c->won.alloc(BN);
+    c->qn.alloc(BL);
+    c->nA.alloc(BL);
+    c->tail.alloc(BL);
+    c->win.alloc(BL);
+    c->vac.alloc(BL);
+    c->dep.alloc(BL);
+    c->newcnt.alloc(BL);
+    c->a0.alloc(B);
+    c->errf.alloc(B);
+    c->tmp_link.alloc(BN);
+    c->tmp_pos.alloc(BN);
+    c->ensure_history(std::max(1, max_steps), 0);
+    CK(cudaStreamSynchronize(st));
+  });
+  if (rc != DTG_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return DTG_OK;
+}
+
+void dtg_destroy(dtg_ctx* c) { delete c; }
+
+const char* dtg_last_error(const dtg_ctx* c) {
+  return c ? c->err.c_str() : g_create_error.c_str();
+}
+
+int dtg_set_stream(dtg_ctx* c, void* s) {
+  return guarded(c, [&] {
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->own_stream) CK(cudaStreamDestroy(c->stream));
+    c->own_stream = s == nullptr;
+    if (s)
+      c->stream = static_cast<cudaStream_t>(s);
+    else
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->drop_graphs();
+  });
+}
+
+int dtg_set_graphs(dtg_ctx* c, int enabled) {
+  c->graphs = enabled != 0;
+  return DTG_OK;
+}
+
+int dtg_set_params(dtg_ctx* c, int scenario, const double* u, const double* kappa,
+                   const double* beta, const double* alpha, const double* cost) {
+  return guarded(c, [&] {
+    if (scenario >= c->B) throw std::invalid_argument("scenario index out of range");
+    const double* src[5] = {u, kappa, beta, alpha, cost};
+    const std::size_t L = c->L, BL = static_cast<std::size_t>(c->B) * L;
+    for (int b = 0; b < c->B; ++b) {
+      if (scenario >= 0 && b != scenario) continue;
+      for (int q = 0; q < 5; ++q)
+        CK(cudaMemcpyAsync(c->params.p + q * BL + b * L, src[q], L * sizeof(double),
+                           cudaMemcpyHostToDevice, c->stream));
+      c->have_params[b] = 1;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int dtg_set_state(dtg_ctx* c, int scenario, const int* link, const double* pos) {
+  return guarded(c, [&] {
+    if (scenario >= c->B) throw std::invalid_argument("scenario index out of range");
+    std::vector<double> length(c->L);
+    CK(cudaMemcpy(length.data(), c->len.p, sizeof(double) * c->L, cudaMemcpyDeviceToHost));
+    std::vector<double> ps, q0;
+    std::vector<int> aid, lnk, off;
+    build_layout(c->N, c->L, link, pos, length, ps, aid, lnk, off, q0);
+    const std::size_t N = c->N, L = c->L;
+    for (int b = 0; b < c->B; ++b) {
+      if (scenario >= 0 && b != scenario) continue;
+      CK(cudaMemcpyAsync(c->pos0.p + b * N, ps.data(), N * 8, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->aid0.p + b * N, aid.data(), N * 4, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->lnk0.p + b * N, lnk.data(), N * 4, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->off0.p + b * (L + 1), off.data(), (L + 1) * 4,
+                         cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->q0.p + b * L, q0.data(), L * 8, cudaMemcpyHostToDevice, c->stream));
+      c->have_state[b] = 1;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int dtg_set_noise(dtg_ctx* c, int scenario, uint64_t root_seed, uint64_t noise_iteration) {
+  return guarded(c, [&] {
+    if (scenario >= c->B) throw std::invalid_argument("scenario index out of range");
+    // engine.cpp:49 then node_model.cpp:65 / :114
+    const std::uint64_t it =
+        dtg::rng_fork(dtg::rng_fork(root_seed, dtg::lane::kIteration), noise_iteration);
+    for (int b = 0; b < c->B; ++b) {
+      if (scenario >= 0 && b != scenario) continue;
+      c->h_seeds[b] = dtg::rng_fork(it, dtg::lane::kGumbelLink);
+      c->h_seeds[c->B + b] = dtg::rng_fork(it, dtg::lane::kGumbelMerge);
+    }
+  });
+}
+
+int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
+  return guarded(c, [&] {
+    if (T < 0) throw std::invalid_argument("negative horizon");
+    if (spi < 1)
+      throw std::runtime_error("observation interval must be a positive multiple of the time step");
+    for (int b = 0; b < c->B; ++b)
+      if (!c->have_params[b] || !c->have_state[b])
+        throw std::invalid_argument("scenario " + std::to_string(b) +
+                                    " has no parameters or initial state");
+    c->ensure_history(T, checkpoint);
+    cudaStream_t st = c->stream;
+    CK(cudaMemcpyAsync(c->seeds.p, c->h_seeds.data(), sizeof(std::uint64_t) * 2 * c->B,
+                       cudaMemcpyHostToDevice, st));
+    const dtg::DevView d = c->view();
+    const std::size_t BN = static_cast<std::size_t>(c->B) * c->N;
+    const std::size_t BL = static_cast<std::size_t>(c->B) * c->L;
+    auto body = [&] {
+      dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
+      CK(cudaMemcpyAsync(c->pos.p, c->pos0.p, BN * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->aid.p, c->aid0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->lnk.p, c->lnk0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->off.p, c->off0.p, static_cast<std::size_t>(c->B) * (c->L + 1) * 4,
+                         cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->qh.p, c->q0.p, BL * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemsetAsync(c->cumh.p, 0, BL * 8, st));
+      CK(cudaMemsetAsync(c->errf.p, 0, sizeof(int) * c->B, st));
+      for (int t = 0; t < T; ++t)
+        dtg::launch_step_forward(d, t, t % c->S, (t + 1) % c->S, st);
+    };
+    const long long key = (static_cast<long long>(T) << 20) ^ (c->S << 1) ^ 1;
+    if (c->graphs && T > 0) {
+      if (c->fwd_key != key || !c->fwd_exec) {
+        if (c->fwd_exec) cudaGraphExecDestroy(c->fwd_exec);
+        c->fwd_exec = nullptr;
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        body();
+        CK(cudaStreamEndCapture(st, &g));
+        CK(cudaGraphInstantiate(&c->fwd_exec, g, 0));
+        cudaGraphDestroy(g);
+        c->fwd_key = key;
+      }
+      CK(cudaGraphLaunch(c->fwd_exec, st));
+    } else {
+      body();
+      CK(cudaGetLastError());
+    }
+    c->launches = 1 + static_cast<std::int64_t>(T) * dtg::kLaunchesPerForwardStep;
+    c->last_T = T;
+    c->last_spi = spi;
+    c->last_ckpt = checkpoint;
+    c->last_K = T / spi;
+    c->pending = true;
+  });
+}
+
+int dtg_sync(dtg_ctx* c) {
+  return guarded(c, [&] { c->sync_check(); });
+}
+
+int dtg_read_cum(dtg_ctx* c, int scenario, double* cum) {
+  return guarded(c, [&] {
+    if (scenario < 0 || scenario >= c->B) throw std::invalid_argument("scenario index out of range");
+    c->sync_check();
+    if (c->last_T < 0) throw std::runtime_error("no forward run");
+    if (c->last_T == 0) return;
+    const std::size_t L = c->L, BL = static_cast<std::size_t>(c->B) * L;
+    CK(cudaMemcpy2D(cum, L * 8, c->cumh.p + BL + scenario * L, BL * 8, L * 8, c->last_T,
+                    cudaMemcpyDeviceToHost));
+  });
+}
+
+int dtg_read_state(dtg_ctx* c, int scenario, int step, int* link, double* pos) {
+  return guarded(c, [&] {
+    if (scenario < 0 || scenario >= c->B) throw std::invalid_argument("scenario index out of range");
+    c->sync_check();
+    const int T = c->last_T;
+    if (T < 0) throw std::runtime_error("no forward run");
+    if (step < 0) step = T;
+    if (step > T || (!c->last_ckpt && step < T - 1))
+      throw std::invalid_argument("step not kept (run dtg_forward with checkpoint=1)");
+    const dtg::DevView d = c->view();
+    dtg::launch_gather_state(d, step % c->S, c->tmp_link.p, c->tmp_pos.p, c->stream);
+    CK(cudaGetLastError());
+    const std::size_t N = c->N;
+    CK(cudaMemcpyAsync(link, c->tmp_link.p + scenario * N, N * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(pos, c->tmp_pos.p + scenario * N, N * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int dtg_n_snapshots(const dtg_ctx* c) { return c->last_T < 0 ? 0 : c->last_K; }
+
+const double* dtg_device_cum(const dtg_ctx* c) { return c->cumh.p; }
+
+int64_t dtg_last_launches(const dtg_ctx* c) { return c->launches; }
+
+static void run_backward(dtg_ctx* c, const double* snap, const double* cum, const double* xs,
+                         cudaMemcpyKind kind) {
+  if (c->last_T < 0 || !c->last_ckpt)
+    throw std::runtime_error("dtg_backward needs a preceding dtg_forward with checkpoint=1");
+  const int T = c->last_T, K = c->last_K, spi = c->last_spi;
+  const std::size_t B = c->B, L = c->L, N = c->N;
+  cudaStream_t st = c->stream;
+  bool changed = false;
+  changed |= c->snap_seed.ensure(std::max<std::size_t>(1, B * K * L));
+  changed |= c->cum_seed.ensure(B * L);
+  changed |= c->x_seed.ensure(B * N);
+  changed |= c->cbar.ensure(B * L);
+  changed |= c->qbar.ensure(B * L);
+  changed |= c->qtot.ensure(B * L);
+  changed |= c->lbar_row.ensure(B * N);
+  changed |= c->prio_bar.ensure(B * N);
+  changed |= c->vbar.ensure(B * N * c->maxdeg);
+  changed |= c->lbar_a0.ensure(B * c->maxdeg);
+  changed |= c->cu.ensure(B * N);
+  changed |= c->cg.ensure(B * N);
+  changed |= c->grads.ensure(B * 5 * L);
+  changed |= c->xbar.ensure(2 * B * N);
+  changed |= c->sort_scratch.ensure(2 * B * N + 2);
+  if (changed) c->drop_graphs();
+  auto up = [&](double* dst, const double* src, std::size_t n) {
+    if (src)
+      CK(cudaMemcpyAsync(dst, src, n * 8, kind, st));
+    else
+      CK(cudaMemsetAsync(dst, 0, n * 8, st));
+  };
+  if (K) up(c->snap_seed.p, snap, B * K * L);
+  up(c->cum_seed.p, cum, B * L);
+  up(c->x_seed.p, xs, B * N);
+  const dtg::DevView d = c->view();
+  double* xb[2] = {c->xbar.p, c->xbar.p + B * N};
+  auto body = [&] {
+    dtg::launch_adj_init(d, T % c->S, c->x_seed.p, xb[T & 1], c->cum_seed.p, st);
+    for (int t = T - 1; t >= 0; --t) {
+      const int snap_k = ((t + 1) % spi == 0) ? (t + 1) / spi - 1 : -1;
+      dtg::launch_step_backward(d, t, t % c->S, (t + 1) % c->S, xb[(t + 1) & 1], xb[t & 1],
+                                c->snap_seed.p, snap_k, K, c->sort_scratch.p, c->force_slow, st);
+    }
+  };
+  const long long key = (static_cast<long long>(T) << 24) ^ (static_cast<long long>(spi) << 2) ^
+                        (c->force_slow << 1) ^ static_cast<long long>(c->S << 12);
+  if (c->graphs && T > 0) {
+    if (c->bwd_key != key || !c->bwd_exec) {
+      if (c->bwd_exec) cudaGraphExecDestroy(c->bwd_exec);
+      c->bwd_exec = nullptr;
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      body();
+      CK(cudaStreamEndCapture(st, &g));
+      CK(cudaGraphInstantiate(&c->bwd_exec, g, 0));
+      cudaGraphDestroy(g);
+      c->bwd_key = key;
+    }
+    CK(cudaGraphLaunch(c->bwd_exec, st));
+  } else {
+    body();
+    CK(cudaGetLastError());
+  }
+  c->launches = 2 + static_cast<std::int64_t>(T) * dtg::kLaunchesPerBackwardStep;
+  c->pending = true;
+}
+
+int dtg_backward(dtg_ctx* c, const double* snap, const double* cum, const double* xs,
+                 double* grads) {
+  return guarded(c, [&] {
+    c->sync_check();
+    run_backward(c, snap, cum, xs, cudaMemcpyHostToDevice);
+    const std::size_t n = static_cast<std::size_t>(c->B) * 5 * c->L;
+    CK(cudaMemcpyAsync(grads, c->grads.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync_check();
+  });
+}
+
+int dtg_backward_device(dtg_ctx* c, const double* snap, const double* cum, const double* xs,
+                        double* d_grads) {
+  return guarded(c, [&] {
+    run_backward(c, snap, cum, xs, cudaMemcpyDeviceToDevice);
+    const std::size_t n = static_cast<std::size_t>(c->B) * 5 * c->L;
+    CK(cudaMemcpyAsync(d_grads, c->grads.p, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  });
+}
+
+int dtg_debug_force_slow_path(dtg_ctx* c, int on) {
+  c->force_slow = on ? 1 : 0;
+  c->drop_graphs();
+  return DTG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,958 @@
+// Host side of the drop-in: the reference's network / scenario / simulate API
+// (include/dtg_engine.hpp) in C++, driving the device engine through the
+// level-1 C-ABI, plus the level-2 flat C-ABI (include/dtg.h) over it.
+//
+// Built with -ffp-contract=off: sample_parameters' lo + (hi - lo) * u must not
+// be contracted into an FMA or parameters differ from the reference in the
+// last bit.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <map>
+#include <memory>
+#include <queue>
+#include <set>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dtg.h"
+#include "../../include/dtg_engine.hpp"
+
+namespace dtg {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+struct ApiError : std::runtime_error {
+  int code;
+  ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void check(dtg_ctx* c, int rc) {
+  if (rc != DTG_OK) throw ApiError(rc, dtg_last_error(c));
+}
+
+std::string trim(const std::string& s) {
+  const auto b = s.find_first_not_of(" \t\r\n");
+  if (b == std::string::npos) return "";
+  const auto e = s.find_last_not_of(" \t\r\n");
+  return s.substr(b, e - b + 1);
+}
+
+[[noreturn]] void parse_fail(int line_no, const std::string& msg) {
+  throw std::runtime_error("tntp parse error at line " + std::to_string(line_no) +
+                           ": " + msg);
+}
+
+}  // namespace
+
+// ---- network ------------------------------------------------------------------
+int Network::n_physical_links() const {
+  int n = 0;
+  for (const auto& l : links) n += (l.kind == LinkKind::Physical);
+  return n;
+}
+
+std::vector<int> Network::links_of_kind(LinkKind k) const {
+  std::vector<int> out;
+  for (const auto& l : links)
+    if (l.kind == k) out.push_back(l.id);
+  return out;
+}
+
+std::vector<double> Network::lengths() const {
+  std::vector<double> out(links.size());
+  for (std::size_t i = 0; i < links.size(); ++i) out[i] = links[i].length;
+  return out;
+}
+
+// CSR form of build_adjacency (network.cpp:28-35) in O(L + E) instead of O(L^2).
+void Network::rebuild_csr() {
+  const int L = n_links();
+  std::map<int, std::vector<int>> by_from;
+  for (int j = 0; j < L; ++j) by_from[links[j].from_node].push_back(j);  // ascending j
+  succ_off.assign(L + 1, 0);
+  succ.clear();
+  for (int i = 0; i < L; ++i) {
+    auto it = by_from.find(links[i].to_node);
+    if (it != by_from.end())
+      for (int j : it->second)
+        if (j != i) succ.push_back(j);
+    succ_off[i + 1] = static_cast<int>(succ.size());
+  }
+}
+
+Network make_network(int n_nodes, std::vector<Link> links) {
+  Network net;
+  net.n_nodes = n_nodes;
+  net.n_physical_nodes = n_nodes;
+  net.links = std::move(links);
+  for (std::size_t i = 0; i < net.links.size(); ++i) net.links[i].id = static_cast<int>(i);
+  net.rebuild_csr();
+  return net;
+}
+
+Network grid_network(int n, double length) {
+  std::vector<Link> links;
+  auto push = [&](int a, int b) {
+    Link l;
+    l.from_node = a;
+    l.to_node = b;
+    l.length = length;
+    links.push_back(l);
+  };
+  for (int r = 0; r < n; ++r)
+    for (int c = 0; c < n; ++c) {
+      if (c + 1 < n) {
+        push(r * n + c, r * n + c + 1);
+        push(r * n + c + 1, r * n + c);
+      }
+      if (r + 1 < n) {
+        push(r * n + c, (r + 1) * n + c);
+        push((r + 1) * n + c, r * n + c);
+      }
+    }
+  return make_network(n * n, std::move(links));
+}
+
+// parse_tntp_text (network.cpp:58-118), same acceptance rules and messages.
+Network parse_tntp_text(const std::string& text, double length_unit_scale) {
+  std::istringstream in(text);
+  std::string line;
+  int line_no = 0, meta_nodes = -1, meta_links = -1;
+  bool in_meta = true;
+  Network net;
+  while (std::getline(in, line)) {
+    ++line_no;
+    std::string t = trim(line);
+    if (t.empty() || t[0] == '~') continue;
+    if (in_meta) {
+      if (t.rfind("<END OF METADATA>", 0) == 0) {
+        in_meta = false;
+        continue;
+      }
+      if (t[0] == '<') {
+        const auto close = t.find('>');
+        if (close == std::string::npos) parse_fail(line_no, "unterminated metadata tag");
+        const std::string key = t.substr(1, close - 1);
+        const std::string val = trim(t.substr(close + 1));
+        if (key == "NUMBER OF NODES") meta_nodes = std::stoi(val);
+        if (key == "NUMBER OF LINKS") meta_links = std::stoi(val);
+        continue;
+      }
+      in_meta = false;
+    }
+    if (t.back() != ';') parse_fail(line_no, "row does not end with ';'");
+    t.pop_back();
+    std::istringstream row(t);
+    std::vector<double> fields;
+    double v;
+    while (row >> v) fields.push_back(v);
+    if (!row.eof()) parse_fail(line_no, "non-numeric field");
+    if (fields.size() < 5) parse_fail(line_no, "expected at least 5 fields");
+    Link l;
+    l.id = net.n_links();
+    l.from_node = static_cast<int>(fields[0]) - 1;
+    l.to_node = static_cast<int>(fields[1]) - 1;
+    l.length = fields[3] * length_unit_scale;
+    if (l.from_node < 0 || l.to_node < 0) parse_fail(line_no, "node ids must be positive");
+    if (meta_nodes > 0 && (l.from_node >= meta_nodes || l.to_node >= meta_nodes))
+      parse_fail(line_no, "node id exceeds <NUMBER OF NODES>");
+    if (!(l.length > 0.0)) parse_fail(line_no, "non-positive link length");
+    net.links.push_back(l);
+  }
+  if (meta_nodes <= 0) throw std::runtime_error("tntp parse error: missing <NUMBER OF NODES>");
+  if (meta_links >= 0 && meta_links != net.n_links())
+    throw std::runtime_error("tntp parse error: <NUMBER OF LINKS> " + std::to_string(meta_links) +
+                             " does not match " + std::to_string(net.n_links()) + " data rows");
+  net.n_nodes = meta_nodes;
+  net.n_physical_nodes = meta_nodes;
+  net.rebuild_csr();
+  return net;
+}
+
+bool all_physical_reachable(const Network& net) {  // network.cpp:128-149 on the CSR
+  const int L = net.n_links();
+  std::vector<char> seen(L, 0);
+  std::queue<int> q;
+  for (const auto& l : net.links)
+    if (l.kind == LinkKind::VirtualInflow) {
+      seen[l.id] = 1;
+      q.push(l.id);
+    }
+  while (!q.empty()) {
+    const int i = q.front();
+    q.pop();
+    for (int e = net.succ_off[i]; e < net.succ_off[i + 1]; ++e)
+      if (!seen[net.succ[e]]) {
+        seen[net.succ[e]] = 1;
+        q.push(net.succ[e]);
+      }
+  }
+  for (const auto& l : net.links)
+    if (l.kind == LinkKind::Physical && !seen[l.id]) return false;
+  return true;
+}
+
+// attach_virtual_links (network.cpp:151-201).
+Network attach_virtual_links(const Network& physical, const RngStream& rng,
+                             double virtual_length) {
+  Network net = physical;
+  const RngStream coin = rng.fork(lane::kVirtualCoin);
+  std::vector<std::set<int>> neighbours(net.n_physical_nodes);
+  for (const auto& l : net.links) {
+    if (l.kind != LinkKind::Physical) continue;
+    neighbours[l.from_node].insert(l.to_node);
+    neighbours[l.to_node].insert(l.from_node);
+  }
+  int next_node = net.n_physical_nodes;
+  for (int node = 0; node < net.n_physical_nodes; ++node) {
+    const bool dead_end = neighbours[node].size() <= 1;
+    bool add_inflow = true, add_outflow = true;
+    if (!dead_end) {
+      if (coin.bits(static_cast<std::uint64_t>(node)) & 1)
+        add_outflow = false;
+      else
+        add_inflow = false;
+    }
+    if (add_inflow) {
+      Link l;
+      l.id = net.n_links();
+      l.from_node = next_node++;
+      l.to_node = node;
+      l.length = virtual_length;
+      l.kind = LinkKind::VirtualInflow;
+      net.links.push_back(l);
+    }
+    if (add_outflow) {
+      Link l;
+      l.id = net.n_links();
+      l.from_node = node;
+      l.to_node = next_node++;
+      l.length = virtual_length;
+      l.kind = LinkKind::VirtualOutflow;
+      net.links.push_back(l);
+    }
+  }
+  net.n_nodes = next_node;
+  net.rebuild_csr();
+  if (!all_physical_reachable(net))
+    throw std::runtime_error(
+        "virtual link construction left a physical link unreachable from every inflow link (seed " +
+        std::to_string(rng.seed()) + ")");
+  return net;
+}
+
+// sample_parameters (network.cpp:203-236).
+LinkParams sample_parameters(const Network& net, const ParamRanges& r, const RngStream& rng,
+                             bool mean_mode) {
+  auto chk = [](double lo, double hi, const char* name) {
+    if (!(lo <= hi)) throw std::runtime_error(std::string("empty parameter range for ") + name);
+  };
+  chk(r.u_lo, r.u_hi, "u");
+  chk(r.kappa_lo, r.kappa_hi, "kappa");
+  chk(r.beta_lo, r.beta_hi, "beta");
+  chk(r.alpha_lo, r.alpha_hi, "alpha");
+  const RngStream lane = rng.fork(lane::kParamSample);
+  const int L = net.n_links();
+  LinkParams p;
+  p.u.resize(L);
+  p.kappa.resize(L);
+  p.beta.resize(L);
+  p.alpha.resize(L);
+  p.cost.assign(L, 1.0);
+  for (int l = 0; l < L; ++l) {
+    if (mean_mode) {
+      p.u[l] = 0.5 * (r.u_lo + r.u_hi);
+      p.kappa[l] = 0.5 * (r.kappa_lo + r.kappa_hi);
+      p.beta[l] = 0.5 * (r.beta_lo + r.beta_hi);
+      p.alpha[l] = 0.5 * (r.alpha_lo + r.alpha_hi);
+    } else {
+      p.u[l] = lane.uniform_in(r.u_lo, r.u_hi, 0, l);
+      p.kappa[l] = lane.uniform_in(r.kappa_lo, r.kappa_hi, 1, l);
+      p.beta[l] = lane.uniform_in(r.beta_lo, r.beta_hi, 2, l);
+      p.alpha[l] = lane.uniform_in(r.alpha_lo, r.alpha_hi, 3, l);
+    }
+  }
+  return p;
+}
+
+// ---- scenario (engine.cpp:139-213) --------------------------------------------
+int Scenario::n_agents() const {
+  if (!custom_init.empty()) return static_cast<int>(custom_init.size());
+  if (cfg.delta_n < 1) throw std::runtime_error("platoon size must be >= 1");
+  if (n_vehicles % cfg.delta_n != 0)
+    throw std::runtime_error("vehicle count " + std::to_string(n_vehicles) +
+                             " is not divisible into platoons of " +
+                             std::to_string(cfg.delta_n));
+  return n_vehicles / cfg.delta_n;
+}
+
+int steps_for_minutes(const SimConfig& cfg, double minutes) {
+  const double steps = minutes * 60.0 / cfg.dt();
+  if (std::abs(steps - std::round(steps)) > 1e-9)
+    throw std::runtime_error("horizon must be a whole number of time steps");
+  return static_cast<int>(std::llround(steps));
+}
+
+InitialState seed_agents(const Scenario& s) {
+  InitialState init;
+  if (!s.custom_init.empty()) {
+    for (const auto& p : s.custom_init) {
+      init.link.push_back(p.link);
+      init.pos.push_back(p.pos);
+    }
+    return init;
+  }
+  const int n = s.n_agents();
+  const auto inflows = s.net.links_of_kind(LinkKind::VirtualInflow);
+  if (inflows.empty()) throw std::runtime_error("scenario network has no virtual inflow links");
+  const double spacing = s.cfg.delta_n / s.seeding_kappa;
+  const int n_in = static_cast<int>(inflows.size());
+  std::vector<int> rank(n_in, 0);
+  init.link.resize(n);
+  init.pos.resize(n);
+  for (int a = 0; a < n; ++a) {
+    const int q = a % n_in;
+    const int lid = inflows[q];
+    const double pos = s.net.links[lid].length - rank[q] * spacing;
+    if (pos < 0.0) {
+      const double need = rank[q] * spacing;
+      throw std::runtime_error("inflow queue does not fit: virtual link " + std::to_string(lid) +
+                               " needs length >= " + std::to_string(need) + " m");
+    }
+    init.link[a] = lid;
+    init.pos[a] = pos;
+    ++rank[q];
+  }
+  return init;
+}
+
+void fit_inflow_queues(Scenario& s) {
+  if (!s.custom_init.empty()) return;
+  const auto inflows = s.net.links_of_kind(LinkKind::VirtualInflow);
+  if (!inflows.empty()) {
+    const int n_in = static_cast<int>(inflows.size());
+    const int veh_per_inflow = (s.n_vehicles + n_in - 1) / n_in;
+    const double need = veh_per_inflow / s.seeding_kappa;
+    for (int q = 0; q < n_in; ++q) {
+      auto& link = s.net.links[inflows[q]];
+      link.length = std::max(link.length, need);
+    }
+  }
+  const double sink_need = s.n_vehicles / s.seeding_kappa;
+  for (int lid : s.net.links_of_kind(LinkKind::VirtualOutflow)) {
+    auto& link = s.net.links[lid];
+    link.length = std::max(link.length, sink_need);
+  }
+}
+
+// ---- device context cache ------------------------------------------------------
+namespace detail {
+
+struct CtxDeleter {
+  void operator()(dtg_ctx* c) const { dtg_destroy(c); }
+};
+
+struct CacheEntry {
+  std::unique_ptr<dtg_ctx, CtxDeleter> ctx;
+  std::vector<int> succ_off, succ;
+  std::vector<double> len;
+  SimConfig cfg;
+  int N = 0, B = 0;
+};
+
+thread_local std::vector<CacheEntry> g_cache;
+thread_local dtg_ctx* g_last_ctx = nullptr;
+
+dtg_ctx* context_for(const Scenario& s, int N, int B, int T) {
+  const std::vector<double> len = s.net.lengths();
+  for (auto& e : g_cache)
+    if (e.N == N && e.B == B && e.succ_off == s.net.succ_off && e.succ == s.net.succ &&
+        e.len == len && e.cfg.delta_n == s.cfg.delta_n && e.cfg.tau == s.cfg.tau &&
+        e.cfg.sentinel == s.cfg.sentinel && e.cfg.gumbel_tau == s.cfg.gumbel_tau &&
+        e.cfg.trajectory_grafting == s.cfg.trajectory_grafting)
+      return g_last_ctx = e.ctx.get();
+  if (g_cache.size() >= 4) g_cache.erase(g_cache.begin());
+  dtg_net_desc nd{s.net.n_links(), s.net.succ_off.data(), s.net.succ.data(), len.data()};
+  dtg_sim_config sc{s.cfg.delta_n, s.cfg.tau, s.cfg.sentinel, s.cfg.gumbel_tau,
+                    s.cfg.trajectory_grafting ? 1 : 0};
+  dtg_ctx* c = nullptr;
+  const int rc = dtg_create(&nd, &sc, N, B, std::max(T, 1), &c);
+  if (rc != DTG_OK) throw ApiError(rc, dtg_last_error(nullptr));
+  CacheEntry e;
+  e.ctx.reset(c);
+  e.succ_off = s.net.succ_off;
+  e.succ = s.net.succ;
+  e.len = len;
+  e.cfg = s.cfg;
+  e.N = N;
+  e.B = B;
+  g_cache.push_back(std::move(e));
+  return g_last_ctx = c;
+}
+
+}  // namespace detail
+
+namespace {
+
+int steps_per_interval(const Scenario& s) {  // make_ctx, engine.cpp:52-57
+  const double spi = s.obs_interval_s / s.cfg.dt();
+  if (std::abs(spi - std::round(spi)) > 1e-9 || spi < 1.0)
+    throw std::runtime_error("observation interval must be a positive multiple of the time step");
+  return static_cast<int>(std::llround(spi));
+}
+
+struct Prepared {
+  dtg_ctx* ctx;
+  int N, L, B, T, spi;
+};
+
+Prepared prepare(const Scenario& s, const LinkParams& params, const RngStream& rng,
+                 const std::vector<std::uint64_t>& its) {
+  const int spi = steps_per_interval(s);
+  const InitialState init = seed_agents(s);
+  const int N = static_cast<int>(init.link.size());
+  const int L = s.net.n_links();
+  const int B = static_cast<int>(its.size());
+  if (B < 1) throw std::runtime_error("no noise draws");
+  if (static_cast<int>(params.u.size()) != L || static_cast<int>(params.kappa.size()) != L ||
+      static_cast<int>(params.beta.size()) != L || static_cast<int>(params.alpha.size()) != L ||
+      static_cast<int>(params.cost.size()) != L)
+    throw std::runtime_error("parameter vectors must have one entry per link");
+  if (s.net.succ_off.size() != static_cast<std::size_t>(L + 1))
+    throw std::runtime_error("network CSR is stale (call rebuild_csr)");
+  dtg_ctx* c = detail::context_for(s, N, B, s.horizon_steps);
+  check(c, dtg_set_params(c, -1, params.u.data(), params.kappa.data(), params.beta.data(),
+                          params.alpha.data(), params.cost.data()));
+  check(c, dtg_set_state(c, -1, init.link.data(), init.pos.data()));
+  for (int b = 0; b < B; ++b) check(c, dtg_set_noise(c, b, rng.seed(), its[b]));
+  return {c, N, L, B, s.horizon_steps, spi};
+}
+
+CompactState read_state(dtg_ctx* c, int b, int step, int N) {
+  CompactState st;
+  st.link.resize(N);
+  st.pos.resize(N);
+  check(c, dtg_read_state(c, b, step, st.link.data(), st.pos.data()));
+  return st;
+}
+
+std::vector<std::vector<double>> read_cum(dtg_ctx* c, int b, int T, int L) {
+  std::vector<double> flat(static_cast<std::size_t>(T) * L);
+  check(c, dtg_read_cum(c, b, flat.data()));
+  std::vector<std::vector<double>> out(T);
+  for (int t = 0; t < T; ++t)
+    out[t].assign(flat.begin() + static_cast<std::size_t>(t) * L,
+                  flat.begin() + static_cast<std::size_t>(t + 1) * L);
+  return out;
+}
+
+}  // namespace
+
+std::vector<Trajectory> simulate_forward_draws(const Scenario& s, const LinkParams& params,
+                                               const RngStream& rng,
+                                               const std::vector<std::uint64_t>& its,
+                                               bool record_states) {
+  const auto t0 = Clock::now();
+  const Prepared p = prepare(s, params, rng, its);
+  check(p.ctx, dtg_forward(p.ctx, p.T, p.spi, record_states ? 1 : 0));
+  std::vector<Trajectory> out(p.B);
+  for (int b = 0; b < p.B; ++b) {
+    Trajectory& tr = out[b];
+    tr.steps = p.T;
+    tr.cum_per_step = read_cum(p.ctx, b, p.T, p.L);
+    tr.final_state = read_state(p.ctx, b, p.T, p.N);
+    tr.cum_final = p.T ? tr.cum_per_step.back() : std::vector<double>(p.L, 0.0);
+    if (record_states)
+      for (int t = 1; t <= p.T; ++t) tr.states.push_back(read_state(p.ctx, b, t, p.N));
+  }
+  const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
+  for (auto& tr : out) tr.wall_seconds = wall;
+  return out;
+}
+
+Trajectory simulate_forward(const Scenario& s, const LinkParams& params, const RngStream& rng,
+                            const ForwardOptions& opt) {
+  if (opt.trace_branches)
+    throw std::runtime_error("trace_branches is FD-validation instrumentation; not on the device path");
+  return std::move(simulate_forward_draws(s, params, rng, {opt.noise_iteration},
+                                          opt.record_states)[0]);
+}
+
+std::vector<GradResult> simulate_gradient_draws(const Scenario& s, const LinkParams& params,
+                                                const RngStream& rng, const LossBuilder& builder,
+                                                const std::vector<std::uint64_t>& its) {
+  if (s.cfg.soft_choices)  // engine.cpp:306-309
+    throw std::runtime_error(
+        "checkpointed backward requires discrete choices (compact state snapshots are exact "
+        "only for one-link-per-agent states)");
+  const auto t0 = Clock::now();
+  const Prepared p = prepare(s, params, rng, its);
+  check(p.ctx, dtg_forward(p.ctx, p.T, p.spi, 1));
+  const int K = dtg_n_snapshots(p.ctx);
+  std::vector<GradResult> res(p.B);
+  const std::size_t L = p.L, N = p.N;
+  std::vector<double> snap_seed(static_cast<std::size_t>(p.B) * K * L, 0.0);
+  std::vector<double> cum_seed(p.B * L, 0.0), x_seed(p.B * N, 0.0);
+  for (int b = 0; b < p.B; ++b) {
+    GradResult& g = res[b];
+    const auto cum = read_cum(p.ctx, b, p.T, p.L);
+    for (int t = 0; t < p.T; ++t)
+      if ((t + 1) % p.spi == 0) g.snapshot_values.push_back(cum[t]);
+    g.cum_final_values = p.T ? cum.back() : std::vector<double>(L, 0.0);
+    g.final_state = read_state(p.ctx, b, p.T, p.N);
+    LossInputs li{&g.snapshot_values, &g.cum_final_values, &g.final_state};
+    const LossValue lv = builder(li);
+    g.loss = lv.loss;
+    for (int k = 0; k < K && k < static_cast<int>(lv.d_snapshots.size()); ++k)
+      if (!lv.d_snapshots[k].empty())
+        std::copy(lv.d_snapshots[k].begin(), lv.d_snapshots[k].end(),
+                  snap_seed.begin() + (static_cast<std::size_t>(b) * K + k) * L);
+    if (!lv.d_cum_final.empty())
+      std::copy(lv.d_cum_final.begin(), lv.d_cum_final.end(), cum_seed.begin() + b * L);
+    if (!lv.d_x_final.empty())
+      std::copy(lv.d_x_final.begin(), lv.d_x_final.end(), x_seed.begin() + b * N);
+  }
+  std::vector<double> grads(static_cast<std::size_t>(p.B) * 5 * L, 0.0);
+  if (p.T > 0)
+    check(p.ctx, dtg_backward(p.ctx, K ? snap_seed.data() : nullptr, cum_seed.data(),
+                              x_seed.data(), grads.data()));
+  const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
+  for (int b = 0; b < p.B; ++b) {
+    const double* g = grads.data() + static_cast<std::size_t>(b) * 5 * L;
+    res[b].grads.u.assign(g, g + L);
+    res[b].grads.kappa.assign(g + L, g + 2 * L);
+    res[b].grads.beta.assign(g + 2 * L, g + 3 * L);
+    res[b].grads.alpha.assign(g + 3 * L, g + 4 * L);
+    res[b].grads.cost.assign(g + 4 * L, g + 5 * L);
+    res[b].wall_seconds = wall;
+  }
+  return res;
+}
+
+GradResult simulate_gradient(const Scenario& s, const LinkParams& params, const RngStream& rng,
+                             const LossBuilder& builder, GradMode, const ForwardOptions& opt) {
+  if (opt.trace_branches)
+    throw std::runtime_error("trace_branches is FD-validation instrumentation; not on the device path");
+  return std::move(simulate_gradient_draws(s, params, rng, builder, {opt.noise_iteration})[0]);
+}
+
+// ---- losses (host mini-tape restated: values and seeds in the reference's op order)
+LossBuilder mse_loss_builder(const CountSeries& obs, int delta_n) {
+  if (obs.link_ids.empty()) throw std::runtime_error("loss: no observed links");
+  return [obs, delta_n](const LossInputs& li) {
+    const int K = obs.n_intervals();
+    const auto& snaps = *li.snapshots;
+    if (static_cast<int>(snaps.size()) < K)
+      throw std::runtime_error("loss: fewer snapshots than observations");
+    const std::size_t n = obs.link_ids.size();
+    const double sc = 1.0 / (static_cast<double>(K) * n);
+    LossValue lv;
+    lv.d_snapshots.assign(snaps.size(), std::vector<double>(snaps.empty() ? 0 : snaps[0].size(), 0.0));
+    double acc = 0.0;
+    for (int k = 0; k < K; ++k) {
+      double r = 0.0;
+      for (std::size_t q = 0; q < n; ++q) {
+        const double d = snaps[k][obs.link_ids[q]] * static_cast<double>(delta_n) - obs.values[k][q];
+        r += d * d;
+        lv.d_snapshots[k][obs.link_ids[q]] += ((0.0 + sc * d) + sc * d) * static_cast<double>(delta_n);
+      }
+      acc = acc + r;
+    }
+    lv.loss = acc * sc;
+    return lv;
+  };
+}
+
+LossBuilder control_loss_builder(int target, double desired, int dn) {
+  return [target, desired, dn](const LossInputs& li) {
+    const auto& cf = *li.cum_final;
+    LossValue lv;
+    const double d = cf[target] * static_cast<double>(dn) + (-desired);
+    lv.loss = d * d;
+    lv.d_cum_final.assign(cf.size(), 0.0);
+    lv.d_cum_final[target] = ((0.0 + d) + d) * static_cast<double>(dn);
+    return lv;
+  };
+}
+
+LossBuilder linear_quadratic_loss(std::vector<double> ws, std::vector<double> qs,
+                                  std::vector<double> wc, std::vector<double> qc,
+                                  std::vector<double> wx) {
+  return [=](const LossInputs& li) {
+    const auto& snaps = *li.snapshots;
+    const auto& cf = *li.cum_final;
+    const std::size_t L = cf.size();
+    LossValue lv;
+    double acc = 0.0;
+    lv.d_snapshots.resize(snaps.size());
+    for (std::size_t k = 0; k < snaps.size(); ++k) {
+      const auto& s = snaps[k];
+      if (!ws.empty()) {
+        double r = 0.0;
+        for (std::size_t j = 0; j < L; ++j) r += s[j] * ws[k * L + j];
+        acc = acc + r;
+      }
+      if (!qs.empty()) {
+        double r = 0.0;
+        for (std::size_t j = 0; j < L; ++j) r += (s[j] * s[j]) * (qs[k * L + j] * 0.5);
+        acc = acc + r;
+      }
+      lv.d_snapshots[k].assign(L, 0.0);
+      for (std::size_t j = 0; j < L; ++j) {
+        double sd = 0.0;
+        if (!qs.empty()) sd = qs[k * L + j] * s[j];
+        if (!ws.empty()) sd = sd + ws[k * L + j];
+        lv.d_snapshots[k][j] = sd;
+      }
+    }
+    if (!wc.empty()) {
+      double r = 0.0;
+      for (std::size_t j = 0; j < L; ++j) r += cf[j] * wc[j];
+      acc = acc + r;
+    }
+    if (!qc.empty()) {
+      double r = 0.0;
+      for (std::size_t j = 0; j < L; ++j) r += (cf[j] * cf[j]) * (qc[j] * 0.5);
+      acc = acc + r;
+    }
+    lv.d_cum_final.assign(L, 0.0);
+    for (std::size_t j = 0; j < L; ++j) {
+      double sd = 0.0;
+      if (!qc.empty()) sd = qc[j] * cf[j];
+      if (!wc.empty()) sd = sd + wc[j];
+      lv.d_cum_final[j] = sd;
+    }
+    if (!wx.empty()) {
+      const auto& st = *li.final_state;
+      double r = 0.0;
+      for (std::size_t n = 0; n < st.pos.size(); ++n)
+        if (st.link[n] >= 0) r += st.pos[n] * wx[n];
+      acc = acc + r;
+      lv.d_x_final = wx;
+    }
+    lv.loss = acc;
+    return lv;
+  };
+}
+
+CountSeries series_from_levels(const std::vector<std::vector<double>>& cum_per_step,
+                               const std::vector<int>& link_ids, int interval_s, double dt,
+                               int delta_n) {
+  CountSeries out;
+  out.link_ids = link_ids;
+  out.interval_s = interval_s;
+  const int T = static_cast<int>(cum_per_step.size());
+  for (int t = 0; t < T; ++t) {
+    const double elapsed = (t + 1) * dt;
+    const double k = elapsed / interval_s;
+    if (std::abs(k - std::round(k)) > 1e-9) continue;
+    std::vector<double> row(link_ids.size());
+    for (std::size_t p = 0; p < link_ids.size(); ++p)
+      row[p] = cum_per_step[t][link_ids[p]] * delta_n;
+    out.values.push_back(std::move(row));
+  }
+  return out;
+}
+
+}  // namespace dtg
+
+// =====================================================================================
+// Level-2 flat C-ABI
+// =====================================================================================
+struct dtg_scenario {
+  dtg::Scenario s;
+  std::string err;
+  dtg_ctx* last_ctx = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_scn_error;
+
+template <class F>
+int scn_guard(dtg_scenario* sc, F&& f) {
+  try {
+    f();
+    return DTG_OK;
+  } catch (const dtg::ApiError& e) {
+    if (sc) sc->err = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    if (sc) sc->err = e.what();
+    return DTG_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    if (sc) sc->err = e.what();
+    return DTG_ERR_RUNTIME;
+  }
+}
+
+dtg::LinkParams make_params(int L, const double* u, const double* k, const double* b,
+                            const double* a, const double* c) {
+  dtg::LinkParams p;
+  p.u.assign(u, u + L);
+  p.kappa.assign(k, k + L);
+  p.beta.assign(b, b + L);
+  p.alpha.assign(a, a + L);
+  p.cost.assign(c, c + L);
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+dtg_scenario* dtg_scenario_from_links(int n_nodes, int n_links, const int* from,
+                                      const int* to, const double* len, const int* kind) {
+  try {
+    std::vector<dtg::Link> links(n_links);
+    for (int i = 0; i < n_links; ++i) {
+      if (kind[i] < 0 || kind[i] > 2) throw std::invalid_argument("bad link kind");
+      links[i].from_node = from[i];
+      links[i].to_node = to[i];
+      links[i].length = len[i];
+      links[i].kind = static_cast<dtg::LinkKind>(kind[i]);
+    }
+    auto* sc = new dtg_scenario;
+    sc->s.net = dtg::make_network(n_nodes, std::move(links));
+    return sc;
+  } catch (const std::exception& e) {
+    g_scn_error = e.what();
+    return nullptr;
+  }
+}
+
+dtg_scenario* dtg_scenario_grid(int n, double length, uint64_t net_seed, double virt_len) {
+  try {
+    auto* sc = new dtg_scenario;
+    sc->s.net = dtg::attach_virtual_links(dtg::grid_network(n, length), dtg::RngStream(net_seed),
+                                          virt_len);
+    return sc;
+  } catch (const std::exception& e) {
+    g_scn_error = e.what();
+    return nullptr;
+  }
+}
+
+dtg_scenario* dtg_scenario_tntp(const char* text, double scale, uint64_t net_seed,
+                                double virt_len) {
+  try {
+    auto* sc = new dtg_scenario;
+    sc->s.net = dtg::attach_virtual_links(dtg::parse_tntp_text(text, scale),
+                                          dtg::RngStream(net_seed), virt_len);
+    return sc;
+  } catch (const std::exception& e) {
+    g_scn_error = e.what();
+    return nullptr;
+  }
+}
+
+void dtg_scenario_free(dtg_scenario* sc) { delete sc; }
+
+const char* dtg_scenario_last_error(const dtg_scenario* sc) {
+  return sc ? sc->err.c_str() : g_scn_error.c_str();
+}
+
+int dtg_scenario_configure(dtg_scenario* sc, int n_vehicles, int delta_n, double tau,
+                           double gumbel_tau, int tg, int horizon_steps, int obs_interval_s,
+                           int fit_queues) {
+  return scn_guard(sc, [&] {
+    sc->s.n_vehicles = n_vehicles;
+    sc->s.cfg.delta_n = delta_n;
+    sc->s.cfg.tau = tau;
+    sc->s.cfg.gumbel_tau = gumbel_tau;
+    sc->s.cfg.trajectory_grafting = tg != 0;
+    sc->s.horizon_steps = horizon_steps;
+    sc->s.obs_interval_s = obs_interval_s;
+    if (fit_queues) dtg::fit_inflow_queues(sc->s);
+  });
+}
+
+int dtg_scenario_custom_init(dtg_scenario* sc, int n, const int* link, const double* pos) {
+  return scn_guard(sc, [&] {
+    sc->s.custom_init.clear();
+    for (int i = 0; i < n; ++i) sc->s.custom_init.push_back({link[i], pos[i]});
+  });
+}
+
+int dtg_scenario_n_links(const dtg_scenario* sc) { return sc->s.net.n_links(); }
+int dtg_scenario_n_nodes(const dtg_scenario* sc) { return sc->s.net.n_nodes; }
+int dtg_scenario_n_agents(const dtg_scenario* sc) {
+  try {
+    return sc->s.n_agents();
+  } catch (const std::exception& e) {
+    const_cast<dtg_scenario*>(sc)->err = e.what();
+    return -1;
+  }
+}
+int dtg_scenario_n_edges(const dtg_scenario* sc) { return static_cast<int>(sc->s.net.succ.size()); }
+
+int dtg_scenario_links(const dtg_scenario* sc, int* from, int* to, double* len, int* kind) {
+  const auto& L = sc->s.net.links;
+  for (std::size_t i = 0; i < L.size(); ++i) {
+    from[i] = L[i].from_node;
+    to[i] = L[i].to_node;
+    len[i] = L[i].length;
+    kind[i] = static_cast<int>(L[i].kind);
+  }
+  return DTG_OK;
+}
+
+int dtg_scenario_csr(const dtg_scenario* sc, int* succ_off, int* succ) {
+  std::copy(sc->s.net.succ_off.begin(), sc->s.net.succ_off.end(), succ_off);
+  std::copy(sc->s.net.succ.begin(), sc->s.net.succ.end(), succ);
+  return DTG_OK;
+}
+
+int dtg_scenario_sample_parameters(const dtg_scenario* sc, uint64_t seed, int mean_mode,
+                                   double* u, double* k, double* b, double* a, double* c) {
+  return scn_guard(const_cast<dtg_scenario*>(sc), [&] {
+    const dtg::LinkParams p =
+        dtg::sample_parameters(sc->s.net, dtg::ParamRanges{}, dtg::RngStream(seed), mean_mode != 0);
+    std::copy(p.u.begin(), p.u.end(), u);
+    std::copy(p.kappa.begin(), p.kappa.end(), k);
+    std::copy(p.beta.begin(), p.beta.end(), b);
+    std::copy(p.alpha.begin(), p.alpha.end(), a);
+    std::copy(p.cost.begin(), p.cost.end(), c);
+  });
+}
+
+int dtg_scenario_seed_agents(const dtg_scenario* sc, int* link, double* pos) {
+  return scn_guard(const_cast<dtg_scenario*>(sc), [&] {
+    const dtg::InitialState init = dtg::seed_agents(sc->s);
+    std::copy(init.link.begin(), init.link.end(), link);
+    std::copy(init.pos.begin(), init.pos.end(), pos);
+  });
+}
+
+int dtg_steps_for_minutes(int delta_n, double tau, double minutes) {
+  try {
+    dtg::SimConfig c;
+    c.delta_n = delta_n;
+    c.tau = tau;
+    return dtg::steps_for_minutes(c, minutes);
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+int dtg_simulate_forward(dtg_scenario* sc, const double* u, const double* k, const double* b,
+                         const double* a, const double* c, uint64_t root_seed, int n_draws,
+                         const uint64_t* its, double* cum_per_step, int* link_final,
+                         double* pos_final, int* states_link, double* states_pos,
+                         double* wall_seconds) {
+  return scn_guard(sc, [&] {
+    const int L = sc->s.net.n_links();
+    const std::vector<std::uint64_t> iv(its, its + n_draws);
+    const auto trs = dtg::simulate_forward_draws(sc->s, make_params(L, u, k, b, a, c),
+                                                 dtg::RngStream(root_seed), iv,
+                                                 states_link != nullptr);
+    sc->last_ctx = dtg::detail::g_last_ctx;
+    const int T = sc->s.horizon_steps;
+    for (int d = 0; d < n_draws; ++d) {
+      const auto& tr = trs[d];
+      const std::size_t N = tr.final_state.link.size();
+      if (cum_per_step)
+        for (int t = 0; t < T; ++t)
+          std::copy(tr.cum_per_step[t].begin(), tr.cum_per_step[t].end(),
+                    cum_per_step + (static_cast<std::size_t>(d) * T + t) * L);
+      if (link_final) std::copy(tr.final_state.link.begin(), tr.final_state.link.end(), link_final + d * N);
+      if (pos_final) std::copy(tr.final_state.pos.begin(), tr.final_state.pos.end(), pos_final + d * N);
+      if (states_link)
+        for (int t = 0; t < T; ++t) {
+          std::copy(tr.states[t].link.begin(), tr.states[t].link.end(),
+                    states_link + (static_cast<std::size_t>(d) * T + t) * N);
+          std::copy(tr.states[t].pos.begin(), tr.states[t].pos.end(),
+                    states_pos + (static_cast<std::size_t>(d) * T + t) * N);
+        }
+      if (wall_seconds) *wall_seconds = tr.wall_seconds;
+    }
+  });
+}
+
+static int gradient_common(dtg_scenario* sc, const double* u, const double* k, const double* b,
+                           const double* a, const double* c, uint64_t root_seed, int n_draws,
+                           const uint64_t* its, const dtg::LossBuilder& builder, double* loss,
+                           double* grads, double* snapshots, double* cum_final, int* link_final,
+                           double* pos_final, double* wall_seconds) {
+  return scn_guard(sc, [&] {
+    const int L = sc->s.net.n_links();
+    const std::vector<std::uint64_t> iv(its, its + n_draws);
+    const auto res = dtg::simulate_gradient_draws(sc->s, make_params(L, u, k, b, a, c),
+                                                  dtg::RngStream(root_seed), builder, iv);
+    sc->last_ctx = dtg::detail::g_last_ctx;
+    for (int d = 0; d < n_draws; ++d) {
+      const auto& g = res[d];
+      if (loss) loss[d] = g.loss;
+      const std::size_t o = static_cast<std::size_t>(d) * 5 * L;
+      if (grads) {
+        std::copy(g.grads.u.begin(), g.grads.u.end(), grads + o);
+        std::copy(g.grads.kappa.begin(), g.grads.kappa.end(), grads + o + L);
+        std::copy(g.grads.beta.begin(), g.grads.beta.end(), grads + o + 2 * L);
+        std::copy(g.grads.alpha.begin(), g.grads.alpha.end(), grads + o + 3 * L);
+        std::copy(g.grads.cost.begin(), g.grads.cost.end(), grads + o + 4 * L);
+      }
+      const std::size_t K = g.snapshot_values.size();
+      if (snapshots)
+        for (std::size_t q = 0; q < K; ++q)
+          std::copy(g.snapshot_values[q].begin(), g.snapshot_values[q].end(),
+                    snapshots + (d * K + q) * L);
+      if (cum_final) std::copy(g.cum_final_values.begin(), g.cum_final_values.end(), cum_final + d * L);
+      const std::size_t N = g.final_state.link.size();
+      if (link_final) std::copy(g.final_state.link.begin(), g.final_state.link.end(), link_final + d * N);
+      if (pos_final) std::copy(g.final_state.pos.begin(), g.final_state.pos.end(), pos_final + d * N);
+      if (wall_seconds) *wall_seconds = g.wall_seconds;
+    }
+  });
+}
+
+int dtg_simulate_gradient(dtg_scenario* sc, const double* u, const double* k, const double* b,
+                          const double* a, const double* c, uint64_t root_seed, int n_draws,
+                          const uint64_t* its, const double* ws, const double* qs,
+                          const double* wc, const double* qc, const double* wx, double* loss,
+                          double* grads, double* snapshots, double* cum_final, int* link_final,
+                          double* pos_final, double* wall_seconds) {
+  std::vector<double> vws, vqs, vwc, vqc, vwx;
+  int rc = scn_guard(sc, [&] {
+    const int L = sc->s.net.n_links();
+    const int T = sc->s.horizon_steps;
+    const double spi = sc->s.obs_interval_s / sc->s.cfg.dt();
+    const int K = spi >= 1.0 ? static_cast<int>(T / std::llround(spi)) : 0;
+    const int N = sc->s.n_agents();
+    if (ws) vws.assign(ws, ws + static_cast<std::size_t>(K) * L);
+    if (qs) vqs.assign(qs, qs + static_cast<std::size_t>(K) * L);
+    if (wc) vwc.assign(wc, wc + L);
+    if (qc) vqc.assign(qc, qc + L);
+    if (wx) vwx.assign(wx, wx + N);
+  });
+  if (rc) return rc;
+  return gradient_common(sc, u, k, b, a, c, root_seed, n_draws, its,
+                         dtg::linear_quadratic_loss(vws, vqs, vwc, vqc, vwx), loss, grads,
+                         snapshots, cum_final, link_final, pos_final, wall_seconds);
+}
+
+int dtg_simulate_gradient_mse(dtg_scenario* sc, const double* u, const double* k,
+                              const double* b, const double* a, const double* c,
+                              uint64_t root_seed, int n_draws, const uint64_t* its, int n_obs,
+                              const int* obs_ids, int k_obs, const double* obs_values,
+                              double* loss, double* grads) {
+  dtg::CountSeries obs;
+  obs.link_ids.assign(obs_ids, obs_ids + n_obs);
+  obs.interval_s = sc->s.obs_interval_s;
+  for (int q = 0; q < k_obs; ++q)
+    obs.values.emplace_back(obs_values + static_cast<std::size_t>(q) * n_obs,
+                            obs_values + static_cast<std::size_t>(q + 1) * n_obs);
+  dtg::LossBuilder builder;
+  int rc = scn_guard(sc, [&] { builder = dtg::mse_loss_builder(obs, sc->s.cfg.delta_n); });
+  if (rc) return rc;
+  return gradient_common(sc, u, k, b, a, c, root_seed, n_draws, its, builder, loss, grads,
+                         nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+dtg_ctx* dtg_scenario_ctx(dtg_scenario* sc) { return sc->last_ctx; }
+
+}  // extern "C"

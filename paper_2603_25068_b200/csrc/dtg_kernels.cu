@@ -1,0 +1,834 @@
+// sm_100a kernels for one engine step and its checkpointed VJP.
+//
+// Forward step t (reference engine_step, src/engine.cpp:70-125):
+//   k_step_cf       one thread per agent slot: Newell car-following with the
+//                   leader in the previous slot, per-link midpoint count and
+//                   arrived-prefix length as segment-boundary writes, vacancy
+//                   tail, and the Gumbel-softmax link choice of arrived agents.
+//   k_step_merge    one thread per link: count/cumulative update, vacancy,
+//                   merge-choice over the arrived heads of the predecessor links.
+//   k_step_scan     one CTA per scenario: departures, new segment sizes and the
+//                   exclusive scan to the next segment offsets.
+//   k_step_transfer one thread per slot: compaction into the next layout
+//                   (winners enter their new link at position 0.0, everyone
+//                   else keeps x1 and its order).
+// Reverse step (the per-step segment VJP of engine.cpp:388-415) replays the
+// first three kernels from the step's checkpoint, then:
+//   k_adj_node    per link: count adjoint and the merge-row VJP (transfer VJP
+//                 seeds, softmax VJP, targeted routing to the first candidate).
+//   k_adj_a0      per scenario: rows the reference routes to the first arrived
+//                 agent (non-targeted rows, reduce_max first-index rule).
+//   k_adj_choice  per link: link-choice VJP of the arrived heads.
+//   k_adj_slot    per slot: transfer pass-through, counting sigmoid VJP,
+//                 car-following VJP with the follower's headway term.
+//   k_adj_link    warp per link: deterministic per-link reductions into the
+//                 u, kappa, beta, alpha, cost gradients.
+// All fp64 with -fmad=false: the forward is bit-identical to the reference.
+#include <climits>
+#include <cstdint>
+
+#include "dtg_device.cuh"
+#include "dtg_kernels.h"
+
+namespace dtg {
+
+// ---------------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_step_cf(DevView d, int t, int s_cur) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= d.N) return;
+  const std::size_t so = sidx(d, s_cur, b);
+  const double* pos = d.pos + so;
+  const int* off = d.off + oidx(d, s_cur, b);
+  const int j = d.lnk[so + k];
+  const int base = off[j], n = off[j + 1] - base, r = k - base;
+  const std::size_t pl = static_cast<std::size_t>(b) * d.L + j;
+  const double jam = d.jam[pl], dxf = d.dxf[pl], len = d.len[j];
+  const double ctr = d.ctr[j], thr = d.thr[j];
+  const double x = pos[k];
+  // headway: leader gets M (car_following.cpp:547-553)
+  const CfPick me = cf_step(x, r == 0 ? d.M : pos[k - 1] - x, jam, dxf, len);
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  d.x1[bn + k] = me.x1;
+  bool fo_n = false, fa_n = false;
+  if (r + 1 < n) {
+    const double xn = pos[k + 1];
+    const CfPick nx = cf_step(xn, x - xn, jam, dxf, len);
+    fo_n = nx.x1 >= ctr;
+    fa_n = nx.x1 >= thr;
+  }
+  const bool fo = me.x1 >= ctr, fa = me.x1 >= thr;
+  // x1 stays ordered inside the segment, so {x1 >= o} and {x1 >= L-0.01} are
+  // prefixes: their lengths are written by the unique boundary slot.
+  int* qn = d.qn + static_cast<std::size_t>(b) * d.L;
+  int* nA = d.nA + static_cast<std::size_t>(b) * d.L;
+  if (r == 0 && !fo) qn[j] = 0;
+  if (fo && !fo_n) qn[j] = r + 1;
+  if (r == 0 && !fa) nA[j] = 0;
+  if (fa && !fa_n) nA[j] = r + 1;
+  if (r == n - 1) d.tail[pl] = me.x1;  // min x1 = vacancy (node_model.cpp:27-41)
+  if (fa) {
+    d.won[bn + k] = 0;
+    int c = -1;
+    const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
+    if (deg > 0) {  // link_choice (node_model.cpp:45-97)
+      double v[kMaxDeg], g[kMaxDeg], lz[kMaxDeg], pi[kMaxDeg];
+      const int agent = d.aid[so + k];
+      const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+      for (int e = 0; e < deg; ++e) {
+        const int jj = d.succ[s0 + e];
+        v[e] = d.pref[bl + jj];
+        g[e] = gumbel(d.seed_link[b], static_cast<std::uint64_t>(t),
+                      static_cast<std::uint64_t>(agent), static_cast<std::uint64_t>(jj));
+      }
+      c = d.succ[s0 + two_softmax<kMaxDeg>(deg, v, g, d.kinv, lz, pi)];
+    }
+    d.choice[bn + k] = c;
+  }
+}
+
+// Merge candidates of row i: arrived heads of predecessor links that chose i,
+// ascending agent id (merge_choice columns, node_model.cpp:99-120).
+__device__ __forceinline__ int gather_candidates(const DevView& d, int b, int i,
+                                                 const int* off, std::size_t so,
+                                                 int* cid, int* cslot, int* clink) {
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  int nc = 0;
+  for (int e = d.pred_off[i]; e < d.pred_off[i + 1]; ++e) {
+    const int p = d.pred[e];
+    const int base = off[p];
+    if (off[p + 1] == base) continue;
+    const int nap = d.nA[bl + p];
+    for (int r = 0; r < nap; ++r) {
+      const int s = base + r;
+      if (d.choice[bn + s] != i) continue;
+      if (nc == kMaxCand) {
+        atomicOr(&d.err[b], kErrCandOverflow);
+        return nc;
+      }
+      cid[nc] = d.aid[so + s];
+      cslot[nc] = s;
+      clink[nc] = p;
+      ++nc;
+    }
+  }
+  for (int a = 1; a < nc; ++a) {  // insertion sort by agent id
+    const int ci = cid[a], cs = cslot[a], cl = clink[a];
+    int m = a - 1;
+    while (m >= 0 && cid[m] > ci) {
+      cid[m + 1] = cid[m];
+      cslot[m + 1] = cslot[m];
+      clink[m + 1] = clink[m];
+      --m;
+    }
+    cid[m + 1] = ci;
+    cslot[m + 1] = cs;
+    clink[m + 1] = cl;
+  }
+  return nc;
+}
+
+__device__ __forceinline__ int merge_softmax(const DevView& d, int b, int t, int i,
+                                             int nc, const int* cid, const int* clink,
+                                             double* lz, double* pi) {
+  double v[kMaxCand], g[kMaxCand];
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  for (int e = 0; e < nc; ++e) {
+    v[e] = d.alpha[bl + clink[e]];  // p = l * matmul(valid, alpha)
+    if (v[e] == 0.0) atomicOr(&d.err[b], kErrZeroAlpha);
+    g[e] = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
+                  static_cast<std::uint64_t>(i), static_cast<std::uint64_t>(cid[e]));
+  }
+  return two_softmax<kMaxCand>(nc, v, g, d.kinv, lz, pi);
+}
+
+__global__ void __launch_bounds__(128) k_step_merge(DevView d, int t, int s_cur,
+                                                     int replay) {
+  const int b = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.L) return;
+  const std::size_t so = sidx(d, s_cur, b);
+  const int* off = d.off + oidx(d, s_cur, b);
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const int n_i = off[i + 1] - off[i];
+  const int qc = n_i ? d.qn[bl + i] : 0;
+  const double tx = n_i ? d.tail[bl + i] : d.M;
+  if (!replay) {  // inc = relu(q - qprev); cum += inc (engine.cpp:111-113)
+    const double a = static_cast<double>(qc) - d.qh[hidx(d, t, b) + i];
+    d.cumh[hidx(d, t + 1, b) + i] = d.cumh[hidx(d, t, b) + i] + (a >= 0.0 ? a : 0.0);
+    d.qh[hidx(d, t + 1, b) + i] = static_cast<double>(qc);
+  }
+  const bool vacant = tx > d.jam[bl + i];
+  d.vac[bl + i] = vacant;
+  int w = -1;
+  if (vacant) {
+    int cid[kMaxCand], cslot[kMaxCand], clink[kMaxCand];
+    const int nc = gather_candidates(d, b, i, off, so, cid, cslot, clink);
+    if (nc) {
+      double lz[kMaxCand], pi[kMaxCand];
+      w = cslot[merge_softmax(d, b, t, i, nc, cid, clink, lz, pi)];
+      d.won[static_cast<std::size_t>(b) * d.N + w] = 1;
+    }
+  }
+  d.win[bl + i] = w;
+}
+
+// Block-wide exclusive scan of one int per thread (blockDim.x == 1024).
+__device__ __forceinline__ int block_excl_scan(int v, int* smem, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int w = lane < (blockDim.x >> 5) ? smem[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    smem[lane] = w;
+  }
+  __syncthreads();
+  const int warp_prefix = wid ? smem[wid - 1] : 0;
+  *total = smem[(blockDim.x >> 5) - 1];
+  return warp_prefix + x - v;
+}
+
+__global__ void __launch_bounds__(1024) k_step_scan(DevView d, int s_cur,
+                                                     int s_next, int replay) {
+  __shared__ int sm[32];
+  __shared__ unsigned long long smin[32];
+  const int b = blockIdx.x;
+  const std::size_t so = sidx(d, s_cur, b);
+  const int* off = d.off + oidx(d, s_cur, b);
+  int* offn = d.off + oidx(d, s_next, b);
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  const int per = (d.L + blockDim.x - 1) / blockDim.x;
+  const int j0 = threadIdx.x * per, j1 = min(d.L, j0 + per);
+  int sum = 0;
+  unsigned long long a0key = ULLONG_MAX;
+  for (int j = j0; j < j1; ++j) {
+    const int base = off[j], n = off[j + 1] - base;
+    const int na = n ? d.nA[bl + j] : 0;
+    int dep = 0;
+    for (int r = 0; r < na; ++r) {
+      const int s = base + r;
+      dep += d.won[bn + s];
+      const unsigned long long key =
+          (static_cast<unsigned long long>(d.aid[so + s]) << 32) | static_cast<unsigned>(s);
+      a0key = key < a0key ? key : a0key;
+    }
+    const int nc = n - dep + (d.win[bl + j] >= 0 ? 1 : 0);
+    d.dep[bl + j] = dep;
+    d.newcnt[bl + j] = nc;
+    sum += nc;
+  }
+  int total;
+  const int excl = block_excl_scan(sum, sm, &total);
+  if (!replay) {
+    int run = excl;
+    for (int j = j0; j < j1; ++j) {
+      offn[j] = run;
+      run += d.newcnt[bl + j];
+    }
+    if (threadIdx.x == 0) {
+      offn[d.L] = total;
+      if (total != d.N) atomicOr(&d.err[b], kErrConservation);
+    }
+  }
+  // first arrived agent A[0] (min id) for the reverse sweep
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, a0key, o);
+    a0key = y < a0key ? y : a0key;
+  }
+  if ((threadIdx.x & 31) == 0) smin[threadIdx.x >> 5] = a0key;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long m = ULLONG_MAX;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = smin[w] < m ? smin[w] : m;
+    d.a0[b] = m == ULLONG_MAX ? -1 : static_cast<int>(m & 0xffffffffull);
+  }
+}
+
+// Slot of the agent in the next layout (the transfer compaction).
+__device__ __forceinline__ int next_slot(const DevView& d, std::size_t bn,
+                                         std::size_t bl, const int* offn, int k,
+                                         int j, int base, int r, int na,
+                                         bool* mover) {
+  if (r < na && d.won[bn + k]) {
+    *mover = true;
+    const int i = d.choice[bn + k];
+    return offn[i] + d.newcnt[bl + i] - 1;
+  }
+  *mover = false;
+  int dd;
+  if (r >= na) {
+    dd = d.dep[bl + j];
+  } else {
+    dd = 0;
+    for (int q = base; q < k; ++q) dd += d.won[bn + q];
+  }
+  return offn[j] + r - dd;
+}
+
+__global__ void __launch_bounds__(256) k_step_transfer(DevView d, int s_cur,
+                                                        int s_next) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= d.N) return;
+  const std::size_t so = sidx(d, s_cur, b), sn = sidx(d, s_next, b);
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  const int* off = d.off + oidx(d, s_cur, b);
+  const int* offn = d.off + oidx(d, s_next, b);
+  const int j = d.lnk[so + k];
+  const int base = off[j], r = k - base;
+  const int na = d.nA[bl + j];
+  bool mover;
+  const int ns = next_slot(d, bn, bl, offn, k, j, base, r, na, &mover);
+  // transfer (node_model.cpp:122-149): -M + M == 0.0 exactly on the new link
+  d.pos[sn + ns] = mover ? 0.0 : d.x1[bn + k];
+  d.aid[sn + ns] = d.aid[so + k];
+  d.lnk[sn + ns] = mover ? d.choice[bn + k] : j;
+}
+
+// ---------------------------------------------------------------------------------
+// reverse
+// ---------------------------------------------------------------------------------
+__global__ void k_adj_init_slots(DevView d, int s_fin, const double* x_seed,
+                                 double* xbar) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= d.N) return;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  xbar[bn + k] = x_seed ? x_seed[bn + d.aid[sidx(d, s_fin, b) + k]] : 0.0;
+}
+
+__global__ void k_adj_init_links(DevView d, const double* cum_seed) {
+  const int b = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.L) return;
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  d.cbar[bl + j] = cum_seed ? cum_seed[bl + j] : 0.0;
+  d.qbar[bl + j] = 0.0;
+  double* g = d.grads + static_cast<std::size_t>(b) * 5 * d.L;
+  for (int c = 0; c < 5; ++c) g[c * d.L + j] = 0.0;
+}
+
+// Adjoint of the non-admitted arrived agent's admitted-sum input
+// (transfer VJP: x_bar * (-M) + (-(x_bar * x1))).
+__device__ __forceinline__ double admitted_bar(double xb, double x1, double M) {
+  double r = 0.0;
+  r += xb * (-M);
+  r += -1.0 * (xb * x1);
+  return r;
+}
+
+__global__ void __launch_bounds__(128) k_adj_node(DevView d, int t, int s_cur,
+                                                   int s_next,
+                                                   const double* xbar_next,
+                                                   const double* snap_seed,
+                                                   int snap_k, int K) {
+  const int b = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.L) return;
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  if (snap_k >= 0 && snap_seed)  // snapshot seed enters before the step VJP (:390-393)
+    d.cbar[bl + i] += snap_seed[(static_cast<std::size_t>(b) * K + snap_k) * d.L + i];
+  const double cb = d.cbar[bl + i];
+  // inc = relu(q - qprev): q_bar += pick * cum_bar; qprev_bar = -pick * cum_bar
+  const double a = d.qh[hidx(d, t + 1, b) + i] - d.qh[hidx(d, t, b) + i];
+  const bool pick = a >= 0.0;
+  d.qtot[bl + i] = d.qbar[bl + i] + (pick ? cb : 0.0);
+  d.qbar[bl + i] = pick ? -1.0 * cb : 0.0;
+
+  const int w = d.win[bl + i];
+  if (w < 0) return;
+  const std::size_t so = sidx(d, s_cur, b);
+  const int* off = d.off + oidx(d, s_cur, b);
+  const int* offn = d.off + oidx(d, s_next, b);
+  int cid[kMaxCand], cslot[kMaxCand], clink[kMaxCand];
+  const int nc = gather_candidates(d, b, i, off, so, cid, cslot, clink);
+  double lz[kMaxCand], pi[kMaxCand], bar[kMaxCand];
+  merge_softmax(d, b, t, i, nc, cid, clink, lz, pi);
+  // winner: a_t[w][i] bar = x_bar_new * M (+ 0 admitted-sum adjoint)
+  const double abar_w = xbar_next[bn + offn[i] + d.newcnt[bl + i] - 1] * d.M + 0.0;
+  for (int e = 0; e < nc; ++e) {
+    const int s = cslot[e];
+    if (s == w) {
+      bar[e] = abar_w * 1.0;
+    } else {
+      const int p = clink[e];
+      const int base = off[p];
+      int dd = 0;
+      for (int q = base; q < s; ++q) dd += d.won[bn + q];
+      const double xb = xbar_next[bn + offn[p] + (s - base) - dd];
+      bar[e] = admitted_bar(xb, d.x1[bn + s], d.M) * 1.0;
+    }
+  }
+  two_softmax_vjp(nc, lz, pi, d.kinv, bar);
+  for (int e = 0; e < nc; ++e) {
+    const int s = cslot[e];
+    // reduce_max(l) routes targeted_bar = a_bar[w] to the first candidate
+    d.lbar_row[bn + s] = (e == 0 ? 0.0 + abar_w : 0.0) + bar[e] * d.alpha[bl + clink[e]];
+    d.prio_bar[bn + s] = 0.0 + bar[e] * 1.0;
+  }
+}
+
+// Block reductions for k_adj_a0 (blockDim.x == 256).
+struct ArgMaxE {
+  double e;
+  int id, slot;
+};
+__device__ __forceinline__ bool better(const ArgMaxE& a, const ArgMaxE& b) {
+  return a.e > b.e || (a.e == b.e && a.id < b.id);
+}
+
+// Rows that the reference routes to the first arrived agent A[0]: successors i
+// of A[0]'s link that are vacant and targeted by nobody.  targeted_i = max over
+// an all-zero column, whose first-index VJP lands on A[0]
+// (reduce_max tensor.cpp:863-876); the row's draw w_i is the Gumbel argmax
+// over every arrived agent with a uniform utility (node_model.cpp:99-120).
+__global__ void __launch_bounds__(256) k_adj_a0(DevView d, int t, int s_cur,
+                                                 int s_next, const double* xbar_next,
+                                                 unsigned long long* sort_scratch,
+                                                 int force_slow) {
+  __shared__ ArgMaxE sh[8];
+  __shared__ double shd[8];
+  __shared__ int shn[8];
+  __shared__ ArgMaxE best_all;
+  __shared__ double m2_all, runner_all;
+  __shared__ int na_all;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* la0 = d.lbar_a0 + static_cast<std::size_t>(b) * d.maxdeg;
+  if (tid < d.maxdeg) la0[tid] = 0.0;
+  const int a0s = d.a0[b];
+  if (a0s < 0) return;
+  const std::size_t so = sidx(d, s_cur, b);
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  const int* off = d.off + oidx(d, s_cur, b);
+  const int* offn = d.off + oidx(d, s_next, b);
+  const int c0 = d.lnk[so + a0s];
+  const int s0 = d.succ_off[c0], deg = d.succ_off[c0 + 1] - s0;
+  // |A|
+  int na_loc = 0;
+  for (int j = tid; j < d.L; j += blockDim.x)
+    if (off[j + 1] > off[j]) na_loc += d.nA[bl + j];
+  for (int o = 16; o > 0; o >>= 1) na_loc += __shfl_xor_sync(0xffffffffu, na_loc, o);
+  if (lane == 0) shn[wid] = na_loc;
+  __syncthreads();
+  if (tid == 0) {
+    int s = 0;
+    for (int w = 0; w < 8; ++w) s += shn[w];
+    na_all = s;
+  }
+  __syncthreads();
+  const int nA = na_all;
+  // uniform first-stage log-softmax: v = -1e12 everywhere, z = |A| exactly
+  const double v = 0.0 - kMaskLarge;
+  const double lzv = log(static_cast<double>(nA) * 1.0) + v;
+  const double logz = v - lzv;
+  for (int e = 0; e < deg; ++e) {
+    const int i = d.succ[s0 + e];
+    if (!d.vac[bl + i] || d.win[bl + i] >= 0) continue;
+    // pass 1: m2 = max y
+    double m2 = -INFINITY;
+    for (int j = tid; j < d.L; j += blockDim.x) {
+      const int base = off[j];
+      if (off[j + 1] == base) continue;
+      const int na = d.nA[bl + j];
+      for (int r = 0; r < na; ++r) {
+        const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
+                                static_cast<std::uint64_t>(i),
+                                static_cast<std::uint64_t>(d.aid[so + base + r]));
+        const double y = (logz + g) * d.kinv;
+        m2 = fmax(m2, y);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+    if (lane == 0) shd[wid] = m2;
+    __syncthreads();
+    if (tid == 0) {
+      double m = shd[0];
+      for (int w = 1; w < 8; ++w) m = fmax(m, shd[w]);
+      m2_all = m;
+    }
+    __syncthreads();
+    const double M2 = m2_all;
+    // pass 2: e = exp(y - m2); argmax e (ties -> lowest id) and runner-up
+    ArgMaxE bst{-1.0, INT_MAX, -1};
+    double runner = -1.0;
+    for (int j = tid; j < d.L; j += blockDim.x) {
+      const int base = off[j];
+      if (off[j + 1] == base) continue;
+      const int na = d.nA[bl + j];
+      for (int r = 0; r < na; ++r) {
+        const int s = base + r;
+        const int id = d.aid[so + s];
+        const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
+                                static_cast<std::uint64_t>(i), static_cast<std::uint64_t>(id));
+        const double ev = exp((logz + g) * d.kinv - M2);
+        ArgMaxE c{ev, id, s};
+        if (better(c, bst)) {
+          if (bst.e != ev) runner = fmax(runner, bst.e);
+          bst = c;
+        } else if (ev != bst.e) {
+          runner = fmax(runner, ev);
+        }
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMaxE c{__shfl_xor_sync(0xffffffffu, bst.e, o), __shfl_xor_sync(0xffffffffu, bst.id, o),
+                __shfl_xor_sync(0xffffffffu, bst.slot, o)};
+      const double rr = __shfl_xor_sync(0xffffffffu, runner, o);
+      // merge: runner-up = max of everything that is not the winner's value
+      double nr = fmax(runner, rr);
+      if (better(c, bst)) {
+        if (bst.e != c.e) nr = fmax(nr, bst.e);
+        bst = c;
+      } else if (c.e != bst.e) {
+        nr = fmax(nr, c.e);
+      }
+      runner = nr;
+    }
+    if (lane == 0) {
+      sh[wid] = bst;
+      shd[wid] = runner;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      ArgMaxE bb = sh[0];
+      double rn = shd[0];
+      for (int w = 1; w < 8; ++w) {
+        const ArgMaxE c = sh[w];
+        double nr = fmax(rn, shd[w]);
+        if (better(c, bb)) {
+          if (bb.e != c.e) nr = fmax(nr, bb.e);
+          bb = c;
+        } else if (c.e != bb.e) {
+          nr = fmax(nr, c.e);
+        }
+        rn = nr;
+      }
+      best_all = bb;
+      runner_all = rn;
+    }
+    __syncthreads();
+    ArgMaxE win = best_all;
+    // pi = e / z2 could merge the top value with a runner-up within an ulp;
+    // then redo the reference's ordered sum (ascending agent id) exactly.
+    const bool near = runner_all >= win.e * (1.0 - 0x1p-48);
+    if (near || force_slow) {
+      if (!force_slow && tid == 0) atomicOr(&d.err[b], kErrNearTieSlow);
+      // collect (id << 32 | slot) keys of A into scratch and sort (one block)
+      unsigned long long* keys = sort_scratch + static_cast<std::size_t>(b) * d.N;
+      __shared__ int cnt;
+      if (tid == 0) cnt = 0;
+      __syncthreads();
+      for (int j = tid; j < d.L; j += blockDim.x) {
+        const int base = off[j];
+        if (off[j + 1] == base) continue;
+        const int na = d.nA[bl + j];
+        for (int r = 0; r < na; ++r) {
+          const int s = base + r;
+          const int q = atomicAdd(&cnt, 1);
+          keys[q] = (static_cast<unsigned long long>(d.aid[so + s]) << 32) | static_cast<unsigned>(s);
+        }
+      }
+      __syncthreads();
+      int P = 1;
+      while (P < nA) P <<= 1;
+      for (int q = nA + tid; q < P; q += blockDim.x) keys[q] = ULLONG_MAX;
+      __syncthreads();
+      for (int kk = 2; kk <= P; kk <<= 1)  // bitonic sort in global scratch
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (int q = tid; q < P; q += blockDim.x) {
+            const int l = q ^ jj;
+            if (l > q) {
+              const unsigned long long a = keys[q], c = keys[l];
+              const bool up = (q & kk) == 0;
+              if ((a > c) == up) {
+                keys[q] = c;
+                keys[l] = a;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      if (tid == 0) {
+        double z2 = 0.0;
+        for (int q = 0; q < nA; ++q) {
+          const int id = static_cast<int>(keys[q] >> 32);
+          const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
+                                  static_cast<std::uint64_t>(i), static_cast<std::uint64_t>(id));
+          z2 += exp((logz + g) * d.kinv - M2);
+        }
+        double bp = -1.0;
+        for (int q = 0; q < nA; ++q) {
+          const int id = static_cast<int>(keys[q] >> 32);
+          const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
+                                  static_cast<std::uint64_t>(i), static_cast<std::uint64_t>(id));
+          const double pv = exp((logz + g) * d.kinv - M2) / z2;
+          if (pv > bp) {
+            bp = pv;
+            best_all = ArgMaxE{pv, id, static_cast<int>(keys[q] & 0xffffffffull)};
+          }
+        }
+      }
+      __syncthreads();
+      win = best_all;
+    }
+    if (tid == 0) {
+      const int ws = win.slot;
+      const int j = d.lnk[so + ws];
+      const int base = off[j];
+      const int na = d.nA[bl + j];
+      bool mover;
+      const int ns = next_slot(d, bn, bl, offn, ws, j, base, ws - base, na, &mover);
+      double ab;
+      if (mover) {
+        ab = 0.0 * d.M + 0.0;
+      } else {
+        const double xb = xbar_next[bn + ns];
+        ab = (i == j ? xb * d.M : 0.0 * d.M) + admitted_bar(xb, d.x1[bn + ws], d.M);
+      }
+      la0[e] = 0.0 + ab;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(128) k_adj_choice(DevView d, int t, int s_cur) {
+  const int b = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.L) return;
+  const std::size_t so = sidx(d, s_cur, b);
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  const int* off = d.off + oidx(d, s_cur, b);
+  const int base = off[j];
+  if (off[j + 1] == base) return;
+  const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
+  if (deg == 0) return;
+  const int na = d.nA[bl + j];
+  const int a0s = d.a0[b];
+  for (int r = 0; r < na; ++r) {
+    const int s = base + r;
+    double v[kMaxDeg], g[kMaxDeg], lz[kMaxDeg], pi[kMaxDeg], bar[kMaxDeg];
+    const int agent = d.aid[so + s];
+    for (int e = 0; e < deg; ++e) {
+      const int jj = d.succ[s0 + e];
+      v[e] = d.pref[bl + jj];
+      g[e] = gumbel(d.seed_link[b], static_cast<std::uint64_t>(t),
+                    static_cast<std::uint64_t>(agent), static_cast<std::uint64_t>(jj));
+    }
+    const int ed = two_softmax<kMaxDeg>(deg, v, g, d.kinv, lz, pi);
+    for (int e = 0; e < deg; ++e) bar[e] = 0.0;
+    const int dch = d.succ[s0 + ed];
+    if (d.vac[bl + dch] && d.win[bl + dch] >= 0) bar[ed] = d.lbar_row[bn + s];
+    if (s == a0s)
+      for (int e = 0; e < deg; ++e) bar[e] += d.lbar_a0[static_cast<std::size_t>(b) * d.maxdeg + e];
+    for (int e = 0; e < deg; ++e)  // l = picked * vacant * arrived * connected
+      bar[e] = ((bar[e] * 1.0) * 1.0) * (d.vac[bl + d.succ[s0 + e]] ? 1.0 : 0.0);
+    two_softmax_vjp(deg, lz, pi, d.kinv, bar);
+    double* vb = d.vbar + (bn + s) * d.maxdeg;
+    for (int e = 0; e < deg; ++e) vb[e] = bar[e];
+  }
+}
+
+// Adjoint of one agent's new position x1 through transfer, replace_rows and
+// the midpoint count (observation.cpp:9-20, sigmoid VJP tensor.cpp:794-800).
+__device__ __forceinline__ double x1_bar(const DevView& d, std::size_t bn,
+                                         std::size_t bl, const int* offn,
+                                         const double* xbar_next, int k, int j,
+                                         int base, int r, int na, double x1) {
+  bool mover;
+  const int ns = next_slot(d, bn, bl, offn, k, j, base, r, na, &mover);
+  double xb = (mover && !d.tg) ? 0.0 : xbar_next[bn + ns];
+  const double qt = d.qtot[bl + j];
+  if (qt != 0.0) {
+    const double sc = d.sc[j];
+    const double z = (x1 + (-d.ctr[j])) * sc;
+    const double sg = z >= 0.0 ? 1.0 / (1.0 + exp(-z)) : exp(z) / (1.0 + exp(z));
+    xb = xb + (((qt * 1.0) * sg) * (1.0 - sg)) * sc;
+  }
+  return xb;
+}
+
+__global__ void __launch_bounds__(256) k_adj_slot(DevView d, int s_cur, int s_next,
+                                                   const double* xbar_next,
+                                                   double* xbar_cur) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= d.N) return;
+  const std::size_t so = sidx(d, s_cur, b);
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  const double* pos = d.pos + so;
+  const int* off = d.off + oidx(d, s_cur, b);
+  const int* offn = d.off + oidx(d, s_next, b);
+  const int j = d.lnk[so + k];
+  const int base = off[j], n = off[j + 1] - base, r = k - base;
+  const int na = d.nA[bl + j];
+  const double jam = d.jam[bl + j], dxf = d.dxf[bl + j], len = d.len[j];
+  const double x = pos[k];
+  // own car-following VJP (car_following.cpp:128-157)
+  const CfPick me = cf_step(x, r == 0 ? d.M : pos[k - 1] - x, jam, dxf, len);
+  const double x1b = x1_bar(d, bn, bl, offn, xbar_next, k, j, base, r, na, d.x1[bn + k]);
+  const double xpb = d.tg ? x1b : (me.cap ? x1b : 0.0);  // graft: cap passes through
+  const double dxcb = me.cong ? xpb : 0.0;
+  const double dxfb = me.cong ? 0.0 : xpb;
+  const double gapb = me.gap >= 0.0 ? dxcb * 1.0 : 0.0;
+  // follower's headway term lands on this (leader) slot
+  double tb = 0.0;
+  if (r + 1 < n) {
+    const double xf = pos[k + 1];
+    const CfPick fo = cf_step(xf, x - xf, jam, dxf, len);
+    const double f1b = x1_bar(d, bn, bl, offn, xbar_next, k + 1, j, base, r + 1, na,
+                              d.x1[bn + k + 1]);
+    const double fpb = d.tg ? f1b : (fo.cap ? f1b : 0.0);
+    const double fcb = fo.cong ? fpb : 0.0;
+    tb += (fo.gap >= 0.0 ? fcb * 1.0 : 0.0) * 1.0;
+  }
+  if (r > 0) tb += -(gapb * 1.0);
+  xbar_cur[bn + k] = xpb + tb * 1.0;
+  d.cu[bn + k] = (dxfb * d.dt) * 1.0;
+  d.cg[bn + k] = gapb;
+}
+
+__global__ void __launch_bounds__(256) k_adj_link(DevView d, int s_cur) {
+  const int b = blockIdx.y;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= d.L) return;
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  const int* off = d.off + oidx(d, s_cur, b);
+  const int base = off[j], n = off[j + 1] - base;
+  double ub = 0.0, jb = 0.0;
+  for (int k = base + lane; k < base + n; k += 32) {
+    ub += d.cu[bn + k];
+    jb += -1.0 * d.cg[bn + k];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {  // fixed xor tree: deterministic
+    ub += __shfl_xor_sync(0xffffffffu, ub, o);
+    jb += __shfl_xor_sync(0xffffffffu, jb, o);
+  }
+  if (lane) return;
+  double* g = d.grads + static_cast<std::size_t>(b) * 5 * d.L;
+  const double kap = d.kappa[bl + j];
+  if (n) {
+    g[j] += 0.0 + ub;
+    g[d.L + j] += 0.0 - jb * static_cast<double>(d.delta_n) / (kap * kap);
+  }
+  // pref_bar_j from the link-choice rows of arrived heads on predecessor links
+  double pb = 0.0;
+  for (int e = d.pred_off[j]; e < d.pred_off[j + 1]; ++e) {
+    const int p = d.pred[e];
+    const int pbse = off[p];
+    if (off[p + 1] == pbse) continue;
+    const int nap = d.nA[bl + p];
+    for (int r = 0; r < nap; ++r) {
+      const int s = pbse + r;
+      if (d.choice[bn + s] >= 0) pb += d.vbar[(bn + s) * d.maxdeg + d.pred_pos[e]] * 1.0;
+    }
+  }
+  const double c = d.cost[bl + j], be = d.beta[bl + j];
+  g[2 * d.L + j] += 0.0 + pb / c;  // pref = beta / cost (tensor.cpp:764-777)
+  g[4 * d.L + j] += 0.0 - pb * be / (c * c);
+  // alpha: prio = matmul(valid, alpha) over this link's candidates
+  double ab = 0.0;
+  if (n) {
+    const int na = d.nA[bl + j];
+    for (int r = 0; r < na; ++r) {
+      const int s = base + r;
+      const int ch = d.choice[bn + s];
+      if (ch >= 0 && d.vac[bl + ch] && d.win[bl + ch] >= 0) ab += 1.0 * d.prio_bar[bn + s];
+    }
+  }
+  g[3 * d.L + j] += ab;
+}
+
+// Compact state of one layout back to agent-id order.
+__global__ void k_gather_state(DevView d, int s, int* link_out, double* pos_out) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= d.N) return;
+  const std::size_t so = sidx(d, s, b);
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  const int a = d.aid[so + k];
+  link_out[bn + a] = d.lnk[so + k];
+  pos_out[bn + a] = d.pos[so + k];
+}
+
+// Per-link derived constants: jam spacing, free-flow advance, link preference.
+__global__ void k_derive(DevView d, double* jam, double* dxf, double* pref) {
+  const int b = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.L) return;
+  const std::size_t i = static_cast<std::size_t>(b) * d.L + j;
+  jam[i] = static_cast<double>(d.delta_n) / d.kappa[i];  // divide(scalar(dn), kappa)
+  dxf[i] = (1.0 * d.u[i]) * d.dt;                        // scale(mul(valid, u), dt)
+  pref[i] = d.beta[i] / d.cost[i];                       // divide(beta, cost)
+}
+
+// ---------------------------------------------------------------------------------
+// launch wrappers
+// ---------------------------------------------------------------------------------
+static inline dim3 grid_n(int n, int bs, int B) { return dim3((n + bs - 1) / bs, B); }
+
+void launch_step_forward(const DevView& d, int t, int s_cur, int s_next,
+                         cudaStream_t st) {
+  k_step_cf<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, t, s_cur);
+  k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 0);
+  k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 0);
+  k_step_transfer<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s_cur, s_next);
+}
+
+void launch_step_backward(const DevView& d, int t, int s_cur, int s_next,
+                          const double* xbar_next, double* xbar_cur,
+                          const double* snap_seed, int snap_k, int K,
+                          unsigned long long* sort_scratch, int force_slow,
+                          cudaStream_t st) {
+  k_step_cf<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, t, s_cur);
+  k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 1);
+  k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 1);
+  k_adj_node<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, s_next, xbar_next,
+                                                      snap_seed, snap_k, K);
+  k_adj_a0<<<d.B, 256, 0, st>>>(d, t, s_cur, s_next, xbar_next, sort_scratch, force_slow);
+  k_adj_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);
+  k_adj_slot<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s_cur, s_next, xbar_next, xbar_cur);
+  k_adj_link<<<grid_n(d.L * 32, 256, d.B), 256, 0, st>>>(d, s_cur);
+}
+
+void launch_adj_init(const DevView& d, int s_fin, const double* x_seed,
+                     double* xbar, const double* cum_seed, cudaStream_t st) {
+  k_adj_init_slots<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s_fin, x_seed, xbar);
+  k_adj_init_links<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, cum_seed);
+}
+
+void launch_gather_state(const DevView& d, int s, int* link_out, double* pos_out,
+                         cudaStream_t st) {
+  k_gather_state<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s, link_out, pos_out);
+}
+
+void launch_derive(const DevView& d, double* jam, double* dxf, double* pref,
+                   cudaStream_t st) {
+  k_derive<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, jam, dxf, pref);
+}
+
+}  // namespace dtg

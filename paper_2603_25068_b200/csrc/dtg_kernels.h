@@ -1,0 +1,26 @@
+// Host-side launch wrappers of dtg_kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "dtg_device.cuh"
+
+namespace dtg {
+
+void launch_step_forward(const DevView& d, int t, int s_cur, int s_next,
+                         cudaStream_t st);
+void launch_step_backward(const DevView& d, int t, int s_cur, int s_next,
+                          const double* xbar_next, double* xbar_cur,
+                          const double* snap_seed, int snap_k, int K,
+                          unsigned long long* sort_scratch, int force_slow,
+                          cudaStream_t st);
+void launch_adj_init(const DevView& d, int s_fin, const double* x_seed,
+                     double* xbar, const double* cum_seed, cudaStream_t st);
+void launch_gather_state(const DevView& d, int s, int* link_out, double* pos_out,
+                         cudaStream_t st);
+void launch_derive(const DevView& d, double* jam, double* dxf, double* pref,
+                   cudaStream_t st);
+
+constexpr int kLaunchesPerForwardStep = 4;
+constexpr int kLaunchesPerBackwardStep = 8;
+
+}  // namespace dtg

@@ -1,0 +1,337 @@
+"""Python host API over the C-ABI (include/dtg.h).
+
+Mirrors the reference's simulator surface for this path
+(/root/reference/proj/include/dtsim/{network,engine}.hpp): build a Scenario
+(network + SimConfig + demand), sample LinkParams, then ``simulate_forward`` /
+``simulate_gradient``.  Every call goes to libdtg.so — the C++ host layer
+builds the CSR network and compact states, the sm_100a kernels run the
+T-step loop and its reverse sweep.  ``Engine`` exposes the level-1 device
+context directly (device-resident benchmarking, custom losses, multi-GPU).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from ._lib import NetDesc, SimConfig, load, ptr, raise_for
+
+PHYSICAL, VIRTUAL_INFLOW, VIRTUAL_OUTFLOW = 0, 1, 2
+
+
+def _f64(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+@dataclass
+class LinkParams:
+    """Per-link parameter vectors (network.hpp:22-28)."""
+
+    u: np.ndarray
+    kappa: np.ndarray
+    beta: np.ndarray
+    alpha: np.ndarray
+    cost: np.ndarray
+
+    def arrays(self):
+        return [np.ascontiguousarray(x, dtype=np.float64) for x in (self.u, self.kappa, self.beta, self.alpha, self.cost)]
+
+    def copy(self) -> "LinkParams":
+        return LinkParams(*[a.copy() for a in self.arrays()])
+
+
+@dataclass
+class Trajectory:
+    """Trajectory (engine.hpp:61-74) with compact states."""
+
+    cum_per_step: np.ndarray  # [T, L]
+    link_final: np.ndarray    # [N]
+    pos_final: np.ndarray     # [N]
+    wall_seconds: float = 0.0
+    states_link: Optional[np.ndarray] = None  # [T, N]
+    states_pos: Optional[np.ndarray] = None
+
+    @property
+    def steps(self) -> int:
+        return self.cum_per_step.shape[0]
+
+    @property
+    def cum_final(self) -> np.ndarray:
+        return self.cum_per_step[-1] if self.steps else np.zeros(self.cum_per_step.shape[1])
+
+
+@dataclass
+class GradResult:
+    """GradResult (engine.hpp:91-99); grads is [5, L] = u, kappa, beta, alpha, cost."""
+
+    loss: float
+    grads: np.ndarray
+    snapshots: np.ndarray
+    cum_final: np.ndarray
+    link_final: np.ndarray
+    pos_final: np.ndarray
+    wall_seconds: float = 0.0
+
+    @property
+    def as_params(self) -> LinkParams:
+        return LinkParams(*self.grads)
+
+
+class Scenario:
+    """Scenario (engine.hpp:16-34): network, SimConfig and demand."""
+
+    def __init__(self, handle):
+        self._lib = load()
+        if not handle:
+            raise RuntimeError(self._lib.dtg_scenario_last_error(None).decode())
+        self._h = handle
+        self.horizon_steps = 0
+        self.delta_n = 1
+        self.tau = 1.0
+        self.obs_interval_s = 300
+
+    def __del__(self):
+        try:
+            self._lib.dtg_scenario_free(self._h)
+        except Exception:
+            pass
+
+    # ---- construction ----------------------------------------------------------
+    @classmethod
+    def grid(cls, n: int, length: float, net_seed: int = 42, virtual_length: float = 1000.0) -> "Scenario":
+        """Synthetic n x n grid + attach_virtual_links."""
+        return cls(load().dtg_scenario_grid(n, float(length), net_seed, float(virtual_length)))
+
+    @classmethod
+    def from_links(cls, n_nodes: int, from_node, to_node, length, kind) -> "Scenario":
+        """make_network (network.cpp:238-247) over explicit links."""
+        f = np.ascontiguousarray(from_node, np.int32)
+        return cls(load().dtg_scenario_from_links(n_nodes, len(f), f, np.ascontiguousarray(to_node, np.int32),
+                                                  _f64(length), np.ascontiguousarray(kind, np.int32)))
+
+    @classmethod
+    def tntp(cls, text: str, length_unit_scale: float, net_seed: int = 42,
+             virtual_length: float = 1000.0) -> "Scenario":
+        return cls(load().dtg_scenario_tntp(text.encode(), float(length_unit_scale), net_seed,
+                                            float(virtual_length)))
+
+    def _check(self, rc):
+        raise_for(rc, self._lib.dtg_scenario_last_error(self._h).decode())
+
+    def configure(self, n_vehicles: int = 0, delta_n: int = 1, horizon_steps: int = 0,
+                  obs_interval_s: int = 300, tau: float = 1.0, gumbel_tau: float = 0.01,
+                  trajectory_grafting: bool = True, fit_queues: bool = True,
+                  custom_init=None) -> "Scenario":
+        if custom_init is not None:
+            lk, ps = custom_init
+            self._check(self._lib.dtg_scenario_custom_init(self._h, len(lk), np.ascontiguousarray(lk, np.int32),
+                                                           _f64(ps)))
+        self._check(self._lib.dtg_scenario_configure(self._h, n_vehicles, delta_n, tau, gumbel_tau,
+                                                     int(trajectory_grafting), horizon_steps, obs_interval_s,
+                                                     int(fit_queues)))
+        self.horizon_steps, self.delta_n, self.tau, self.obs_interval_s = horizon_steps, delta_n, tau, obs_interval_s
+        self.gumbel_tau, self.trajectory_grafting = gumbel_tau, trajectory_grafting
+        return self
+
+    # ---- queries -----------------------------------------------------------------
+    @property
+    def n_links(self) -> int:
+        return self._lib.dtg_scenario_n_links(self._h)
+
+    @property
+    def n_nodes(self) -> int:
+        return self._lib.dtg_scenario_n_nodes(self._h)
+
+    @property
+    def n_agents(self) -> int:
+        n = self._lib.dtg_scenario_n_agents(self._h)
+        if n < 0:
+            raise RuntimeError(self._lib.dtg_scenario_last_error(self._h).decode())
+        return n
+
+    @property
+    def steps_per_interval(self) -> int:
+        return int(round(self.obs_interval_s / (self.tau * self.delta_n)))
+
+    @property
+    def n_snapshots(self) -> int:
+        return self.horizon_steps // self.steps_per_interval
+
+    def links(self):
+        L = self.n_links
+        f, t, k = (np.zeros(L, np.int32) for _ in range(3))
+        ln = np.zeros(L)
+        self._lib.dtg_scenario_links(self._h, f, t, ln, k)
+        return f, t, ln, k
+
+    def csr(self):
+        off = np.zeros(self.n_links + 1, np.int32)
+        succ = np.zeros(max(1, self._lib.dtg_scenario_n_edges(self._h)), np.int32)
+        self._lib.dtg_scenario_csr(self._h, off, succ)
+        return off, succ[: off[-1]]
+
+    def sample_parameters(self, seed: int, mean_mode: bool = False) -> LinkParams:
+        L = self.n_links
+        a = [np.zeros(L) for _ in range(5)]
+        self._check(self._lib.dtg_scenario_sample_parameters(self._h, seed, int(mean_mode), *a))
+        return LinkParams(*a)
+
+    def seed_agents(self):
+        N = self.n_agents
+        lk, ps = np.zeros(N, np.int32), np.zeros(N)
+        self._check(self._lib.dtg_scenario_seed_agents(self._h, lk, ps))
+        return lk, ps
+
+    def device_context(self):
+        return self._lib.dtg_scenario_ctx(self._h)
+
+
+def steps_for_minutes(delta_n: int, tau: float, minutes: float) -> int:
+    n = load().dtg_steps_for_minutes(delta_n, tau, minutes)
+    if n < 0:
+        raise RuntimeError("horizon must be a whole number of time steps")
+    return n
+
+
+def _its(noise_iteration, noise_iterations):
+    its = [noise_iteration] if noise_iterations is None else list(noise_iterations)
+    return np.ascontiguousarray(its, dtype=np.uint64)
+
+
+def simulate_forward(sc: Scenario, params: LinkParams, seed: int, noise_iteration: int = 0,
+                     record_states: bool = False, noise_iterations: Optional[Sequence[int]] = None):
+    """simulate_forward (engine.cpp:227-254) on the GPU.  With noise_iterations,
+    all draws run batched in one device pass and a list is returned."""
+    its = _its(noise_iteration, noise_iterations)
+    D, T, L, N = len(its), sc.horizon_steps, sc.n_links, sc.n_agents
+    cum = np.zeros((D, T, L))
+    lk, ps = np.zeros((D, N), np.int32), np.zeros((D, N))
+    sl = np.zeros((D, T, N), np.int32) if record_states else None
+    sp = np.zeros((D, T, N)) if record_states else None
+    wall = np.zeros(1)
+    sc._check(sc._lib.dtg_simulate_forward(sc._h, *params.arrays(), seed, D, its, ptr(cum), ptr(lk), ptr(ps),
+                                           ptr(sl), ptr(sp), ptr(wall)))
+    out = [Trajectory(cum[d], lk[d], ps[d], float(wall[0]),
+                      None if sl is None else sl[d], None if sp is None else sp[d]) for d in range(D)]
+    return out if noise_iterations is not None else out[0]
+
+
+def simulate_gradient(sc: Scenario, params: LinkParams, seed: int, ws=None, qs=None, wc=None, qc=None,
+                      wx=None, noise_iteration: int = 0, noise_iterations: Optional[Sequence[int]] = None):
+    """simulate_gradient (engine.cpp:303-429, Checkpointed) with the loss
+    sum_k <ws_k, s_k> + 1/2 <qs_k, s_k^2> + <wc, c> + 1/2 <qc, c^2> + <wx, x_final>."""
+    its = _its(noise_iteration, noise_iterations)
+    D, L, N, K = len(its), sc.n_links, sc.n_agents, sc.n_snapshots
+    ws, qs, wc, qc, wx = (None if a is None else _f64(a).ravel() for a in (ws, qs, wc, qc, wx))
+    loss = np.zeros(D)
+    grads = np.zeros((D, 5, L))
+    snaps = np.zeros((D, K, L))
+    cumf = np.zeros((D, L))
+    lk, ps = np.zeros((D, N), np.int32), np.zeros((D, N))
+    wall = np.zeros(1)
+    sc._check(sc._lib.dtg_simulate_gradient(sc._h, *params.arrays(), seed, D, its, ptr(ws), ptr(qs), ptr(wc),
+                                            ptr(qc), ptr(wx), ptr(loss), ptr(grads), ptr(snaps), ptr(cumf),
+                                            ptr(lk), ptr(ps), ptr(wall)))
+    out = [GradResult(float(loss[d]), grads[d], snaps[d], cumf[d], lk[d], ps[d], float(wall[0])) for d in range(D)]
+    return out if noise_iterations is not None else out[0]
+
+
+def simulate_gradient_mse(sc: Scenario, params: LinkParams, seed: int, obs_ids, obs_values,
+                          noise_iterations: Sequence[int] = (0,)):
+    """simulate_gradient with mse_loss_builder (optimization.cpp:84-101)."""
+    its = _its(0, noise_iterations)
+    D, L = len(its), sc.n_links
+    obs_ids = np.ascontiguousarray(obs_ids, np.int32)
+    obs_values = np.ascontiguousarray(obs_values, np.float64)
+    loss = np.zeros(D)
+    grads = np.zeros((D, 5, L))
+    sc._check(sc._lib.dtg_simulate_gradient_mse(sc._h, *params.arrays(), seed, D, its, len(obs_ids), obs_ids,
+                                                obs_values.shape[0], obs_values.ravel(), ptr(loss), ptr(grads)))
+    return loss, grads
+
+
+class Engine:
+    """Level-1 device context: B scenarios of one network on one GPU."""
+
+    def __init__(self, sc: Scenario, n_scenarios: int = 1, max_steps: int = 1):
+        self._lib = load()
+        off, succ = sc.csr()
+        _, _, length, _ = sc.links()
+        self._keep = (off, succ, length)
+        nd = NetDesc(sc.n_links, off.ctypes.data, succ.ctypes.data, length.ctypes.data)
+        cfg = SimConfig(sc.delta_n, sc.tau, 99999.0, getattr(sc, "gumbel_tau", 0.01),
+                        int(getattr(sc, "trajectory_grafting", True)))
+        h = C.c_void_p()
+        rc = self._lib.dtg_create(C.byref(nd), C.byref(cfg), sc.n_agents, n_scenarios, max_steps, C.byref(h))
+        raise_for(rc, self._lib.dtg_last_error(None).decode())
+        self._h = h
+        self.L, self.N, self.B = sc.n_links, sc.n_agents, n_scenarios
+        self.T = 0
+
+    def __del__(self):
+        try:
+            self._lib.dtg_destroy(self._h)
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        raise_for(rc, self._lib.dtg_last_error(self._h).decode())
+
+    def set_stream(self, stream_ptr: int):
+        self._check(self._lib.dtg_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    def set_graphs(self, on: bool):
+        self._check(self._lib.dtg_set_graphs(self._h, int(on)))
+
+    def force_slow_path(self, on: bool):
+        self._check(self._lib.dtg_debug_force_slow_path(self._h, int(on)))
+
+    def set_params(self, p: LinkParams, scenario: int = -1):
+        self._check(self._lib.dtg_set_params(self._h, scenario, *p.arrays()))
+
+    def set_state(self, link, pos, scenario: int = -1):
+        self._check(self._lib.dtg_set_state(self._h, scenario, np.ascontiguousarray(link, np.int32), _f64(pos)))
+
+    def set_noise(self, root_seed: int, noise_iteration: int, scenario: int = -1):
+        self._check(self._lib.dtg_set_noise(self._h, scenario, root_seed, noise_iteration))
+
+    def forward(self, T: int, steps_per_interval: int, checkpoint: bool = False):
+        self._check(self._lib.dtg_forward(self._h, T, steps_per_interval, int(checkpoint)))
+        self.T = T
+
+    def sync(self):
+        self._check(self._lib.dtg_sync(self._h))
+
+    def read_cum(self, scenario: int = 0) -> np.ndarray:
+        out = np.zeros((self.T, self.L))
+        self._check(self._lib.dtg_read_cum(self._h, scenario, out))
+        return out
+
+    def read_state(self, scenario: int = 0, step: int = -1):
+        lk, ps = np.zeros(self.N, np.int32), np.zeros(self.N)
+        self._check(self._lib.dtg_read_state(self._h, scenario, step, lk, ps))
+        return lk, ps
+
+    @property
+    def n_snapshots(self) -> int:
+        return self._lib.dtg_n_snapshots(self._h)
+
+    def backward(self, snap_seeds=None, cum_seeds=None, x_seeds=None) -> np.ndarray:
+        grads = np.zeros((self.B, 5, self.L))
+        a = [None if s is None else _f64(s).ravel() for s in (snap_seeds, cum_seeds, x_seeds)]
+        self._check(self._lib.dtg_backward(self._h, ptr(a[0]), ptr(a[1]), ptr(a[2]), grads))
+        return grads
+
+    def backward_device(self, d_snap, d_cum, d_x, d_grads):
+        """Device pointers (ints, e.g. torch.Tensor.data_ptr()); no host sync."""
+        self._check(self._lib.dtg_backward_device(self._h, C.c_void_p(d_snap), C.c_void_p(d_cum),
+                                                  C.c_void_p(d_x), C.c_void_p(d_grads)))
+
+    def device_cum_ptr(self) -> int:
+        return self._lib.dtg_device_cum(self._h) or 0
+
+    @property
+    def last_launches(self) -> int:
+        return int(self._lib.dtg_last_launches(self._h))
