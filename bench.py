@@ -1,0 +1,515 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path — one JSON line (rank 0).
+
+Workload (BASELINE.json configs[2]): synthetic
+Chicago-scale 23x23 grid (2,553 links incl. virtual, 1,609.34 m links),
+1,000,020 vehicles, platoon dn = 30 (33,334 agents), 1-hour forward nowcast
+(120 engine steps of 30 s), parameters sample_parameters(RngStream(3)),
+simulation RngStream(7).  A bench "step" is one full 1-hour nowcast of
+``--scenarios`` independent stochastic scenarios per GPU (noise iteration =
+rank * B + b).
+
+metric: real-time factor = simulated scenario-seconds / wall second, summed
+over all GPUs (weak scaling: fixed scenarios per GPU).  `value` is the
+device-resident number (inputs in HBM, CUDA events on the launching stream,
+max over ranks, L2 flushed between timed iterations); `e2e` is the same
+metric through the C-ABI scenario call (dtg_simulate_forward) with host
+buffers: host seeding + H2D of parameters/state + the run + D2H of all
+per-step counts and the final state.  `gradient` reports the paper's second
+number: forward + adjoint gradient s/iter of the 30-min calibration window
+(C4: 60 steps, 8 noise draws sharded over the GPUs, MSE loss, NCCL gather of
+the per-draw gradients + fixed-order sum, AdamW on the raw parameters).
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, built
+from /root/reference sources; falls back to the C port) on the same workload,
+rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+# ---- workload -------------------------------------------------------------------
+GRID_N, LINK_LEN, NET_SEED, VIRT_LEN = 23, 1609.34, 42, 1000.0
+VEHICLES, DELTA_N, HORIZON_MIN, OBS_S = 1_000_020, 30, 60, 300
+PARAM_SEED, SIM_SEED = 3, 7
+DT = 1.0 * DELTA_N
+T_STEPS = int(HORIZON_MIN * 60 / DT)  # 120
+SPI = int(OBS_S / DT)  # 10
+SIM_SECONDS = HORIZON_MIN * 60.0
+CAL_MIN, CAL_DRAWS = 30, 8
+METRIC = "real-time factor, 1M-vehicle Chicago-scale synthetic net (C3), 1-h forward nowcast"
+UNIT = "x real time (simulated scenario-s per wall-s, all GPUs)"
+
+
+def config_dict(B, n_gpus):
+    return {
+        "workload": "C3 nowcast: 23x23 grid, 2553 links, 1000020 veh, dn=30 (33334 agents), "
+                    "120 steps x 30 s (1 h)",
+        "scenarios_per_gpu": B,
+        "n_links": 2553,
+        "n_agents": 33334,
+        "steps_per_nowcast": T_STEPS,
+        "parallelism": f"scenario-parallel x{n_gpus} (replicas; no data-path collective)",
+        "l2": "flushed between timed iterations (256 MiB write)",
+        "gradient_workload": "C4: same net, 30-min window (60 steps), 8 draws, MSE loss",
+    }
+
+
+def build_scenario(P, horizon_steps=T_STEPS):
+    sc = P.Scenario.grid(GRID_N, LINK_LEN, NET_SEED, VIRT_LEN).configure(
+        VEHICLES, DELTA_N, horizon_steps, OBS_S)
+    return sc
+
+
+# ---- clocks -----------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- roofline bookkeeping ------------------------------------------------
+# algorithmic bytes per launch = per-agent bytes x agents + per-link bytes x links
+ALG_BYTES = {
+    "k_step_cf": (16, 64),        # read x, write x1 (SURVEY §8d forward figure); link params/counts
+    "k_step_merge": (0, 64),      # per-link count/cum/vacancy/merge state
+    "k_step_scan": (0, 24),       # per-link sizes, departures, next offsets
+    "k_step_transfer": (16, 16),  # read x1, write next x; per-link offsets
+}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+# ---- CPU baseline (the reference build, or the C port) ---------------------------------
+def cpu_reference_rtf(max_samples=1, use_ref=True):
+    """Steady-state real-time factor of the reference on C3: per-step cost from
+    a horizon-0 run (setup only) and horizon-1 runs on one host core."""
+    from oracle.oracle import REF_SO, PortLib, PortScenario, RefLib, RefScenario
+
+    if use_ref and os.path.exists(REF_SO):
+        R = RefLib()
+        kind = "reference"
+
+        def make(T):
+            return RefScenario.grid(R, GRID_N, LINK_LEN, NET_SEED, VIRT_LEN).configure(VEHICLES, DELTA_N, T, OBS_S)
+
+        s0 = make(0)
+        p = s0.sample_parameters(PARAM_SEED)
+        t = time.perf_counter()
+        s0.forward(p, SIM_SEED, 0)
+        setup = time.perf_counter() - t
+        s1 = make(1)
+        walls = []
+        for i in range(max_samples):
+            t = time.perf_counter()
+            s1.forward(p, SIM_SEED, i)
+            walls.append(time.perf_counter() - t)
+        step = max(1e-9, statistics.mean(walls) - setup)
+        sample = (f"C3 reference simulate_forward: horizon 0 (setup {setup:.2f} s) and {max_samples} x horizon 1 "
+                  f"on 1 core; steady per-step {step:.2f} s (30 simulated s)")
+        return DT / step, kind, sample, step, setup
+    import paper_2603_25068_b200 as P
+
+    PL = PortLib()
+    sc = build_scenario(P)
+    f, t_, ln, _ = sc.links()
+    lk, ps = sc.seed_agents()
+    p = sc.sample_parameters(PARAM_SEED)
+    port = PortScenario(PL, f, t_, ln, link0=lk, pos0=ps, delta_n=DELTA_N, horizon_steps=T_STEPS,
+                        obs_interval_s=OBS_S)
+    t = time.perf_counter()
+    port.forward(p, SIM_SEED, 0)
+    w = time.perf_counter() - t
+    return SIM_SECONDS / w, "port", f"C3 1-h forward of the C port on 1 core ({w:.2f} s)", w / T_STEPS, 0.0
+
+
+# ---- distributed helpers ---------------------------------------------------------------
+def dist_setup(n_gpus):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---- our arm -------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    import paper_2603_25068_b200 as P
+
+    world, rank, local = dist_setup(args.gpus)
+    B = args.scenarios
+    sc = build_scenario(P)
+    p = sc.sample_parameters(PARAM_SEED)
+    lk0, ps0 = sc.seed_agents()
+    N, L = sc.n_agents, sc.n_links
+
+    stream = torch.cuda.Stream()  # a real stream handle (the legacy default is 0)
+    torch.cuda.set_stream(stream)
+    eng = P.Engine(sc, n_scenarios=B, max_steps=T_STEPS)
+    eng.set_stream(stream.cuda_stream)
+    eng.set_params(p)
+    eng.set_state(lk0, ps0)
+    for b in range(B):
+        eng.set_noise(SIM_SEED, rank * B + b, b)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    for _ in range(max(3, args.warmup)):
+        eng.forward(T_STEPS, SPI, checkpoint=False)
+    eng.sync()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            eng.forward(T_STEPS, SPI, checkpoint=False)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    eng.sync()
+    launches_per_step = eng.last_launches
+    dev_s = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / 1e3
+    dev_s = max_over_ranks(dev_s, world)
+    ms_per_step = dev_s / args.steps * 1e3
+    value = world * B * SIM_SECONDS / (dev_s / args.steps)
+    single_rtf = SIM_SECONDS / (dev_s / args.steps)
+
+    # per-kernel attribution with CUDA events on the launching stream
+    ker_ms, _ = eng.profile_kernels(T_STEPS, SPI)
+    total = sum(ker_ms.values())
+    dom = max(ker_ms, key=ker_ms.get)
+    per_launch_s = ker_ms[dom] / 1e3 / T_STEPS
+    ba, bl = ALG_BYTES[dom]
+    alg_bytes = B * (ba * N + bl * L)
+    peak, peak_kind = measured_peak_hbm()
+    achieved = alg_bytes / per_launch_s / 1e9
+    traffic = ncu_traffic(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                "alg_bytes_per_launch": alg_bytes, "avg_launch_us": per_launch_s * 1e6,
+                "share_of_step": ker_ms[dom] / total,
+                "kernel_ms_per_nowcast": {k: round(v, 4) for k, v in ker_ms.items()}}
+
+    # e2e through the C-ABI scenario call with host buffers
+    its = [rank * B + b for b in range(B)]
+    P.simulate_forward(sc, p, seed=SIM_SEED, noise_iterations=its)  # warm (context + graph)
+    e2e_times = []
+    for _ in range(max(3, args.steps // 2)):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        P.simulate_forward(sc, p, seed=SIM_SEED, noise_iterations=its)
+        e2e_times.append(time.perf_counter() - t)
+    e2e_s = max_over_ranks(statistics.mean(e2e_times), world)
+    h2d = B * (5 * L * 8 + N * (8 + 4 + 4) + (L + 1) * 4 + L * 8) + 16 * B
+    d2h = B * (T_STEPS * L * 8 + N * (4 + 8)) + 4 * B
+    e2e = {"value": world * B * SIM_SECONDS / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "s_per_call": e2e_s,
+           "path": "dtg_simulate_forward (C-ABI, host buffers, synchronous)"}
+
+    grad = run_gradient(P, torch, world, rank, args)
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, kind, sample, step_s, setup = cpu_reference_rtf()
+            cpu = {"value": v, "unit": "x real time (1 scenario, 1 core)", "cores": 1, "kind": kind,
+                   "sample": sample, "est_full_hour_s": setup + T_STEPS * step_s}
+        out = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(3, args.warmup),
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (SURVEY §8d grid generator, sampled parameters, seeded demand)",
+            "config": config_dict(B, world),
+            "single_scenario_rtf": single_rtf,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "gradient": grad,
+        }
+        print(json.dumps(out), flush=True)
+    barrier(world)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return out
+
+
+def run_gradient(P, torch, world, rank, args):
+    """C4 calibration iteration: forward(ckpt)+adjoint of 8 draws sharded over
+    the GPUs, MSE loss seeds on the host (the reference's host loss tape,
+    engine.cpp:369-385), NCCL gather + fixed-order sum, AdamW step."""
+    if args.no_gradient:
+        return None
+    T = int(CAL_MIN * 60 / DT)  # 60
+    draws_per_rank = max(1, CAL_DRAWS // world)
+    sc = build_scenario(P, horizon_steps=T)
+    truth = sc.sample_parameters(NET_SEED)  # truth = sample_parameters(root)
+    start = sc.sample_parameters(0, mean_mode=True)  # calibration start = midpoints
+    L, N = sc.n_links, sc.n_agents
+    K = T // SPI
+    obs_ids = np.array([j for j in range(L) if j % 5 != 0], dtype=np.int32)
+    tr = P.simulate_forward(sc, truth, seed=SIM_SEED)
+    obs_vals = tr.cum_per_step[SPI - 1::SPI][:K][:, obs_ids] * DELTA_N
+    lk0, ps0 = sc.seed_agents()
+    eng = P.Engine(sc, n_scenarios=draws_per_rank, max_steps=T)
+    eng.set_stream(torch.cuda.current_stream().cuda_stream)
+    eng.set_state(lk0, ps0)
+    lo = np.array([13.9, 0.18, 0.0, 0.01])
+    hi = np.array([22.2, 0.22, 5.0, 5.0])
+    raw = np.zeros((4, L))
+    m = np.zeros_like(raw)
+    v = np.zeros_like(raw)
+    sc_loss = 1.0 / (K * len(obs_ids))
+
+    def iteration(it):
+        s = np.where(raw >= 0, 1.0 / (1.0 + np.exp(-raw)), np.exp(raw) / (1.0 + np.exp(raw)))
+        vals = lo[:, None] + (hi - lo)[:, None] * s
+        params = P.LinkParams(vals[0], vals[1], vals[2], vals[3], start.cost)
+        eng.set_params(params)
+        for b in range(draws_per_rank):
+            eng.set_noise(SIM_SEED, it * CAL_DRAWS + rank * draws_per_rank + b + 1, b)
+        eng.forward(T, SPI, checkpoint=True)
+        seeds = np.zeros((draws_per_rank, K, L))
+        for b in range(draws_per_rank):
+            cum = eng.read_cum(b)
+            snaps = cum[SPI - 1::SPI][:K]
+            d = snaps[:, obs_ids] * DELTA_N - obs_vals
+            seeds[b][:, obs_ids] = ((0.0 + sc_loss * d) + sc_loss * d) * DELTA_N
+        g = eng.backward(snap_seeds=seeds)  # [draws, 5, L]
+        gt = torch.from_numpy(g).cuda()
+        if world > 1:
+            import torch.distributed as dist
+
+            allg = [torch.empty_like(gt) for _ in range(world)]
+            dist.all_gather(allg, gt)
+            gt = torch.cat(allg)
+        gsum = gt[0].clone()
+        for q in range(1, gt.shape[0]):  # fixed draw order (optimization.cpp:181-190)
+            gsum += gt[q]
+        gsum = gsum.cpu().numpy()
+        ds = (hi - lo)[:, None] * s * (1.0 - s)
+        rg = gsum[:4] / CAL_DRAWS * ds
+        t_ = it + 1
+        m[:] = 0.9 * m + 0.1 * rg
+        v[:] = 0.999 * v + 0.001 * rg * rg
+        raw[:] -= 0.1 * ((m / (1 - 0.9 ** t_)) / (np.sqrt(v / (1 - 0.999 ** t_)) + 1e-8) + 1e-5 * raw)
+
+    for it in range(2):
+        iteration(it)
+    n_it = max(3, args.steps // 4)
+    barrier(world)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for it in range(2, 2 + n_it):
+        iteration(it)
+    torch.cuda.synchronize()
+    s_iter = max_over_ranks((time.perf_counter() - t) / n_it, world)
+    ker_f, _ = eng.profile_kernels(T, SPI)
+    eng.forward(T, SPI, checkpoint=True)
+    ker_b, _ = eng.profile_kernels(T, SPI, backward=True)
+    return {"s_per_iter": s_iter, "draws": CAL_DRAWS, "draws_per_gpu": draws_per_rank, "steps": T,
+            "iterations_timed": n_it, "params": 4 * L,
+            "projected_200_iter_s": 200 * s_iter,
+            "paper_calibration_s": 455.3,
+            "fwd_ms_per_pass": sum(ker_f.values()), "adj_ms_per_pass": sum(ker_b.values()),
+            "adj_kernel_ms": {k: round(x, 4) for k, x in ker_b.items()},
+            "timing": "wall clock per full iteration (host loss + H2D/D2H + NCCL + AdamW included)"}
+
+
+# ---- reference arm -----------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle.oracle import REF_SO, RefLib, RefScenario
+
+    if not os.path.exists(REF_SO):
+        v, kind, sample, step_s, setup = cpu_reference_rtf(use_ref=False)
+        walls = []
+    else:
+        R = RefLib()
+        kind = "reference"
+
+        def make(T):
+            return RefScenario.grid(R, GRID_N, LINK_LEN, NET_SEED, VIRT_LEN).configure(VEHICLES, DELTA_N, T, OBS_S)
+
+        s0, s1 = make(0), make(1)
+        p = s0.sample_parameters(PARAM_SEED)
+        setups = []
+        for _ in range(max(3, args.warmup)):  # warm-up: setup-only runs (horizon 0)
+            t = time.perf_counter()
+            s0.forward(p, SIM_SEED, 0)
+            setups.append(time.perf_counter() - t)
+        setup = min(setups)
+        walls = []
+        for i in range(args.steps):  # timed: one 30-s engine step each (horizon 1)
+            t = time.perf_counter()
+            s1.forward(p, SIM_SEED, i)
+            walls.append(time.perf_counter() - t)
+        step_s = max(1e-9, statistics.mean(walls) - setup)
+        v = DT / step_s
+        sample = (f"C3 reference simulate_forward, {args.steps} x horizon-1 runs minus the horizon-0 setup "
+                  f"({setup:.2f} s): steady per-step {step_s:.2f} s per 30 simulated s, 1 core "
+                  f"(the reference is single-threaded)")
+    out = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": v,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": step_s * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (SURVEY §8d grid generator, sampled parameters, seeded demand)",
+        "config": config_dict(1, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "est_full_hour_s": setup + T_STEPS * step_s,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scenarios", type=int, default=1, help="independent scenarios per GPU")
+    ap.add_argument("--no-gradient", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -137,6 +137,15 @@ int dtg_backward_device(dtg_ctx* ctx, const double* d_snap_seeds,
                         const double* d_cum_seeds, const double* d_x_seeds,
                         double* d_grads);
 
+/* Measurement hook: run n_steps of the forward (backward != 0: the reverse
+ * sweep of the preceding checkpointed forward) without graphs, bracketing
+ * every kernel with CUDA events on the context stream.  ms_out[w] receives
+ * the summed duration of kernel kind w (4 forward / 8 reverse kinds, named by
+ * dtg_kernel_name); launches_out the number of kernels launched. */
+int dtg_profile_kernels(dtg_ctx* ctx, int n_steps, int steps_per_interval,
+                        int backward, double* ms_out, int64_t* launches_out);
+const char* dtg_kernel_name(int backward, int which);
+
 /* Device pointer to the cumulative-count history [n_steps + 1][B][L]
  * (row 0 = zeros) of the last forward, valid until the next forward. */
 const double* dtg_device_cum(const dtg_ctx* ctx);

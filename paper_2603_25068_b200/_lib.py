@@ -76,6 +76,8 @@ SIGNATURES = [
     ("dtg_backward", i32, [vp, vp, vp, vp, _dp]),
     ("dtg_backward_device", i32, [vp, vp, vp, vp, vp]),
     ("dtg_device_cum", vp, [vp]),
+    ("dtg_profile_kernels", i32, [vp, i32, i32, i32, _dp, C.POINTER(C.c_int64)]),
+    ("dtg_kernel_name", C.c_char_p, [i32, i32]),
     ("dtg_last_launches", C.c_int64, [vp]),
     ("dtg_scenario_from_links", vp, [i32, i32, _ip, _ip, _dp, _ip]),
     ("dtg_scenario_grid", vp, [i32, C.c_double, u64, C.c_double]),

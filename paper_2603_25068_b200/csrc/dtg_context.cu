@@ -4,6 +4,7 @@
 // CUDA graphs of the whole T-step forward and reverse sweeps (one graph launch
 // per simulate call instead of 4T / 8T kernel launches).
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -657,6 +658,109 @@ int dtg_backward_device(dtg_ctx* c, const double* snap, const double* cum, const
     const std::size_t n = static_cast<std::size_t>(c->B) * 5 * c->L;
     CK(cudaMemcpyAsync(d_grads, c->grads.p, n * 8, cudaMemcpyDeviceToDevice, c->stream));
   });
+}
+
+int dtg_profile_kernels(dtg_ctx* c, int T, int spi, int backward, double* ms_out,
+                        int64_t* launches_out) {
+  return guarded(c, [&] {
+    if (T < 1) throw std::invalid_argument("profile needs at least one step");
+    c->sync_check();
+    // The launch sequence is captured into a CUDA graph with an event record
+    // node before and after every kernel, so kernels run back to back exactly
+    // as in the production graph and each event pair brackets one kernel.
+    const int nk = backward ? dtg::kBwdKernels : dtg::kFwdKernels;
+    for (int w = 0; w < nk; ++w) ms_out[w] = 0.0;
+    cudaStream_t st = c->stream;
+    std::vector<cudaEvent_t> ev(2 * static_cast<std::size_t>(nk) * T);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    struct EvGuard {
+      std::vector<cudaEvent_t>& v;
+      ~EvGuard() {
+        for (auto e : v) cudaEventDestroy(e);
+      }
+    } guard{ev};
+    std::size_t q = 0;
+    std::int64_t launches = 0;
+    std::function<void()> body;
+    if (!backward) {
+      c->ensure_history(T, 0);
+      CK(cudaMemcpyAsync(c->seeds.p, c->h_seeds.data(), sizeof(std::uint64_t) * 2 * c->B,
+                         cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+      body = [&] {
+        const dtg::DevView d = c->view();
+        const std::size_t BN = static_cast<std::size_t>(c->B) * c->N;
+        const std::size_t BL = static_cast<std::size_t>(c->B) * c->L;
+        dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
+        CK(cudaMemcpyAsync(c->pos.p, c->pos0.p, BN * 8, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(c->aid.p, c->aid0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(c->lnk.p, c->lnk0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(c->off.p, c->off0.p, static_cast<std::size_t>(c->B) * (c->L + 1) * 4,
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(c->qh.p, c->q0.p, BL * 8, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemsetAsync(c->cumh.p, 0, BL * 8, st));
+        CK(cudaMemsetAsync(c->errf.p, 0, sizeof(int) * c->B, st));
+        for (int t = 0; t < T; ++t)
+          for (int w = 0; w < nk; ++w) {
+            CK(cudaEventRecordWithFlags(ev[q++], st, cudaEventRecordExternal));
+            dtg::launch_fwd_kernel(w, d, t, t % c->S, (t + 1) % c->S, st);
+            CK(cudaEventRecordWithFlags(ev[q++], st, cudaEventRecordExternal));
+            ++launches;
+          }
+      };
+      c->last_T = T;
+      c->last_spi = spi;
+      c->last_ckpt = 0;
+      c->last_K = T / spi;
+    } else {
+      if (c->last_T != T || !c->last_ckpt)
+        throw std::runtime_error("profile(backward) needs a preceding dtg_forward(T, checkpoint=1)");
+      run_backward(c, nullptr, nullptr, nullptr, cudaMemcpyHostToDevice);  // allocate + warm
+      c->sync_check();
+      body = [&] {
+        const dtg::DevView d = c->view();
+        const std::size_t B = c->B, N = c->N;
+        const int K = c->last_K;
+        double* xb[2] = {c->xbar.p, c->xbar.p + B * N};
+        dtg::launch_adj_init(d, T % c->S, c->x_seed.p, xb[T & 1], c->cum_seed.p, st);
+        for (int t = T - 1; t >= 0; --t) {
+          const int snap_k = ((t + 1) % spi == 0) ? (t + 1) / spi - 1 : -1;
+          for (int w = 0; w < nk; ++w) {
+            CK(cudaEventRecordWithFlags(ev[q++], st, cudaEventRecordExternal));
+            dtg::launch_bwd_kernel(w, d, t, t % c->S, (t + 1) % c->S, xb[(t + 1) & 1], xb[t & 1],
+                                   c->snap_seed.p, snap_k, K, c->sort_scratch.p, c->force_slow, st);
+            CK(cudaEventRecordWithFlags(ev[q++], st, cudaEventRecordExternal));
+            ++launches;
+          }
+        }
+      };
+    }
+    cudaGraph_t g;
+    cudaGraphExec_t ex = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    body();
+    CK(cudaStreamEndCapture(st, &g));
+    CK(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    CK(cudaGraphLaunch(ex, st));  // warm
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGraphLaunch(ex, st));
+    CK(cudaStreamSynchronize(st));
+    cudaGraphExecDestroy(ex);
+    c->pending = true;
+    c->sync_check();
+    for (std::size_t p = 0; p < q; p += 2) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ev[p], ev[p + 1]));
+      ms_out[(p / 2) % nk] += ms;
+    }
+    if (launches_out) *launches_out = launches;
+  });
+}
+
+const char* dtg_kernel_name(int backward, int which) {
+  if (backward) return which >= 0 && which < dtg::kBwdKernels ? dtg::kBwdKernelNames[which] : "";
+  return which >= 0 && which < dtg::kFwdKernels ? dtg::kFwdKernelNames[which] : "";
 }
 
 int dtg_debug_force_slow_path(dtg_ctx* c, int on) {

@@ -791,12 +791,65 @@ __global__ void k_derive(DevView d, double* jam, double* dxf, double* pref) {
 // ---------------------------------------------------------------------------------
 static inline dim3 grid_n(int n, int bs, int B) { return dim3((n + bs - 1) / bs, B); }
 
+const char* const kFwdKernelNames[kFwdKernels] = {"k_step_cf", "k_step_merge",
+                                                 "k_step_scan", "k_step_transfer"};
+const char* const kBwdKernelNames[kBwdKernels] = {
+    "k_step_cf(replay)", "k_step_merge(replay)", "k_step_scan(replay)", "k_adj_node",
+    "k_adj_a0",          "k_adj_choice",         "k_adj_slot",          "k_adj_link"};
+
+void launch_fwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next,
+                       cudaStream_t st) {
+  switch (which) {
+    case 0:
+      k_step_cf<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, t, s_cur);
+      break;
+    case 1:
+      k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 0);
+      break;
+    case 2:
+      k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 0);
+      break;
+    default:
+      k_step_transfer<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s_cur, s_next);
+  }
+}
+
 void launch_step_forward(const DevView& d, int t, int s_cur, int s_next,
                          cudaStream_t st) {
-  k_step_cf<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, t, s_cur);
-  k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 0);
-  k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 0);
-  k_step_transfer<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s_cur, s_next);
+  for (int w = 0; w < kFwdKernels; ++w) launch_fwd_kernel(w, d, t, s_cur, s_next, st);
+}
+
+void launch_bwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next,
+                       const double* xbar_next, double* xbar_cur,
+                       const double* snap_seed, int snap_k, int K,
+                       unsigned long long* sort_scratch, int force_slow,
+                       cudaStream_t st) {
+  switch (which) {
+    case 0:
+      k_step_cf<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, t, s_cur);
+      break;
+    case 1:
+      k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 1);
+      break;
+    case 2:
+      k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 1);
+      break;
+    case 3:
+      k_adj_node<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, s_next, xbar_next,
+                                                          snap_seed, snap_k, K);
+      break;
+    case 4:
+      k_adj_a0<<<d.B, 256, 0, st>>>(d, t, s_cur, s_next, xbar_next, sort_scratch, force_slow);
+      break;
+    case 5:
+      k_adj_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);
+      break;
+    case 6:
+      k_adj_slot<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s_cur, s_next, xbar_next, xbar_cur);
+      break;
+    default:
+      k_adj_link<<<grid_n(d.L * 32, 256, d.B), 256, 0, st>>>(d, s_cur);
+  }
 }
 
 void launch_step_backward(const DevView& d, int t, int s_cur, int s_next,
@@ -804,15 +857,9 @@ void launch_step_backward(const DevView& d, int t, int s_cur, int s_next,
                           const double* snap_seed, int snap_k, int K,
                           unsigned long long* sort_scratch, int force_slow,
                           cudaStream_t st) {
-  k_step_cf<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, t, s_cur);
-  k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 1);
-  k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 1);
-  k_adj_node<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, s_next, xbar_next,
-                                                      snap_seed, snap_k, K);
-  k_adj_a0<<<d.B, 256, 0, st>>>(d, t, s_cur, s_next, xbar_next, sort_scratch, force_slow);
-  k_adj_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);
-  k_adj_slot<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s_cur, s_next, xbar_next, xbar_cur);
-  k_adj_link<<<grid_n(d.L * 32, 256, d.B), 256, 0, st>>>(d, s_cur);
+  for (int w = 0; w < kBwdKernels; ++w)
+    launch_bwd_kernel(w, d, t, s_cur, s_next, xbar_next, xbar_cur, snap_seed, snap_k, K,
+                      sort_scratch, force_slow, st);
 }
 
 void launch_adj_init(const DevView& d, int s_fin, const double* x_seed,

@@ -20,7 +20,18 @@ void launch_gather_state(const DevView& d, int s, int* link_out, double* pos_out
 void launch_derive(const DevView& d, double* jam, double* dxf, double* pref,
                    cudaStream_t st);
 
-constexpr int kLaunchesPerForwardStep = 4;
-constexpr int kLaunchesPerBackwardStep = 8;
+constexpr int kFwdKernels = 4;
+constexpr int kBwdKernels = 8;
+constexpr int kLaunchesPerForwardStep = kFwdKernels;
+constexpr int kLaunchesPerBackwardStep = kBwdKernels;
+extern const char* const kFwdKernelNames[kFwdKernels];
+extern const char* const kBwdKernelNames[kBwdKernels];
+void launch_fwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next,
+                       cudaStream_t st);
+void launch_bwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next,
+                       const double* xbar_next, double* xbar_cur,
+                       const double* snap_seed, int snap_k, int K,
+                       unsigned long long* sort_scratch, int force_slow,
+                       cudaStream_t st);
 
 }  // namespace dtg

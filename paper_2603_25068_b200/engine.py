@@ -280,6 +280,11 @@ class Engine:
         raise_for(rc, self._lib.dtg_last_error(self._h).decode())
 
     def set_stream(self, stream_ptr: int):
+        """Run on this cudaStream_t (e.g. torch.cuda.Stream().cuda_stream).  The
+        legacy default stream (handle 0) is rejected: the context would keep its
+        own stream and events on stream 0 would not time it."""
+        if not stream_ptr:
+            raise ValueError("pass a real CUDA stream handle (torch.cuda.Stream()), not the legacy default 0")
         self._check(self._lib.dtg_set_stream(self._h, C.c_void_p(stream_ptr)))
 
     def set_graphs(self, on: bool):
@@ -328,6 +333,16 @@ class Engine:
         """Device pointers (ints, e.g. torch.Tensor.data_ptr()); no host sync."""
         self._check(self._lib.dtg_backward_device(self._h, C.c_void_p(d_snap), C.c_void_p(d_cum),
                                                   C.c_void_p(d_x), C.c_void_p(d_grads)))
+
+    def profile_kernels(self, T: int, steps_per_interval: int, backward: bool = False):
+        """Per-kernel-kind device time (ms, CUDA events) of one forward (or the
+        reverse sweep of the preceding checkpointed forward)."""
+        nk = 8 if backward else 4
+        ms = np.zeros(nk)
+        n = C.c_int64()
+        self._check(self._lib.dtg_profile_kernels(self._h, T, steps_per_interval, int(backward), ms, C.byref(n)))
+        names = [self._lib.dtg_kernel_name(int(backward), w).decode() for w in range(nk)]
+        return dict(zip(names, ms.tolist())), int(n.value)
 
     def device_cum_ptr(self) -> int:
         return self._lib.dtg_device_cum(self._h) or 0
