@@ -111,6 +111,11 @@ int dtg_sync(dtg_ctx* ctx);
  * the first arrived agent (normally used only on near ties). */
 int dtg_debug_force_slow_path(dtg_ctx* ctx, int on);
 
+/* Test hook: n Gumbel draws -log(-log(u)), u = uniform(seed, key, rows[i],
+ * cols[i]), computed by the device code path (libdevice log). */
+int dtg_debug_gumbel(uint64_t seed, uint64_t key, int n, const uint64_t* rows,
+                     const uint64_t* cols, double* out);
+
 /* Results of the last dtg_forward.
  * cum_per_step: n_steps x L cumulative counts (Trajectory::cum_per_step).
  * state: compact (link, pos) per agent after `step` steps (step in
@@ -244,6 +249,11 @@ int dtg_simulate_gradient_mse(dtg_scenario* sc, const double* u,
 /* Device context a scenario uses (for dtg_set_stream / dtg_last_launches);
  * NULL before the first simulate call. */
 dtg_ctx* dtg_scenario_ctx(dtg_scenario* sc);
+/* Host-side calibration loss (mse_loss_builder, optimization.cpp:84-101):
+ * value and adjoint seeds over k_snap snapshots (k_snap x L). */
+int dtg_mse_loss(int k_snap, int n_links, const double* snapshots, int n_obs,
+                 const int* obs_ids, int k_obs, const double* obs_values,
+                 int delta_n, double* loss, double* seeds);
 const char* dtg_scenario_last_error(const dtg_scenario* sc);
 
 #ifdef __cplusplus

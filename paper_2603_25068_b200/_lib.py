@@ -100,6 +100,8 @@ SIGNATURES = [
     ("dtg_simulate_gradient_mse", i32, [vp, _dp, _dp, _dp, _dp, _dp, u64, i32, _u64p,
                                         i32, _ip, i32, _dp, vp, vp]),
     ("dtg_scenario_ctx", vp, [vp]),
+    ("dtg_mse_loss", i32, [i32, i32, _dp, i32, _ip, i32, _dp, i32, _dp, _dp]),
+    ("dtg_debug_gumbel", i32, [u64, u64, i32, _u64p, _u64p, _dp]),
     ("dtg_scenario_last_error", C.c_char_p, [vp]),
 ]
 

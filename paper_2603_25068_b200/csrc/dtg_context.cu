@@ -763,6 +763,22 @@ const char* dtg_kernel_name(int backward, int which) {
   return which >= 0 && which < dtg::kFwdKernels ? dtg::kFwdKernelNames[which] : "";
 }
 
+int dtg_debug_gumbel(uint64_t seed, uint64_t key, int n, const uint64_t* rows,
+                     const uint64_t* cols, double* out) {
+  return guarded(nullptr, [&] {
+    DevBuf<std::uint64_t> r, c;
+    DevBuf<double> o;
+    r.alloc(n);
+    c.alloc(n);
+    o.alloc(n);
+    CK(cudaMemcpy(r.p, rows, n * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c.p, cols, n * 8, cudaMemcpyHostToDevice));
+    dtg::launch_gumbel_batch(seed, key, r.p, c.p, n, o.p, nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, o.p, n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
 int dtg_debug_force_slow_path(dtg_ctx* c, int on) {
   c->force_slow = on ? 1 : 0;
   c->drop_graphs();

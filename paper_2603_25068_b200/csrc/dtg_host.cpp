@@ -955,4 +955,30 @@ int dtg_simulate_gradient_mse(dtg_scenario* sc, const double* u, const double* k
 
 dtg_ctx* dtg_scenario_ctx(dtg_scenario* sc) { return sc->last_ctx; }
 
+int dtg_mse_loss(int k_snap, int n_links, const double* snapshots, int n_obs, const int* obs_ids,
+                 int k_obs, const double* obs_values, int delta_n, double* loss, double* seeds) {
+  try {
+    dtg::CountSeries obs;
+    obs.link_ids.assign(obs_ids, obs_ids + n_obs);
+    for (int q = 0; q < k_obs; ++q)
+      obs.values.emplace_back(obs_values + static_cast<std::size_t>(q) * n_obs,
+                              obs_values + static_cast<std::size_t>(q + 1) * n_obs);
+    std::vector<std::vector<double>> snaps(k_snap);
+    for (int q = 0; q < k_snap; ++q)
+      snaps[q].assign(snapshots + static_cast<std::size_t>(q) * n_links,
+                      snapshots + static_cast<std::size_t>(q + 1) * n_links);
+    const std::vector<double> cf(n_links, 0.0);
+    dtg::LossInputs li{&snaps, &cf, nullptr};
+    const dtg::LossValue lv = dtg::mse_loss_builder(obs, delta_n)(li);
+    *loss = lv.loss;
+    for (int q = 0; q < k_snap; ++q)
+      std::copy(lv.d_snapshots[q].begin(), lv.d_snapshots[q].end(),
+                seeds + static_cast<std::size_t>(q) * n_links);
+    return DTG_OK;
+  } catch (const std::exception& e) {
+    g_scn_error = e.what();
+    return DTG_ERR_RUNTIME;
+  }
+}
+
 }  // extern "C"

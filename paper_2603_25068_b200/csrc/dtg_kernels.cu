@@ -775,6 +775,18 @@ __global__ void k_gather_state(DevView d, int s, int* link_out, double* pos_out)
   pos_out[bn + a] = d.pos[so + k];
 }
 
+// Test hook: Gumbel draws on the device (counter RNG + CUDA libdevice log).
+__global__ void k_gumbel_batch(std::uint64_t seed, std::uint64_t key, const std::uint64_t* rows,
+                               const std::uint64_t* cols, int n, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = gumbel(seed, key, rows[i], cols[i]);
+}
+
+void launch_gumbel_batch(std::uint64_t seed, std::uint64_t key, const std::uint64_t* rows,
+                         const std::uint64_t* cols, int n, double* out, cudaStream_t st) {
+  k_gumbel_batch<<<(n + 255) / 256, 256, 0, st>>>(seed, key, rows, cols, n, out);
+}
+
 // Per-link derived constants: jam spacing, free-flow advance, link preference.
 __global__ void k_derive(DevView d, double* jam, double* dxf, double* pref) {
   const int b = blockIdx.y;

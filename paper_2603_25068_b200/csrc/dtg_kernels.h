@@ -20,6 +20,9 @@ void launch_gather_state(const DevView& d, int s, int* link_out, double* pos_out
 void launch_derive(const DevView& d, double* jam, double* dxf, double* pref,
                    cudaStream_t st);
 
+void launch_gumbel_batch(std::uint64_t seed, std::uint64_t key, const std::uint64_t* rows,
+                         const std::uint64_t* cols, int n, double* out, cudaStream_t st);
+
 constexpr int kFwdKernels = 4;
 constexpr int kBwdKernels = 8;
 constexpr int kLaunchesPerForwardStep = kFwdKernels;
