@@ -356,64 +356,50 @@ def run_ours(args):
 
 
 def run_gradient(P, torch, world, rank, args):
-    """C4 calibration iteration: forward(ckpt)+adjoint of 8 draws sharded over
-    the GPUs, MSE loss seeds on the host (the reference's host loss tape,
-    engine.cpp:369-385), NCCL gather + fixed-order sum, AdamW step."""
+    """C4 calibration iteration (calibrate(), optimization.cpp:122-219): the
+    8 noise draws sharded over the GPUs, each rank's draws in one batched
+    forward(checkpoint) + adjoint pass, MSE loss seeds on the host (the
+    reference's host loss tape, engine.cpp:369-385), NCCL all-gather of the
+    per-draw gradients + fixed-order sum, BoundedTransform chain rule + AdamW."""
     if args.no_gradient:
         return None
+    from paper_2603_25068_b200.dist import ShardedGradient, calibration_draws
+
     T = int(CAL_MIN * 60 / DT)  # 60
-    draws_per_rank = max(1, CAL_DRAWS // world)
     sc = build_scenario(P, horizon_steps=T)
     truth = sc.sample_parameters(NET_SEED)  # truth = sample_parameters(root)
     start = sc.sample_parameters(0, mean_mode=True)  # calibration start = midpoints
-    L, N = sc.n_links, sc.n_agents
+    L = sc.n_links
     K = T // SPI
-    obs_ids = np.array([j for j in range(L) if j % 5 != 0], dtype=np.int32)
+    obs_ids = np.array([j for j in range(L) if j % 5 != 0], dtype=np.int32)  # 80% coverage
     tr = P.simulate_forward(sc, truth, seed=SIM_SEED)
     obs_vals = tr.cum_per_step[SPI - 1::SPI][:K][:, obs_ids] * DELTA_N
-    lk0, ps0 = sc.seed_agents()
-    eng = P.Engine(sc, n_scenarios=draws_per_rank, max_steps=T)
-    eng.set_stream(torch.cuda.current_stream().cuda_stream)
-    eng.set_state(lk0, ps0)
+    sg = ShardedGradient(sc, CAL_DRAWS, world, rank, stream_ptr=torch.cuda.current_stream().cuda_stream)
     lo = np.array([13.9, 0.18, 0.0, 0.01])
     hi = np.array([22.2, 0.22, 5.0, 5.0])
     raw = np.zeros((4, L))
     m = np.zeros_like(raw)
     v = np.zeros_like(raw)
-    sc_loss = 1.0 / (K * len(obs_ids))
+    scl = 1.0 / (K * len(obs_ids))
+
+    def seeds_fn(snaps, cum_final):  # mse_loss_builder value + seeds per draw
+        d = snaps[:, :, obs_ids] * DELTA_N - obs_vals[None]
+        loss = (d * d).sum(axis=(1, 2)) * scl
+        seeds = np.zeros_like(snaps)
+        seeds[:, :, obs_ids] = ((0.0 + scl * d) + scl * d) * DELTA_N
+        return loss, seeds, None
 
     def iteration(it):
         s = np.where(raw >= 0, 1.0 / (1.0 + np.exp(-raw)), np.exp(raw) / (1.0 + np.exp(raw)))
         vals = lo[:, None] + (hi - lo)[:, None] * s
         params = P.LinkParams(vals[0], vals[1], vals[2], vals[3], start.cost)
-        eng.set_params(params)
-        for b in range(draws_per_rank):
-            eng.set_noise(SIM_SEED, it * CAL_DRAWS + rank * draws_per_rank + b + 1, b)
-        eng.forward(T, SPI, checkpoint=True)
-        seeds = np.zeros((draws_per_rank, K, L))
-        for b in range(draws_per_rank):
-            cum = eng.read_cum(b)
-            snaps = cum[SPI - 1::SPI][:K]
-            d = snaps[:, obs_ids] * DELTA_N - obs_vals
-            seeds[b][:, obs_ids] = ((0.0 + sc_loss * d) + sc_loss * d) * DELTA_N
-        g = eng.backward(snap_seeds=seeds)  # [draws, 5, L]
-        gt = torch.from_numpy(g).cuda()
-        if world > 1:
-            import torch.distributed as dist
-
-            allg = [torch.empty_like(gt) for _ in range(world)]
-            dist.all_gather(allg, gt)
-            gt = torch.cat(allg)
-        gsum = gt[0].clone()
-        for q in range(1, gt.shape[0]):  # fixed draw order (optimization.cpp:181-190)
-            gsum += gt[q]
-        gsum = gsum.cpu().numpy()
-        ds = (hi - lo)[:, None] * s * (1.0 - s)
-        rg = gsum[:4] / CAL_DRAWS * ds
-        t_ = it + 1
-        m[:] = 0.9 * m + 0.1 * rg
-        v[:] = 0.999 * v + 0.001 * rg * rg
+        loss, gsum, _ = sg(params, SIM_SEED, calibration_draws(it, CAL_DRAWS), seeds_fn)
+        rg = gsum[:4] / CAL_DRAWS * ((hi - lo)[:, None] * s * (1.0 - s))
+        t_ = it + 1  # AdamW, optimization.cpp:10-25
+        m[:] = 0.9 * m + (1.0 - 0.9) * rg
+        v[:] = 0.999 * v + (1.0 - 0.999) * rg * rg
         raw[:] -= 0.1 * ((m / (1 - 0.9 ** t_)) / (np.sqrt(v / (1 - 0.999 ** t_)) + 1e-8) + 1e-5 * raw)
+        return loss
 
     for it in range(2):
         iteration(it)
@@ -421,20 +407,20 @@ def run_gradient(P, torch, world, rank, args):
     barrier(world)
     torch.cuda.synchronize()
     t = time.perf_counter()
-    for it in range(2, 2 + n_it):
-        iteration(it)
+    losses = [iteration(it) for it in range(2, 2 + n_it)]
     torch.cuda.synchronize()
     s_iter = max_over_ranks((time.perf_counter() - t) / n_it, world)
+    eng = sg.engine
     ker_f, _ = eng.profile_kernels(T, SPI)
     eng.forward(T, SPI, checkpoint=True)
     ker_b, _ = eng.profile_kernels(T, SPI, backward=True)
-    return {"s_per_iter": s_iter, "draws": CAL_DRAWS, "draws_per_gpu": draws_per_rank, "steps": T,
-            "iterations_timed": n_it, "params": 4 * L,
+    return {"s_per_iter": s_iter, "draws": CAL_DRAWS, "draws_per_gpu": len(sg.mine), "steps": T,
+            "iterations_timed": n_it, "params": 4 * L, "loss_last": losses[-1],
             "projected_200_iter_s": 200 * s_iter,
             "paper_calibration_s": 455.3,
             "fwd_ms_per_pass": sum(ker_f.values()), "adj_ms_per_pass": sum(ker_b.values()),
             "adj_kernel_ms": {k: round(x, 4) for k, x in ker_b.items()},
-            "timing": "wall clock per full iteration (host loss + H2D/D2H + NCCL + AdamW included)"}
+            "timing": "wall clock per full iteration (host loss + H2D/D2H + NCCL gather + AdamW included)"}
 
 
 # ---- reference arm -----------------------------------------------------------------------

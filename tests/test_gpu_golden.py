@@ -172,3 +172,28 @@ def test_stress_dn1_million_agents(port):
     assert len(tr.link_final) == 1000020
     assert np.all(np.diff(tr.cum_per_step, axis=0) >= 0)
     assert np.all(tr.pos_final >= -0.01) and np.all(tr.pos_final <= ln[tr.link_final])
+
+
+def test_sharded_gradient_world1_equals_per_draw_sum():
+    """dist.ShardedGradient (the multi-GPU calibration path, here one rank)
+    == the ordered sum of per-draw simulate_gradient results."""
+    from paper_2603_25068_b200.dist import ShardedGradient, calibration_draws
+
+    sc = P.Scenario.grid(4, 400.0, 42, 1000.0).configure(1000, 1, 300, 60)
+    p = sc.sample_parameters(3)
+    L = sc.n_links
+    rng = np.random.default_rng(9)
+    ws = rng.normal(size=(5, L))
+
+    def seeds_fn(snaps, cum_final):
+        loss = (snaps * ws[None]).sum(axis=(1, 2))
+        return loss, np.broadcast_to(ws, snaps.shape).copy(), None
+
+    its = calibration_draws(3, 4)
+    loss, gsum, rows = ShardedGradient(sc, 4)(p, 7, its, seeds_fn)
+    per = P.simulate_gradient(sc, p, seed=7, ws=ws, noise_iterations=its)
+    seq = per[0].grads.copy()
+    for g in per[1:]:
+        seq += g.grads
+    assert np.array_equal(gsum, seq)
+    assert loss == pytest.approx(sum(g.loss for g in per) / 4, rel=1e-12)
