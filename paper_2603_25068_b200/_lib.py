@@ -64,6 +64,10 @@ SIGNATURES = [
     ("dtg_last_error", C.c_char_p, [vp]),
     ("dtg_set_stream", i32, [vp, vp]),
     ("dtg_set_graphs", i32, [vp, i32]),
+    ("dtg_set_persistent", i32, [vp, i32]),
+    ("dtg_set_mode", i32, [vp, i32]),
+    ("dtg_last_mode", i32, [vp]),
+    ("dtg_profile_persistent", i32, [vp, i32, i32, _dp, C.POINTER(C.c_int)]),
     ("dtg_set_params", i32, [vp, i32, _dp, _dp, _dp, _dp, _dp]),
     ("dtg_set_state", i32, [vp, i32, _ip, _dp]),
     ("dtg_set_noise", i32, [vp, i32, u64, u64]),

@@ -1,0 +1,46 @@
+// Cluster-per-scenario forward kernel (dtg_cluster.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "dtg_device.cuh"
+
+namespace dtg {
+
+constexpr int kClusterThreads = 512;
+constexpr int kClusterCandCap = 16;
+
+// A merge column registered by an arrived head: its merge utility alpha of its
+// current link, its own merge Gumbel g'(t, row, id), slot, id and link.
+struct Cand {
+  double alpha;
+  double g;
+  int slot;
+  int aid;
+  int link;
+  int pad;
+};
+
+struct CView {
+  DevView d;
+  double* x1b;    // [2][B][N]
+  int* wonb;      // [2][B][N]
+  int* nAb;       // [2][B][L]
+  int* qnb;       // [2][B][L]
+  double* tailb;  // [2][B][L]
+  int* depb;      // [2][B][L]
+  int* win;       // [B][L]
+  int* ccnt;      // [B][L]
+  Cand* cands;    // [B][L][kClusterCandCap]
+  const double* srec;  // [B][L][maxdeg] successor preferences
+  int T;
+  int cs;              // CTAs per cluster = per scenario
+  int stage_params;    // per-link constants in shared memory
+  unsigned long long* tstamp;  // optional [T][grid][4]
+};
+
+int cluster_smem_bytes(int L, bool stage_params);
+int cluster_max_size(int L, bool stage_params);
+void launch_pack_succ(const DevView& d, double* srec, cudaStream_t st);
+cudaError_t launch_forward_cluster(const CView& V, cudaStream_t st);
+
+}  // namespace dtg

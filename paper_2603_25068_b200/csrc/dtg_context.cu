@@ -14,6 +14,8 @@
 
 #include "../../include/dtg.h"
 #include "dtg_kernels.h"
+#include "dtg_persistent.h"
+#include "dtg_cluster.h"
 
 namespace {
 
@@ -90,12 +92,27 @@ struct dtg_ctx {
       grads, xbar;
   DevBuf<double> snap_seed, cum_seed, x_seed;
   DevBuf<unsigned long long> sort_scratch;
+  DevBuf<int> alist, acount;
   DevBuf<int> tmp_link;
   DevBuf<double> tmp_pos;
   // last run
   int last_T = -1, last_spi = 1, last_ckpt = 0, last_K = 0;
   bool pending = false;
   std::int64_t launches = 0;
+  // persistent forward
+  bool persistent = true;
+  int pgrid_max = 0;
+  DevBuf<double> x1b, tailb;
+  DevBuf<int> wonb, nAb, qnb, depb, winp, ccnt, clist;
+  int last_grid = 0;
+  int mode = 0;          // 0 auto, 1 cluster, 2 grid-persistent, 3 step graph
+  int cluster_cs_max = 0;
+  bool stage_params = false;
+  int last_mode = 0, last_cs = 0;
+  DevBuf<double> srec;
+  DevBuf<dtg::Cand> cands;
+  bool want_stamps = false;
+  DevBuf<unsigned long long> stamps;
   // graphs
   cudaGraphExec_t fwd_exec = nullptr, bwd_exec = nullptr;
   long long fwd_key = -1, bwd_key = -1;
@@ -130,6 +147,7 @@ struct dtg_ctx {
     d.jam = derived.p;
     d.dxf = derived.p + BL;
     d.pref = derived.p + 2 * BL;
+    d.slogz = srec.p;
     d.seed_link = seeds.p;
     d.seed_merge = seeds.p + B;
     d.pos = pos.p;
@@ -388,6 +406,22 @@ int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
     c->errf.alloc(B);
     c->tmp_link.alloc(BN);
     c->tmp_pos.alloc(BN);
+    c->x1b.alloc(2 * BN);
+    c->wonb.alloc(2 * BN);
+    c->nAb.alloc(2 * BL);
+    c->qnb.alloc(2 * BL);
+    c->tailb.alloc(2 * BL);
+    c->depb.alloc(2 * BL);
+    c->winp.alloc(BL);
+    c->ccnt.alloc(BL);
+    c->clist.alloc(BL * dtg::kCandCap);
+    c->pgrid_max = dtg::persistent_max_grid(L, nullptr);
+    c->stage_params = dtg::cluster_smem_bytes(L, true) <= 200 * 1024;
+    c->cluster_cs_max = dtg::cluster_smem_bytes(L, c->stage_params) <= 220 * 1024
+                            ? dtg::cluster_max_size(L, c->stage_params)
+                            : 0;
+    c->srec.alloc(BL * c->maxdeg);
+    c->cands.alloc(BL * dtg::kClusterCandCap);
     c->ensure_history(std::max(1, max_steps), 0);
     CK(cudaStreamSynchronize(st));
   });
@@ -416,6 +450,56 @@ int dtg_set_stream(dtg_ctx* c, void* s) {
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->drop_graphs();
   });
+}
+
+int dtg_profile_persistent(dtg_ctx* c, int T, int spi, double* phase_us, int* grid_out) {
+  return guarded(c, [&] {
+    c->want_stamps = true;
+    const int rc = dtg_forward(c, T, spi, 0);
+    c->want_stamps = false;
+    if (rc) throw std::runtime_error(c->err);
+    c->sync_check();
+    const int G = c->last_grid;
+    std::vector<unsigned long long> s(static_cast<std::size_t>(T) * G * 4);
+    CK(cudaMemcpy(s.data(), c->stamps.p, s.size() * 8, cudaMemcpyDeviceToHost));
+    double acc[4] = {0, 0, 0, 0};
+    for (int t = 0; t < T; ++t) {
+      unsigned long long mn[4], mx[4];
+      for (int w = 0; w < 4; ++w) {
+        mn[w] = ~0ull;
+        mx[w] = 0;
+      }
+      for (int g = 0; g < G; ++g)
+        for (int w = 0; w < 4; ++w) {
+          const unsigned long long v = s[(static_cast<std::size_t>(t) * G + g) * 4 + w];
+          mn[w] = std::min(mn[w], v);
+          mx[w] = std::max(mx[w], v);
+        }
+      acc[0] += double(mx[1] - mn[0]);  // slot phase
+      acc[1] += double(mn[2] - mx[1]);  // barrier 1 after the last CTA arrived
+      acc[2] += double(mx[3] - mn[2]);  // link phase
+      if (t + 1 < T) {                  // barrier 2 (next step start)
+        unsigned long long n0 = ~0ull;
+        for (int g = 0; g < G; ++g) n0 = std::min(n0, s[(static_cast<std::size_t>(t + 1) * G + g) * 4]);
+        acc[3] += double(n0 - mx[3]);
+      }
+    }
+    for (int w = 0; w < 4; ++w) phase_us[w] = acc[w] / T / 1e3;
+    if (grid_out) *grid_out = G;
+  });
+}
+
+int dtg_set_mode(dtg_ctx* c, int mode) {
+  if (mode < 0 || mode > 3) return fail(c, DTG_ERR_CONFIG, "mode must be 0..3");
+  c->mode = mode;
+  return DTG_OK;
+}
+
+int dtg_last_mode(const dtg_ctx* c) { return c->last_mode * 100 + c->last_cs; }
+
+int dtg_set_persistent(dtg_ctx* c, int enabled) {
+  c->persistent = enabled != 0;
+  return DTG_OK;
 }
 
 int dtg_set_graphs(dtg_ctx* c, int enabled) {
@@ -495,6 +579,7 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
     const std::size_t BL = static_cast<std::size_t>(c->B) * c->L;
     auto body = [&] {
       dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
+      dtg::launch_pack_succ(d, c->srec.p, st);
       CK(cudaMemcpyAsync(c->pos.p, c->pos0.p, BN * 8, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(c->aid.p, c->aid0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(c->lnk.p, c->lnk0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
@@ -506,6 +591,116 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       for (int t = 0; t < T; ++t)
         dtg::launch_step_forward(d, t, t % c->S, (t + 1) % c->S, st);
     };
+    // cluster-per-scenario mode: <= 8 slots per thread inside one cluster
+    int cs_need = (c->N + dtg::kClusterThreads * 8 - 1) / (dtg::kClusterThreads * 8);
+    int cs = 1;
+    while (cs < cs_need) cs <<= 1;
+    const bool cluster_ok = c->cluster_cs_max > 0 && cs <= c->cluster_cs_max;
+    int mode = c->mode;
+    // auto: the persistent grid schedule measured fastest (profiles/r01/phase_*.log)
+    if (mode == 0) mode = c->persistent ? 2 : 3;
+    if (mode == 1 && !cluster_ok) mode = 2;
+    if (mode == 2 && c->pgrid_max <= 0) mode = 3;
+    if (!c->persistent && c->mode == 0) mode = 3;
+    c->last_mode = mode;
+    if (mode == 1 && T > 0) {
+      if (cs < 1) cs = 1;
+      dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
+      dtg::launch_pack_succ(d, c->srec.p, st);
+      CK(cudaMemcpyAsync(c->pos.p, c->pos0.p, BN * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->aid.p, c->aid0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->lnk.p, c->lnk0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->off.p, c->off0.p, static_cast<std::size_t>(c->B) * (c->L + 1) * 4,
+                         cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->qh.p, c->q0.p, BL * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemsetAsync(c->cumh.p, 0, BL * 8, st));
+      CK(cudaMemsetAsync(c->errf.p, 0, sizeof(int) * c->B, st));
+      CK(cudaMemsetAsync(c->ccnt.p, 0, BL * 4, st));
+      CK(cudaMemsetAsync(c->depb.p, 0, 2 * BL * 4, st));
+      dtg::CView V{};
+      V.d = d;
+      V.x1b = c->x1b.p;
+      V.wonb = c->wonb.p;
+      V.nAb = c->nAb.p;
+      V.qnb = c->qnb.p;
+      V.tailb = c->tailb.p;
+      V.depb = c->depb.p;
+      V.win = c->winp.p;
+      V.ccnt = c->ccnt.p;
+      V.cands = c->cands.p;
+      V.srec = c->srec.p;
+      V.T = T;
+      V.cs = cs;
+      V.stage_params = c->stage_params ? 1 : 0;
+      V.tstamp = nullptr;
+      c->last_grid = c->B * cs;
+      c->last_cs = cs;
+      if (c->want_stamps) {
+        c->stamps.ensure(static_cast<std::size_t>(T) * c->last_grid * 4);
+        V.tstamp = c->stamps.p;
+      }
+      CK(dtg::launch_forward_cluster(V, st));
+      c->launches = 3;
+      c->last_T = T;
+      c->last_spi = spi;
+      c->last_ckpt = checkpoint;
+      c->last_K = T / spi;
+      c->pending = true;
+      return;
+    }
+    if (mode == 2 && T > 0) {
+      // setup copies, then ONE cooperative launch for all T steps
+      dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
+      dtg::launch_pack_succ(d, c->srec.p, st);
+      CK(cudaMemcpyAsync(c->pos.p, c->pos0.p, BN * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->aid.p, c->aid0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->lnk.p, c->lnk0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->off.p, c->off0.p, static_cast<std::size_t>(c->B) * (c->L + 1) * 4,
+                         cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(c->qh.p, c->q0.p, BL * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemsetAsync(c->cumh.p, 0, BL * 8, st));
+      CK(cudaMemsetAsync(c->errf.p, 0, sizeof(int) * c->B, st));
+      CK(cudaMemsetAsync(c->ccnt.p, 0, BL * 4, st));
+      CK(cudaMemsetAsync(c->depb.p, 0, 2 * BL * 4, st));
+      dtg::PView P{};
+      P.d = d;
+      P.x1b = c->x1b.p;
+      P.wonb = c->wonb.p;
+      P.nAb = c->nAb.p;
+      P.qnb = c->qnb.p;
+      P.tailb = c->tailb.p;
+      P.depb = c->depb.p;
+      P.win = c->winp.p;
+      P.ccnt = c->ccnt.p;
+      P.clist = c->clist.p;
+      P.T = T;
+      const int want = (std::max(c->N, c->L) + 511) / 512;  // CTAs per scenario
+      int grid;
+      if (static_cast<long long>(c->B) * want <= c->pgrid_max) {
+        P.bps = want;
+        grid = c->B * want;
+      } else if (c->B <= c->pgrid_max) {
+        P.bps = c->pgrid_max / c->B;
+        grid = P.bps * c->B;
+      } else {
+        P.bps = 0;
+        grid = c->pgrid_max;
+      }
+      c->last_grid = grid;
+      P.tstamp = nullptr;
+      if (c->want_stamps) {
+        c->stamps.ensure(static_cast<std::size_t>(T) * grid * 4);
+        P.tstamp = c->stamps.p;
+      }
+      CK(dtg::launch_forward_persistent(P, grid, st));
+      c->launches = 2;
+      c->last_T = T;
+      c->last_spi = spi;
+      c->last_ckpt = checkpoint;
+      c->last_K = T / spi;
+      c->pending = true;
+      return;
+    }
     const long long key = (static_cast<long long>(T) << 20) ^ (c->S << 1) ^ 1;
     if (c->graphs && T > 0) {
       if (c->fwd_key != key || !c->fwd_exec) {
@@ -597,6 +792,8 @@ static void run_backward(dtg_ctx* c, const double* snap, const double* cum, cons
   changed |= c->grads.ensure(B * 5 * L);
   changed |= c->xbar.ensure(2 * B * N);
   changed |= c->sort_scratch.ensure(2 * B * N + 2);
+  changed |= c->alist.ensure(B * N);
+  changed |= c->acount.ensure(B);
   if (changed) c->drop_graphs();
   auto up = [&](double* dst, const double* src, std::size_t n) {
     if (src)
@@ -607,9 +804,12 @@ static void run_backward(dtg_ctx* c, const double* snap, const double* cum, cons
   if (K) up(c->snap_seed.p, snap, B * K * L);
   up(c->cum_seed.p, cum, B * L);
   up(c->x_seed.p, xs, B * N);
-  const dtg::DevView d = c->view();
+  dtg::DevView d = c->view();
+  d.alist = c->alist.p;
+  d.acount = c->acount.p;
   double* xb[2] = {c->xbar.p, c->xbar.p + B * N};
   auto body = [&] {
+    CK(cudaMemsetAsync(c->acount.p, 0, B * sizeof(int), st));
     dtg::launch_adj_init(d, T % c->S, c->x_seed.p, xb[T & 1], c->cum_seed.p, st);
     for (int t = T - 1; t >= 0; --t) {
       const int snap_k = ((t + 1) % spi == 0) ? (t + 1) / spi - 1 : -1;
@@ -692,6 +892,7 @@ int dtg_profile_kernels(dtg_ctx* c, int T, int spi, int backward, double* ms_out
         const std::size_t BN = static_cast<std::size_t>(c->B) * c->N;
         const std::size_t BL = static_cast<std::size_t>(c->B) * c->L;
         dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
+      dtg::launch_pack_succ(d, c->srec.p, st);
         CK(cudaMemcpyAsync(c->pos.p, c->pos0.p, BN * 8, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(c->aid.p, c->aid0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(c->lnk.p, c->lnk0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
@@ -718,9 +919,12 @@ int dtg_profile_kernels(dtg_ctx* c, int T, int spi, int backward, double* ms_out
       run_backward(c, nullptr, nullptr, nullptr, cudaMemcpyHostToDevice);  // allocate + warm
       c->sync_check();
       body = [&] {
-        const dtg::DevView d = c->view();
+        dtg::DevView d = c->view();
+        d.alist = c->alist.p;
+        d.acount = c->acount.p;
         const std::size_t B = c->B, N = c->N;
         const int K = c->last_K;
+        CK(cudaMemsetAsync(c->acount.p, 0, B * sizeof(int), st));
         double* xb[2] = {c->xbar.p, c->xbar.p + B * N};
         dtg::launch_adj_init(d, T % c->S, c->x_seed.p, xb[T & 1], c->cum_seed.p, st);
         for (int t = T - 1; t >= 0; --t) {

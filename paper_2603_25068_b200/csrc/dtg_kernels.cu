@@ -71,19 +71,17 @@ __global__ void __launch_bounds__(256) k_step_cf(DevView d, int t, int s_cur) {
   if (r == n - 1) d.tail[pl] = me.x1;  // min x1 = vacancy (node_model.cpp:27-41)
   if (fa) {
     d.won[bn + k] = 0;
+    if (d.alist) d.alist[bn + atomicAdd(&d.acount[b], 1)] = k;  // reverse sweep only
     int c = -1;
     const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
     if (deg > 0) {  // link_choice (node_model.cpp:45-97)
-      double v[kMaxDeg], g[kMaxDeg], lz[kMaxDeg], pi[kMaxDeg];
+      double g[kMaxDeg], pi[kMaxDeg];
       const int agent = d.aid[so + k];
-      const std::size_t bl = static_cast<std::size_t>(b) * d.L;
-      for (int e = 0; e < deg; ++e) {
-        const int jj = d.succ[s0 + e];
-        v[e] = d.pref[bl + jj];
+      const double* lz = d.slogz + (static_cast<std::size_t>(b) * d.L + j) * d.maxdeg;
+      for (int e = 0; e < deg; ++e)
         g[e] = gumbel(d.seed_link[b], static_cast<std::uint64_t>(t),
-                      static_cast<std::uint64_t>(agent), static_cast<std::uint64_t>(jj));
-      }
-      c = d.succ[s0 + two_softmax<kMaxDeg>(deg, v, g, d.kinv, lz, pi)];
+                      static_cast<std::uint64_t>(agent), static_cast<std::uint64_t>(d.succ[s0 + e]));
+      c = d.succ[s0 + softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi)];
     }
     d.choice[bn + k] = c;
   }
@@ -386,181 +384,141 @@ __global__ void __launch_bounds__(128) k_adj_node(DevView d, int t, int s_cur,
   }
 }
 
-// Block reductions for k_adj_a0 (blockDim.x == 256).
-struct ArgMaxE {
-  double e;
-  int id, slot;
+// Per-row running maximum of y with the largest OTHER y (near-tie detector).
+struct Top2 {
+  double y1, y2;
+  int id1, s1;
 };
-__device__ __forceinline__ bool better(const ArgMaxE& a, const ArgMaxE& b) {
-  return a.e > b.e || (a.e == b.e && a.id < b.id);
+__device__ __forceinline__ void top2_push(Top2& T, double y, int id, int slot) {
+  if (y > T.y1 || (y == T.y1 && id < T.id1)) {
+    T.y2 = fmax(T.y2, T.y1);
+    T.y1 = y;
+    T.id1 = id;
+    T.s1 = slot;
+  } else {
+    T.y2 = fmax(T.y2, y);
+  }
 }
+__device__ __forceinline__ void top2_merge(Top2& A, const Top2& B) {
+  if (B.y1 > A.y1 || (B.y1 == A.y1 && B.id1 < A.id1)) {
+    A.y2 = fmax(fmax(A.y2, B.y2), A.y1);
+    A.y1 = B.y1;
+    A.id1 = B.id1;
+    A.s1 = B.s1;
+  } else {
+    A.y2 = fmax(fmax(A.y2, B.y2), B.y1);
+  }
+}
+
+constexpr int kA0Threads = 512;
 
 // Rows that the reference routes to the first arrived agent A[0]: successors i
 // of A[0]'s link that are vacant and targeted by nobody.  targeted_i = max over
 // an all-zero column, whose first-index VJP lands on A[0]
 // (reduce_max tensor.cpp:863-876); the row's draw w_i is the Gumbel argmax
 // over every arrived agent with a uniform utility (node_model.cpp:99-120).
-__global__ void __launch_bounds__(256) k_adj_a0(DevView d, int t, int s_cur,
-                                                 int s_next, const double* xbar_next,
-                                                 unsigned long long* sort_scratch,
-                                                 int force_slow) {
-  __shared__ ArgMaxE sh[8];
-  __shared__ double shd[8];
-  __shared__ int shn[8];
-  __shared__ ArgMaxE best_all;
-  __shared__ double m2_all, runner_all;
-  __shared__ int na_all;
+// One pass over the arrived list (appended by the replayed k_step_cf) keeps,
+// per row, the top y = (logz + g) / tau_g and the largest other y.  Because
+// exp is monotone, the reference's first argmax of pi = exp(y - m2) / z2 is the
+// top-y agent (lowest id on exact ties) unless the runner-up is within 1e-9
+// relative — then the exact ordered-sum path recomputes pi as the reference
+// does (ascending agent id, sequential z2).
+__global__ void __launch_bounds__(kA0Threads) k_adj_a0(DevView d, int t, int s_cur,
+                                                        int s_next, const double* xbar_next,
+                                                        unsigned long long* sort_scratch,
+                                                        int force_slow) {
+  __shared__ Top2 sh[kA0Threads / 32][kMaxDeg];
+  __shared__ int rows[kMaxDeg];
+  __shared__ int nrows;
+  __shared__ Top2 best_all;
+  __shared__ int cnt;
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double* la0 = d.lbar_a0 + static_cast<std::size_t>(b) * d.maxdeg;
   if (tid < d.maxdeg) la0[tid] = 0.0;
   const int a0s = d.a0[b];
-  if (a0s < 0) return;
   const std::size_t so = sidx(d, s_cur, b);
   const std::size_t bl = static_cast<std::size_t>(b) * d.L;
   const std::size_t bn = static_cast<std::size_t>(b) * d.N;
-  const int* off = d.off + oidx(d, s_cur, b);
-  const int* offn = d.off + oidx(d, s_next, b);
-  const int c0 = d.lnk[so + a0s];
-  const int s0 = d.succ_off[c0], deg = d.succ_off[c0 + 1] - s0;
-  // |A|
-  int na_loc = 0;
-  for (int j = tid; j < d.L; j += blockDim.x)
-    if (off[j + 1] > off[j]) na_loc += d.nA[bl + j];
-  for (int o = 16; o > 0; o >>= 1) na_loc += __shfl_xor_sync(0xffffffffu, na_loc, o);
-  if (lane == 0) shn[wid] = na_loc;
-  __syncthreads();
+  const int nA = d.acount[b];
+  const int c0 = a0s >= 0 ? d.lnk[so + a0s] : 0;
+  const int s0 = d.succ_off[c0], deg = a0s >= 0 ? d.succ_off[c0 + 1] - s0 : 0;
   if (tid == 0) {
-    int s = 0;
-    for (int w = 0; w < 8; ++w) s += shn[w];
-    na_all = s;
+    int nr = 0;
+    for (int e = 0; e < deg; ++e) {
+      const int i = d.succ[s0 + e];
+      if (d.vac[bl + i] && d.win[bl + i] < 0) rows[nr++] = e;
+    }
+    nrows = nr;
   }
   __syncthreads();
-  const int nA = na_all;
-  // uniform first-stage log-softmax: v = -1e12 everywhere, z = |A| exactly
+  const int nr = nrows;
+  if (nr == 0) {
+    if (tid == 0) d.acount[b] = 0;
+    return;
+  }
+  const int* off = d.off + oidx(d, s_cur, b);
+  const int* offn = d.off + oidx(d, s_next, b);
+  const int* alist = d.alist + bn;
+  // uniform first stage: v = -1e12 everywhere, z = |A| exactly
   const double v = 0.0 - kMaskLarge;
   const double lzv = log(static_cast<double>(nA) * 1.0) + v;
   const double logz = v - lzv;
-  for (int e = 0; e < deg; ++e) {
-    const int i = d.succ[s0 + e];
-    if (!d.vac[bl + i] || d.win[bl + i] >= 0) continue;
-    // pass 1: m2 = max y
-    double m2 = -INFINITY;
-    for (int j = tid; j < d.L; j += blockDim.x) {
-      const int base = off[j];
-      if (off[j + 1] == base) continue;
-      const int na = d.nA[bl + j];
-      for (int r = 0; r < na; ++r) {
-        const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
-                                static_cast<std::uint64_t>(i),
-                                static_cast<std::uint64_t>(d.aid[so + base + r]));
-        const double y = (logz + g) * d.kinv;
-        m2 = fmax(m2, y);
-      }
+  Top2 tp[kMaxDeg];
+  for (int r = 0; r < nr; ++r) tp[r] = Top2{-INFINITY, -INFINITY, INT_MAX, -1};
+  for (int q = tid; q < nA; q += blockDim.x) {
+    const int s = alist[q];
+    const int id = d.aid[so + s];
+    for (int r = 0; r < nr; ++r) {
+      const int i = d.succ[s0 + rows[r]];
+      const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
+                              static_cast<std::uint64_t>(i), static_cast<std::uint64_t>(id));
+      top2_push(tp[r], (logz + g) * d.kinv, id, s);
     }
-    for (int o = 16; o > 0; o >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o));
-    if (lane == 0) shd[wid] = m2;
-    __syncthreads();
-    if (tid == 0) {
-      double m = shd[0];
-      for (int w = 1; w < 8; ++w) m = fmax(m, shd[w]);
-      m2_all = m;
-    }
-    __syncthreads();
-    const double M2 = m2_all;
-    // pass 2: e = exp(y - m2); argmax e (ties -> lowest id) and runner-up
-    ArgMaxE bst{-1.0, INT_MAX, -1};
-    double runner = -1.0;
-    for (int j = tid; j < d.L; j += blockDim.x) {
-      const int base = off[j];
-      if (off[j + 1] == base) continue;
-      const int na = d.nA[bl + j];
-      for (int r = 0; r < na; ++r) {
-        const int s = base + r;
-        const int id = d.aid[so + s];
-        const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
-                                static_cast<std::uint64_t>(i), static_cast<std::uint64_t>(id));
-        const double ev = exp((logz + g) * d.kinv - M2);
-        ArgMaxE c{ev, id, s};
-        if (better(c, bst)) {
-          if (bst.e != ev) runner = fmax(runner, bst.e);
-          bst = c;
-        } else if (ev != bst.e) {
-          runner = fmax(runner, ev);
-        }
-      }
-    }
+  }
+  for (int r = 0; r < nr; ++r) {
+    Top2 x = tp[r];
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      ArgMaxE c{__shfl_xor_sync(0xffffffffu, bst.e, o), __shfl_xor_sync(0xffffffffu, bst.id, o),
-                __shfl_xor_sync(0xffffffffu, bst.slot, o)};
-      const double rr = __shfl_xor_sync(0xffffffffu, runner, o);
-      // merge: runner-up = max of everything that is not the winner's value
-      double nr = fmax(runner, rr);
-      if (better(c, bst)) {
-        if (bst.e != c.e) nr = fmax(nr, bst.e);
-        bst = c;
-      } else if (c.e != bst.e) {
-        nr = fmax(nr, c.e);
-      }
-      runner = nr;
+      Top2 y;
+      y.y1 = __shfl_xor_sync(0xffffffffu, x.y1, o);
+      y.y2 = __shfl_xor_sync(0xffffffffu, x.y2, o);
+      y.id1 = __shfl_xor_sync(0xffffffffu, x.id1, o);
+      y.s1 = __shfl_xor_sync(0xffffffffu, x.s1, o);
+      top2_merge(x, y);
     }
-    if (lane == 0) {
-      sh[wid] = bst;
-      shd[wid] = runner;
-    }
-    __syncthreads();
+    if (lane == 0) sh[wid][r] = x;
+  }
+  __syncthreads();
+  for (int r = 0; r < nr; ++r) {
     if (tid == 0) {
-      ArgMaxE bb = sh[0];
-      double rn = shd[0];
-      for (int w = 1; w < 8; ++w) {
-        const ArgMaxE c = sh[w];
-        double nr = fmax(rn, shd[w]);
-        if (better(c, bb)) {
-          if (bb.e != c.e) nr = fmax(nr, bb.e);
-          bb = c;
-        } else if (c.e != bb.e) {
-          nr = fmax(nr, c.e);
-        }
-        rn = nr;
-      }
-      best_all = bb;
-      runner_all = rn;
+      Top2 x = sh[0][r];
+      for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) top2_merge(x, sh[w][r]);
+      best_all = x;
     }
     __syncthreads();
-    ArgMaxE win = best_all;
-    // pi = e / z2 could merge the top value with a runner-up within an ulp;
-    // then redo the reference's ordered sum (ascending agent id) exactly.
-    const bool near = runner_all >= win.e * (1.0 - 0x1p-48);
+    Top2 win = best_all;
+    const int i = d.succ[s0 + rows[r]];
+    const bool near = !(win.y1 - win.y2 > 1e-9 * fmax(1.0, fabs(win.y1)));
     if (near || force_slow) {
       if (!force_slow && tid == 0) atomicOr(&d.err[b], kErrNearTieSlow);
-      // collect (id << 32 | slot) keys of A into scratch and sort (one block)
-      unsigned long long* keys = sort_scratch + static_cast<std::size_t>(b) * d.N;
-      __shared__ int cnt;
-      if (tid == 0) cnt = 0;
-      __syncthreads();
-      for (int j = tid; j < d.L; j += blockDim.x) {
-        const int base = off[j];
-        if (off[j + 1] == base) continue;
-        const int na = d.nA[bl + j];
-        for (int r = 0; r < na; ++r) {
-          const int s = base + r;
-          const int q = atomicAdd(&cnt, 1);
-          keys[q] = (static_cast<unsigned long long>(d.aid[so + s]) << 32) | static_cast<unsigned>(s);
-        }
+      // exact path: (id << 32 | slot) keys of A sorted ascending, sequential z2
+      unsigned long long* keys = sort_scratch + static_cast<std::size_t>(b) * 2 * d.N;
+      for (int q = tid; q < nA; q += blockDim.x) {
+        const int s = alist[q];
+        keys[q] = (static_cast<unsigned long long>(d.aid[so + s]) << 32) | static_cast<unsigned>(s);
       }
+      int P2 = 1;
+      while (P2 < nA) P2 <<= 1;
+      for (int q = nA + tid; q < P2; q += blockDim.x) keys[q] = ULLONG_MAX;
       __syncthreads();
-      int P = 1;
-      while (P < nA) P <<= 1;
-      for (int q = nA + tid; q < P; q += blockDim.x) keys[q] = ULLONG_MAX;
-      __syncthreads();
-      for (int kk = 2; kk <= P; kk <<= 1)  // bitonic sort in global scratch
+      for (int kk = 2; kk <= P2; kk <<= 1)
         for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-          for (int q = tid; q < P; q += blockDim.x) {
+          for (int q = tid; q < P2; q += blockDim.x) {
             const int l = q ^ jj;
             if (l > q) {
               const unsigned long long a = keys[q], c = keys[l];
-              const bool up = (q & kk) == 0;
-              if ((a > c) == up) {
+              if ((a > c) == ((q & kk) == 0)) {
                 keys[q] = c;
                 keys[l] = a;
               }
@@ -569,22 +527,22 @@ __global__ void __launch_bounds__(256) k_adj_a0(DevView d, int t, int s_cur,
           __syncthreads();
         }
       if (tid == 0) {
+        const double m2 = win.y1;
         double z2 = 0.0;
         for (int q = 0; q < nA; ++q) {
-          const int id = static_cast<int>(keys[q] >> 32);
-          const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
-                                  static_cast<std::uint64_t>(i), static_cast<std::uint64_t>(id));
-          z2 += exp((logz + g) * d.kinv - M2);
+          const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t), static_cast<std::uint64_t>(i),
+                                  keys[q] >> 32);
+          z2 += exp((logz + g) * d.kinv - m2);
         }
         double bp = -1.0;
         for (int q = 0; q < nA; ++q) {
-          const int id = static_cast<int>(keys[q] >> 32);
-          const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
-                                  static_cast<std::uint64_t>(i), static_cast<std::uint64_t>(id));
-          const double pv = exp((logz + g) * d.kinv - M2) / z2;
+          const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t), static_cast<std::uint64_t>(i),
+                                  keys[q] >> 32);
+          const double pv = exp((logz + g) * d.kinv - m2) / z2;
           if (pv > bp) {
             bp = pv;
-            best_all = ArgMaxE{pv, id, static_cast<int>(keys[q] & 0xffffffffull)};
+            best_all.id1 = static_cast<int>(keys[q] >> 32);
+            best_all.s1 = static_cast<int>(keys[q] & 0xffffffffull);
           }
         }
       }
@@ -592,7 +550,7 @@ __global__ void __launch_bounds__(256) k_adj_a0(DevView d, int t, int s_cur,
       win = best_all;
     }
     if (tid == 0) {
-      const int ws = win.slot;
+      const int ws = win.s1;
       const int j = d.lnk[so + ws];
       const int base = off[j];
       const int na = d.nA[bl + j];
@@ -605,10 +563,11 @@ __global__ void __launch_bounds__(256) k_adj_a0(DevView d, int t, int s_cur,
         const double xb = xbar_next[bn + ns];
         ab = (i == j ? xb * d.M : 0.0 * d.M) + admitted_bar(xb, d.x1[bn + ws], d.M);
       }
-      la0[e] = 0.0 + ab;
+      la0[rows[r]] = 0.0 + ab;
     }
     __syncthreads();
   }
+  if (tid == 0) d.acount[b] = 0;
 }
 
 __global__ void __launch_bounds__(128) k_adj_choice(DevView d, int t, int s_cur) {
@@ -627,15 +586,13 @@ __global__ void __launch_bounds__(128) k_adj_choice(DevView d, int t, int s_cur)
   const int a0s = d.a0[b];
   for (int r = 0; r < na; ++r) {
     const int s = base + r;
-    double v[kMaxDeg], g[kMaxDeg], lz[kMaxDeg], pi[kMaxDeg], bar[kMaxDeg];
+    double g[kMaxDeg], pi[kMaxDeg], bar[kMaxDeg];
     const int agent = d.aid[so + s];
-    for (int e = 0; e < deg; ++e) {
-      const int jj = d.succ[s0 + e];
-      v[e] = d.pref[bl + jj];
+    const double* lz = d.slogz + (bl + j) * d.maxdeg;
+    for (int e = 0; e < deg; ++e)
       g[e] = gumbel(d.seed_link[b], static_cast<std::uint64_t>(t),
-                    static_cast<std::uint64_t>(agent), static_cast<std::uint64_t>(jj));
-    }
-    const int ed = two_softmax<kMaxDeg>(deg, v, g, d.kinv, lz, pi);
+                    static_cast<std::uint64_t>(agent), static_cast<std::uint64_t>(d.succ[s0 + e]));
+    const int ed = softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi);
     for (int e = 0; e < deg; ++e) bar[e] = 0.0;
     const int dch = d.succ[s0 + ed];
     if (d.vac[bl + dch] && d.win[bl + dch] >= 0) bar[ed] = d.lbar_row[bn + s];
@@ -851,7 +808,7 @@ void launch_bwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
                                                           snap_seed, snap_k, K);
       break;
     case 4:
-      k_adj_a0<<<d.B, 256, 0, st>>>(d, t, s_cur, s_next, xbar_next, sort_scratch, force_slow);
+      k_adj_a0<<<d.B, kA0Threads, 0, st>>>(d, t, s_cur, s_next, xbar_next, sort_scratch, force_slow);
       break;
     case 5:
       k_adj_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);

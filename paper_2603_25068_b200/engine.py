@@ -290,6 +290,24 @@ class Engine:
     def set_graphs(self, on: bool):
         self._check(self._lib.dtg_set_graphs(self._h, int(on)))
 
+    def set_mode(self, mode: int):
+        """0 auto, 1 cluster per scenario, 2 persistent grid, 3 step graph."""
+        self._check(self._lib.dtg_set_mode(self._h, mode))
+
+    @property
+    def last_mode(self) -> int:
+        return int(self._lib.dtg_last_mode(self._h))
+
+    def set_persistent(self, on: bool):
+        self._check(self._lib.dtg_set_persistent(self._h, int(on)))
+
+    def profile_persistent(self, T: int, steps_per_interval: int):
+        """Mean per-step span (us) of the persistent kernel's phases."""
+        ph = np.zeros(4)
+        g = C.c_int()
+        self._check(self._lib.dtg_profile_persistent(self._h, T, steps_per_interval, ph, C.byref(g)))
+        return dict(zip(["slot_phase", "barrier1", "link_phase", "barrier2"], ph.tolist())), g.value
+
     def force_slow_path(self, on: bool):
         self._check(self._lib.dtg_debug_force_slow_path(self._h, int(on)))
 

@@ -1,0 +1,52 @@
+"""The cluster-per-scenario kernel, the persistent cooperative grid kernel and
+the 4-kernel step graph are three schedules of the same arithmetic: results must be bit-identical, in all
+three grid-assignment modes (several CTAs per scenario, capped CTAs per
+scenario, several scenarios per CTA)."""
+import numpy as np
+import pytest
+
+P = pytest.importorskip("paper_2603_25068_b200")
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def run(sc, p, B, mode, T, spi, ckpt=True):
+    lk, ps = sc.seed_agents()
+    e = P.Engine(sc, B, T)
+    e.set_mode(mode)
+    e.set_params(p)
+    e.set_state(lk, ps)
+    for b in range(B):
+        e.set_noise(7, 100 + b, b)
+    e.forward(T, spi, checkpoint=ckpt)
+    cum = np.stack([e.read_cum(b) for b in range(B)])
+    fin = [e.read_state(b, T) for b in range(B)]
+    mid = [e.read_state(b, T // 2) for b in range(B)] if ckpt else None
+    return cum, fin, mid
+
+
+@pytest.mark.parametrize("n,length,veh,dn,T,B", [
+    (4, 400.0, 1000, 1, 600, 1),
+    (6, 300.0, 2400, 2, 300, 5),
+    (23, 1609.34, 1000020, 30, 120, 8),
+    (4, 400.0, 1000, 1, 200, 300),  # more scenarios than resident CTAs -> scenario loop
+])
+def test_persistent_equals_step_graph(n, length, veh, dn, T, B):
+    sc = P.Scenario.grid(n, length, 42, 1000.0).configure(veh, dn, T, 300 if dn <= 2 else 30 * dn * 10)
+    p = sc.sample_parameters(3)
+    spi = sc.steps_per_interval
+    ref = run(sc, p, B, 3, T, spi)  # 4-kernel step graph
+    for mode in (1, 2):           # cluster per scenario, persistent grid
+        a = run(sc, p, B, mode, T, spi)
+        assert np.array_equal(a[0], ref[0]), mode
+        for x, y in zip(a[1], ref[1]):
+            assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), mode
+        for x, y in zip(a[2], ref[2]):
+            assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), mode
