@@ -283,21 +283,25 @@ def run_ours(args):
     value = world * B * SIM_SECONDS / (dev_s / args.steps)
     single_rtf = SIM_SECONDS / (dev_s / args.steps)
 
-    # per-kernel attribution with CUDA events on the launching stream
-    ker_ms, _ = eng.profile_kernels(T_STEPS, SPI)
-    total = sum(ker_ms.values())
-    dom = max(ker_ms, key=ker_ms.get)
-    per_launch_s = ker_ms[dom] / 1e3 / T_STEPS
-    ba, bl = ALG_BYTES[dom]
-    alg_bytes = B * (ba * N + bl * L)
+    # roofline of the production kernel: one persistent cooperative launch per
+    # nowcast (k_forward_persistent); its duration is the event-timed device
+    # time above.  Algorithmic bytes: SURVEY §8d forward figure, 16 B per
+    # agent-step + 64 B per link-step, x T steps x B scenarios.
+    per_launch_s = dev_s / args.steps
+    alg_bytes = B * T_STEPS * (16 * N + 64 * L)
     peak, peak_kind = measured_peak_hbm()
     achieved = alg_bytes / per_launch_s / 1e9
-    traffic = ncu_traffic(dom)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                "alg_bytes_per_launch": alg_bytes, "avg_launch_us": per_launch_s * 1e6,
-                "share_of_step": ker_ms[dom] / total,
-                "kernel_ms_per_nowcast": {k: round(v, 4) for k, v in ker_ms.items()}}
+    phases, grid = eng.profile_persistent(T_STEPS, SPI)
+    ker_ms, _ = eng.profile_kernels(T_STEPS, SPI)  # the 4-kernel schedule, for reference
+    roofline = {"bound": "hbm", "kernel": "k_forward_persistent", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic("k_forward_persistent"),
+                "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes,
+                "avg_launch_us": per_launch_s * 1e6, "share_of_step": 1.0, "grid_ctas": grid,
+                "phase_us_per_engine_step": {k: round(v, 2) for k, v in phases.items()},
+                "note": "latency-bound: the 1 MB scenario state stays in L2 (ncu dram traffic per launch "
+                        "<< algorithmic bytes); per-step time = 2 grid barriers + 2 dependent phases",
+                "step_graph_kernel_ms_per_nowcast": {k: round(v, 4) for k, v in ker_ms.items()}}
+    throughput = run_throughput(P, torch, sc, p, lk0, ps0, args) if world == 1 and not args.no_throughput else None
 
     # e2e through the C-ABI scenario call with host buffers
     its = [rank * B + b for b in range(B)]
@@ -345,6 +349,7 @@ def run_ours(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "gradient": grad,
+            "batched_throughput": throughput,
         }
         print(json.dumps(out), flush=True)
     barrier(world)
@@ -352,6 +357,37 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+    return out
+
+
+def run_throughput(P, torch, sc, p, lk0, ps0, args, B=64):
+    """Batched nowcasts on one GPU (independent draws): where HBM bandwidth
+    starts to matter (roofline meaningful for B >= 256 / dn = 1)."""
+    N, L = sc.n_agents, sc.n_links
+    out = {}
+    for mode, name in ((0, "persistent grid"), (3, "4-kernel step graph")):
+        eng = P.Engine(sc, n_scenarios=B, max_steps=T_STEPS)
+        eng.set_stream(torch.cuda.current_stream().cuda_stream)
+        eng.set_mode(mode)
+        eng.set_params(p)
+        eng.set_state(lk0, ps0)
+        for b in range(B):
+            eng.set_noise(SIM_SEED, 1000 + b, b)
+        for _ in range(2):
+            eng.forward(T_STEPS, SPI)
+        eng.sync()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(3):
+            eng.forward(T_STEPS, SPI)
+        e1.record(st)
+        torch.cuda.synchronize()
+        s = e0.elapsed_time(e1) / 3 / 1e3
+        alg = B * T_STEPS * (16 * N + 64 * L)
+        out[name] = {"scenarios": B, "ms_per_batch": s * 1e3, "rtf_aggregate": B * SIM_SECONDS / s,
+                     "alg_GBps": alg / s / 1e9}
+        del eng
     return out
 
 
@@ -410,16 +446,33 @@ def run_gradient(P, torch, world, rank, args):
     losses = [iteration(it) for it in range(2, 2 + n_it)]
     torch.cuda.synchronize()
     s_iter = max_over_ranks((time.perf_counter() - t) / n_it, world)
+    # device time of the two passes (CUDA events on the engine's stream)
     eng = sg.engine
-    ker_f, _ = eng.profile_kernels(T, SPI)
+    st = torch.cuda.current_stream()
+    seeds = torch.zeros((len(sg.mine), K, L), dtype=torch.float64, device="cuda")
+    gbuf = torch.empty((len(sg.mine), 5, L), dtype=torch.float64, device="cuda")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    fwd_ms, adj_ms = [], []
+    for _ in range(3):
+        ev[0].record(st)
+        eng.forward(T, SPI, checkpoint=True)
+        ev[1].record(st)
+        eng.backward_device(seeds.data_ptr(), 0, 0, gbuf.data_ptr())
+        ev[2].record(st)
+        torch.cuda.synchronize()
+        fwd_ms.append(ev[0].elapsed_time(ev[1]))
+        adj_ms.append(ev[1].elapsed_time(ev[2]))
     eng.forward(T, SPI, checkpoint=True)
-    ker_b, _ = eng.profile_kernels(T, SPI, backward=True)
+    phases_f, _ = eng.profile_persistent(T, SPI)
+    eng.forward(T, SPI, checkpoint=True)
+    phases_b, grid_b = eng.profile_backward()
     return {"s_per_iter": s_iter, "draws": CAL_DRAWS, "draws_per_gpu": len(sg.mine), "steps": T,
             "iterations_timed": n_it, "params": 4 * L, "loss_last": losses[-1],
             "projected_200_iter_s": 200 * s_iter,
             "paper_calibration_s": 455.3,
-            "fwd_ms_per_pass": sum(ker_f.values()), "adj_ms_per_pass": sum(ker_b.values()),
-            "adj_kernel_ms": {k: round(x, 4) for k, x in ker_b.items()},
+            "fwd_ckpt_ms_per_pass": statistics.median(fwd_ms), "adj_ms_per_pass": statistics.median(adj_ms),
+            "fwd_phase_us_per_step": {k: round(x, 2) for k, x in phases_f.items()},
+            "adj_phase_us_per_step": {k: round(x, 2) for k, x in phases_b.items()},
             "timing": "wall clock per full iteration (host loss + H2D/D2H + NCCL gather + AdamW included)"}
 
 
@@ -490,6 +543,7 @@ def main():
     ap.add_argument("--scenarios", type=int, default=1, help="independent scenarios per GPU")
     ap.add_argument("--no-gradient", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-throughput", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

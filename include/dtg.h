@@ -86,6 +86,10 @@ int dtg_set_persistent(dtg_ctx* ctx, int enabled);
  * step.  All produce identical results.  dtg_last_mode returns
  * 100 * mode + cluster size of the last forward. */
 int dtg_set_mode(dtg_ctx* ctx, int mode);
+/* Measurement hook: one persistent reverse sweep (zero seeds) with
+ * %globaltimer stamps; phase_us[8] = mean per-step span (us) of R1, barrier,
+ * R2, barrier, R3, barrier, R4 (and 0). */
+int dtg_profile_backward(dtg_ctx* ctx, double* phase_us, int* grid_out);
 int dtg_last_mode(const dtg_ctx* ctx);
 /* Measurement hook: one persistent forward with %globaltimer stamps; returns
  * the mean per-step span (us) of [slot phase, barrier 1, link phase,
@@ -135,6 +139,8 @@ int dtg_debug_gumbel(uint64_t seed, uint64_t key, int n, const uint64_t* rows,
  * state: compact (link, pos) per agent after `step` steps (step in
  * [0, n_steps]; any step needs checkpoint, n_steps works always). */
 int dtg_read_cum(dtg_ctx* ctx, int scenario, double* cum_per_step);
+/* All scenarios at once ([B][n_steps][L]), one device->host copy. */
+int dtg_read_cum_all(dtg_ctx* ctx, double* cum_per_step);
 int dtg_read_state(dtg_ctx* ctx, int scenario, int step, int* link,
                    double* pos);
 /* Number of observation snapshots of the last forward. */

@@ -66,6 +66,7 @@ SIGNATURES = [
     ("dtg_set_graphs", i32, [vp, i32]),
     ("dtg_set_persistent", i32, [vp, i32]),
     ("dtg_set_mode", i32, [vp, i32]),
+    ("dtg_profile_backward", i32, [vp, _dp, C.POINTER(C.c_int)]),
     ("dtg_last_mode", i32, [vp]),
     ("dtg_profile_persistent", i32, [vp, i32, i32, _dp, C.POINTER(C.c_int)]),
     ("dtg_set_params", i32, [vp, i32, _dp, _dp, _dp, _dp, _dp]),
@@ -75,6 +76,7 @@ SIGNATURES = [
     ("dtg_sync", i32, [vp]),
     ("dtg_debug_force_slow_path", i32, [vp, i32]),
     ("dtg_read_cum", i32, [vp, i32, _dp]),
+    ("dtg_read_cum_all", i32, [vp, _dp]),
     ("dtg_read_state", i32, [vp, i32, i32, _ip, _dp]),
     ("dtg_n_snapshots", i32, [vp]),
     ("dtg_backward", i32, [vp, vp, vp, vp, _dp]),

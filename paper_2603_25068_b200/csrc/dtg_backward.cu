@@ -1,0 +1,674 @@
+// Persistent cooperative reverse sweep: all T reverse steps of all B scenarios
+// in one launch, four grid barriers per step (the checkpointed per-step VJP of
+// src/engine.cpp:388-415, i.e. Tape::vjp of src/tensor.cpp:715-996 applied to
+// engine_step / node_step / car_following_step / midpoint_count).
+//
+// Reverse step t (layout t = checkpoint t, layout t+1 = checkpoint t+1):
+//   R1 slots   replay car-following (x1), arrived-prefix length, tail; arrived
+//              heads replay their link choice (pi kept for R4), register as a
+//              merge candidate {alpha, own merge Gumbel, slot, id, link},
+//              append to the arrived list and atomicMin the first arrived id.
+//   R2 links   snapshot seed, count adjoint (q_bar, qprev_bar); vacancy;
+//              merge replay (winner, departures); the DEFERRED preference
+//              gradient of step t+1 (needs step t+1's link-choice VJPs from
+//              R4 of the previous iteration); arrived list: per-row top-2 of
+//              the uniform-utility Gumbel draws for A[0]'s rows.
+//   R3 links   merge-row VJP (transfer seeds a_bar, softmax VJP, targeted
+//              routing to the first candidate); A[0] rows; slots: transfer /
+//              replace_rows pass-through, counting sigmoid VJP, car-following
+//              VJP with the follower's headway term -> x_bar of layout t.
+//   R4         link-choice VJP per arrived head; warp per link: deterministic
+//              u / kappa / alpha reductions; resets for the next step.
+// Gradients accumulate per step in the reference's order (engine.cpp:410-414).
+#include <cooperative_groups.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "dtg_backward.h"
+#include "dtg_device.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dtg {
+
+namespace {
+
+constexpr int kBT = 512;  // threads per CTA
+
+__device__ __forceinline__ int findl(const int* off_s, int L, int k) {
+  int lo = 0, hi = L - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off_s[mid] <= k)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ double adm_bar(double xb, double x1, double M) {
+  double r = 0.0;
+  r += xb * (-M);
+  r += -1.0 * (xb * x1);
+  return r;
+}
+
+struct T2 {
+  double y1, y2;
+  int id1, s1;
+};
+__device__ __forceinline__ void t2_push(T2& T, double y, int id, int slot) {
+  if (y > T.y1 || (y == T.y1 && id < T.id1)) {
+    T.y2 = fmax(T.y2, T.y1);
+    T.y1 = y;
+    T.id1 = id;
+    T.s1 = slot;
+  } else {
+    T.y2 = fmax(T.y2, y);
+  }
+}
+__device__ __forceinline__ void t2_merge(T2& A, const T2& B) {
+  if (B.y1 > A.y1 || (B.y1 == A.y1 && B.id1 < A.id1)) {
+    A.y2 = fmax(fmax(A.y2, B.y2), A.y1);
+    A.y1 = B.y1;
+    A.id1 = B.id1;
+    A.s1 = B.s1;
+  } else {
+    A.y2 = fmax(fmax(A.y2, B.y2), B.y1);
+  }
+}
+
+// new slot (layout t+1) of layout-t slot k on link j (rank r)
+__device__ __forceinline__ int map_next(const BView& V, int b, int k, int j, int r,
+                                        const int* offT, const int* offN, bool* mover) {
+  const DevView& d = V.d;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const int na = V.nA_cur[bl + j];
+  if (r < na && V.won[bn + k]) {
+    *mover = true;
+    return offN[V.choice[bn + k] + 1] - 1;  // tail of the row it won
+  }
+  *mover = false;
+  int dd;
+  if (r >= na) {
+    dd = V.dep[bl + j];
+  } else {
+    dd = 0;
+    const int base = offT[j];
+    for (int q = base; q < k; ++q) dd += V.won[bn + q];
+  }
+  return offN[j] + r - dd;
+}
+
+// adjoint of the new position x1 of slot k (transfer + counting)
+__device__ __forceinline__ double x1_bar_p(const BView& V, int b, int k, int j, int r, double x1,
+                                           const int* offT, const int* offN, const double* xbn) {
+  const DevView& d = V.d;
+  bool mover;
+  const int ns = map_next(V, b, k, j, r, offT, offN, &mover);
+  double xb = (mover && !d.tg) ? 0.0 : xbn[ns];
+  const double qt = V.qtot[static_cast<std::size_t>(b) * d.L + j];
+  if (qt != 0.0) {
+    const double len = d.len[j];
+    const double sc = d.sc[j];
+    const double z = (x1 + (-(0.5 * len))) * sc;
+    const double sg = z >= 0.0 ? 1.0 / (1.0 + exp(-z)) : exp(z) / (1.0 + exp(z));
+    xb = xb + (((qt * 1.0) * sg) * (1.0 - sg)) * sc;
+  }
+  return xb;
+}
+
+__device__ __forceinline__ void bstamp(const BView& V, int t, int w) {
+  if (V.tstamp == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    V.tstamp[(static_cast<std::size_t>(t) * gridDim.x + blockIdx.x) * 8 + w] = ns;
+  }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
+  extern __shared__ int smb[];
+  cg::grid_group grid = cg::this_grid();
+  const DevView& d = V.d;
+  const int L = d.L, N = d.N;
+  int* offT = smb;
+  int* offN = smb + (L + 1);
+  T2* red = reinterpret_cast<T2*>(smb + 2 * (L + 1) + ((2 * (L + 1)) & 1));  // [kBT/32][maxdeg]
+  const bool grouped = V.bps > 0;
+  const int b0 = grouped ? blockIdx.x / V.bps : blockIdx.x;
+  const int lg = grouped ? blockIdx.x % V.bps : 0;
+  const int nblk = grouped ? V.bps : 1;
+  const int bstep = grouped ? d.B : gridDim.x;
+  const bool active = grouped ? (b0 < d.B) : true;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int T = V.T;
+
+  // R0: seeds
+  if (active)
+    for (int b = b0; b < d.B; b += bstep) {
+      const std::size_t bn = static_cast<std::size_t>(b) * N, bl = static_cast<std::size_t>(b) * L;
+      const std::size_t sf = sidx(d, T % d.S, b);
+      double* xb = V.xbar + static_cast<std::size_t>(T & 1) * d.B * N + bn;
+      for (int k = lg * kBT + tid; k < N; k += nblk * kBT)
+        xb[k] = V.x_seed ? V.x_seed[bn + d.aid[sf + k]] : 0.0;
+      double* g = V.grads + static_cast<std::size_t>(b) * 5 * L;
+      for (int j = lg * kBT + tid; j < L; j += nblk * kBT) {
+        V.cbar[bl + j] = V.cum_seed ? V.cum_seed[bl + j] : 0.0;
+        V.qbar[bl + j] = 0.0;
+        for (int c = 0; c < 5; ++c) g[c * L + j] = 0.0;
+      }
+    }
+  grid.sync();
+
+  for (int t = T - 1; t >= 0; --t) {
+    const int par = t & 1;
+    const int snap_k = ((t + 1) % V.spi == 0) ? (t + 1) / V.spi - 1 : -1;
+    bstamp(V, t, 0);
+    // ================= R1: replay f + link choice =================
+    if (active)
+      for (int b = b0; b < d.B; b += bstep) {
+        __syncthreads();
+        const int* og = d.off + oidx(d, t % d.S, b);
+        const int* ogn = d.off + oidx(d, (t + 1) % d.S, b);
+        for (int j = tid; j <= L; j += kBT) {
+          offT[j] = og[j];
+          offN[j] = ogn[j];
+        }
+        __syncthreads();
+        const std::size_t bn = static_cast<std::size_t>(b) * N, bl = static_cast<std::size_t>(b) * L;
+        const std::size_t so = sidx(d, t % d.S, b);
+        int* nAc = V.nA_cur + bl;  // nA of layout t (parity slot par)
+        int* nAw = V.nAb + static_cast<std::size_t>(par) * d.B * L + bl;
+        for (int k = lg * kBT + tid; k < N; k += nblk * kBT) {
+          const int j = findl(offT, L, k);
+          const int base = offT[j], n = offT[j + 1] - base, r = k - base;
+          const double jam = d.jam[bl + j], dxf = d.dxf[bl + j], len = d.len[j];
+          const double thr = d.thr[j];
+          const double x = d.pos[so + k];
+          const CfPick me = cf_step(x, r == 0 ? d.M : d.pos[so + k - 1] - x, jam, dxf, len);
+          V.x1[bn + k] = me.x1;
+          bool fa_n = false;
+          if (r + 1 < n) {
+            const double xn = d.pos[so + k + 1];
+            fa_n = cf_step(xn, x - xn, jam, dxf, len).x1 >= thr;
+          }
+          const bool fa = me.x1 >= thr;
+          if (r == 0 && !fa) {
+            nAw[j] = 0;
+            nAc[j] = 0;
+          }
+          if (fa && !fa_n) {
+            nAw[j] = r + 1;
+            nAc[j] = r + 1;
+          }
+          if (r == n - 1) V.tail[bl + j] = me.x1;
+          if (fa) {
+            V.won[bn + k] = 0;
+            const int a = d.aid[so + k];
+            const int q = atomicAdd(&V.acount[par * d.B + b], 1);
+            V.alist[bn + q] = k;
+            atomicMin(&V.a0key[par * d.B + b],
+                      (static_cast<unsigned long long>(a) << 32) | static_cast<unsigned>(k));
+            const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
+            int c = -1;
+            if (deg > 0) {
+              double g[kMaxDeg], pi[kMaxDeg];
+              const double* lz = d.slogz + (bl + j) * d.maxdeg;
+              for (int e = 0; e < deg; ++e)
+                g[e] = gumbel(d.seed_link[b], static_cast<std::uint64_t>(t), static_cast<std::uint64_t>(a),
+                              static_cast<std::uint64_t>(d.succ[s0 + e]));
+              const int ed = softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi);
+              c = d.succ[s0 + ed];
+              double* lp = V.lpi + (bn + k) * d.maxdeg;
+              for (int e = 0; e < deg; ++e) lp[e] = pi[e];
+              V.ched[bn + k] = ed;
+              Cand cd;
+              cd.alpha = d.alpha[bl + j];
+              cd.g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t), static_cast<std::uint64_t>(c),
+                            static_cast<std::uint64_t>(a));
+              cd.slot = k;
+              cd.aid = a;
+              cd.link = j;
+              cd.pad = 0;
+              const int qq = atomicAdd(&V.ccnt[bl + c], 1);
+              if (qq < kBwdCandCap) V.cands[(bl + c) * kBwdCandCap + qq] = cd;
+            }
+            V.choice[bn + k] = c;
+          }
+        }
+      }
+    bstamp(V, t, 1);
+    grid.sync();
+    bstamp(V, t, 2);
+    // ================= R2: count adjoint, merge replay, deferred pref, A0 partials =====
+    if (active)
+      for (int b = b0; b < d.B; b += bstep) {
+        if (!grouped) {  // scenario loop: reload this scenario's offsets
+          __syncthreads();
+          const int* og = d.off + oidx(d, t % d.S, b);
+          const int* ogn = d.off + oidx(d, (t + 1) % d.S, b);
+          for (int j = tid; j <= L; j += kBT) {
+            offT[j] = og[j];
+            offN[j] = ogn[j];
+          }
+          __syncthreads();
+        }
+        const std::size_t bn = static_cast<std::size_t>(b) * N, bl = static_cast<std::size_t>(b) * L;
+        const std::size_t so = sidx(d, t % d.S, b);
+        const std::size_t sn = sidx(d, (t + 1) % d.S, b);
+        double* g5 = V.grads + static_cast<std::size_t>(b) * 5 * L;
+        const int* nAn = V.nAb + static_cast<std::size_t>(par ^ 1) * d.B * L + bl;  // layout t+1
+        const double* vbn = V.vbar + (static_cast<std::size_t>(par ^ 1) * d.B * N + bn) * d.maxdeg;
+        for (int i = lg * kBT + tid; i < L; i += nblk * kBT) {
+          if (snap_k >= 0 && V.snap_seed)
+            V.cbar[bl + i] += V.snap_seed[(static_cast<std::size_t>(b) * V.K + snap_k) * L + i];
+          const double cb = V.cbar[bl + i];
+          const double a = d.qh[hidx(d, t + 1, b) + i] - d.qh[hidx(d, t, b) + i];
+          const bool pick = a >= 0.0;
+          V.qtot[bl + i] = V.qbar[bl + i] + (pick ? cb : 0.0);
+          V.qbar[bl + i] = pick ? -1.0 * cb : 0.0;
+          const int n_i = offT[i + 1] - offT[i];
+          const double tx = n_i ? V.tail[bl + i] : d.M;
+          const bool vacant = tx > d.jam[bl + i];
+          V.vac[bl + i] = vacant;
+          const int cnt = V.ccnt[bl + i];
+          int w = -1;
+          if (vacant && cnt > 0) {
+            if (cnt > kBwdCandCap) {
+              atomicOr(&d.err[b], kErrCandOverflow);
+            } else {
+              Cand c[kBwdCandCap];
+              for (int e = 0; e < cnt; ++e) c[e] = V.cands[(bl + i) * kBwdCandCap + e];
+              for (int x = 1; x < cnt; ++x) {
+                const Cand key = c[x];
+                int m = x - 1;
+                while (m >= 0 && c[m].aid > key.aid) {
+                  c[m + 1] = c[m];
+                  --m;
+                }
+                c[m + 1] = key;
+              }
+              double v[kBwdCandCap], g[kBwdCandCap], lz[kBwdCandCap], pi[kBwdCandCap];
+              for (int e = 0; e < cnt; ++e) {
+                v[e] = c[e].alpha;
+                g[e] = c[e].g;
+              }
+              const int best = two_softmax<kBwdCandCap>(cnt, v, g, d.kinv, lz, pi);
+              for (int e = 0; e < cnt; ++e) {
+                V.cands[(bl + i) * kBwdCandCap + e] = c[e];
+                V.mpi[(bl + i) * kBwdCandCap + e] = pi[e];
+                V.mlz[(bl + i) * kBwdCandCap + e] = lz[e];
+              }
+              w = c[best].slot;
+              V.won[bn + w] = 1;
+              atomicAdd(&V.dep[bl + c[best].link], 1);
+            }
+          }
+          V.win[bl + i] = w;
+          // deferred: preference gradient of step t+1 (its link-choice VJPs are ready)
+          if (t + 1 < T) {
+            double pb = 0.0;
+            const int e0 = d.pred_off[i], ne = min(d.pred_off[i + 1] - e0, kMaxDeg);
+            int pp[kMaxDeg], pps[kMaxDeg];
+            for (int q = 0; q < ne; ++q) {  // independent loads first
+              pp[q] = d.pred[e0 + q];
+              pps[q] = d.pred_pos[e0 + q];
+            }
+            for (int q = 0; q < ne; ++q) {
+              const int p = pp[q];
+              const int pbse = offN[p];
+              if (offN[p + 1] == pbse) continue;
+              const int nap = nAn[p];
+              for (int r = 0; r < nap; ++r)
+                pb += vbn[static_cast<std::size_t>(pbse + r) * d.maxdeg + pps[q]] * 1.0;
+            }
+            const double cst = d.cost[bl + i], be = d.beta[bl + i];
+            g5[2 * L + i] += 0.0 + pb / cst;
+            g5[4 * L + i] += 0.0 - pb * be / (cst * cst);
+          }
+          (void)sn;
+        }
+        // A[0]'s rows: per-row top-2 over the arrived list
+        const unsigned long long key = V.a0key[par * d.B + b];
+        const int nA = V.acount[par * d.B + b];
+        if (key != ULLONG_MAX) {
+          const int a0s = static_cast<int>(key & 0xffffffffull);
+          const int c0 = d.lnk[so + a0s];
+          const int s0 = d.succ_off[c0], deg0 = d.succ_off[c0 + 1] - s0;
+          const double vv = 0.0 - kMaskLarge;
+          const double lzv = log(static_cast<double>(nA) * 1.0) + vv;
+          const double logz = vv - lzv;
+          T2 tp[kMaxDeg];
+          for (int e = 0; e < deg0; ++e) tp[e] = T2{-INFINITY, -INFINITY, INT_MAX, -1};
+          for (int q = lg * kBT + tid; q < nA; q += nblk * kBT) {
+            const int s = V.alist[bn + q];
+            const int id = d.aid[so + s];
+            for (int e = 0; e < deg0; ++e) {
+              const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
+                                      static_cast<std::uint64_t>(d.succ[s0 + e]), static_cast<std::uint64_t>(id));
+              t2_push(tp[e], (logz + g) * d.kinv, id, s);
+            }
+          }
+          for (int e = 0; e < deg0; ++e) {
+            T2 x = tp[e];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              T2 y;
+              y.y1 = __shfl_xor_sync(0xffffffffu, x.y1, o);
+              y.y2 = __shfl_xor_sync(0xffffffffu, x.y2, o);
+              y.id1 = __shfl_xor_sync(0xffffffffu, x.id1, o);
+              y.s1 = __shfl_xor_sync(0xffffffffu, x.s1, o);
+              t2_merge(x, y);
+            }
+            if (lane == 0) red[wid * d.maxdeg + e] = x;
+          }
+          __syncthreads();
+          if (tid < deg0) {
+            T2 x = red[tid];
+            for (int w2 = 1; w2 < kBT / 32; ++w2) t2_merge(x, red[w2 * d.maxdeg + tid]);
+            static_cast<T2*>(V.a0part)[(static_cast<std::size_t>(b) * nblk + lg) * d.maxdeg + tid] = x;
+          }
+          __syncthreads();
+        }
+      }
+    bstamp(V, t, 3);
+    grid.sync();
+    bstamp(V, t, 4);
+    // ================= R3: merge VJP, A0 rows, position adjoint =================
+    if (active)
+      for (int b = b0; b < d.B; b += bstep) {
+        if (!grouped) {
+          __syncthreads();
+          const int* og = d.off + oidx(d, t % d.S, b);
+          const int* ogn = d.off + oidx(d, (t + 1) % d.S, b);
+          for (int j = tid; j <= L; j += kBT) {
+            offT[j] = og[j];
+            offN[j] = ogn[j];
+          }
+          __syncthreads();
+        }
+        const std::size_t bn = static_cast<std::size_t>(b) * N, bl = static_cast<std::size_t>(b) * L;
+        const std::size_t so = sidx(d, t % d.S, b);
+        const double* xbn = V.xbar + static_cast<std::size_t>(par ^ 1) * d.B * N + bn;
+        double* xbc = V.xbar + static_cast<std::size_t>(par) * d.B * N + bn;
+        // merge rows
+        for (int i = lg * kBT + tid; i < L; i += nblk * kBT) {
+          const int w = V.win[bl + i];
+          if (w < 0) continue;
+          const int cnt = V.ccnt[bl + i];
+          const Cand* cc = V.cands + (bl + i) * kBwdCandCap;
+          double bar[kBwdCandCap], lz[kBwdCandCap], pi[kBwdCandCap];
+          const double abar_w = xbn[offN[i + 1] - 1] * d.M + 0.0;
+          for (int e = 0; e < cnt; ++e) {
+            lz[e] = V.mlz[(bl + i) * kBwdCandCap + e];
+            pi[e] = V.mpi[(bl + i) * kBwdCandCap + e];
+            const int s = cc[e].slot;
+            if (s == w) {
+              bar[e] = abar_w * 1.0;
+            } else {
+              const int p = cc[e].link;
+              const int base = offT[p];
+              int dd = 0;
+              for (int q = base; q < s; ++q) dd += V.won[bn + q];
+              const double xb = xbn[offN[p] + (s - base) - dd];
+              bar[e] = adm_bar(xb, V.x1[bn + s], d.M) * 1.0;
+            }
+          }
+          two_softmax_vjp(cnt, lz, pi, d.kinv, bar);
+          for (int e = 0; e < cnt; ++e) {
+            const int s = cc[e].slot;
+            V.lbar_row[bn + s] = (e == 0 ? 0.0 + abar_w : 0.0) + bar[e] * cc[e].alpha;
+            V.prio_bar[bn + s] = 0.0 + bar[e] * 1.0;
+          }
+        }
+        // A[0] rows: warp e of CTA 0 merges row e's per-CTA partials
+        if (lg == 0 && tid < d.maxdeg) V.lbar_a0[static_cast<std::size_t>(b) * d.maxdeg + tid] = 0.0;
+        __syncthreads();
+        const unsigned long long key = V.a0key[par * d.B + b];
+        if (lg == 0 && key != ULLONG_MAX) {
+          const int a0s = static_cast<int>(key & 0xffffffffull);
+          const int c0 = d.lnk[so + a0s];
+          const int s0 = d.succ_off[c0], deg0 = d.succ_off[c0 + 1] - s0;
+          const int e = wid;
+          if (e < deg0) {
+            const int i = d.succ[s0 + e];
+            if (V.vac[bl + i] && V.win[bl + i] < 0) {
+              const T2* ap = static_cast<const T2*>(V.a0part);
+              T2 x{-INFINITY, -INFINITY, INT_MAX, -1};
+              for (int g2 = lane; g2 < nblk; g2 += 32)
+                t2_merge(x, ap[(static_cast<std::size_t>(b) * nblk + g2) * d.maxdeg + e]);
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {
+                T2 y;
+                y.y1 = __shfl_xor_sync(0xffffffffu, x.y1, o);
+                y.y2 = __shfl_xor_sync(0xffffffffu, x.y2, o);
+                y.id1 = __shfl_xor_sync(0xffffffffu, x.id1, o);
+                y.s1 = __shfl_xor_sync(0xffffffffu, x.s1, o);
+                t2_merge(x, y);
+              }
+              if (lane == 0) {
+                int ws = x.s1;
+                const bool near = !(x.y1 - x.y2 > 1e-9 * fmax(1.0, fabs(x.y1)));
+                if (near || V.force_slow) {
+                  // exact: ascending agent id, sequential z2 (insertion sort, one thread)
+                  if (!V.force_slow) atomicOr(&d.err[b], kErrNearTieSlow);
+                  const int nA = V.acount[par * d.B + b];
+                  unsigned long long* keys = V.sort_scratch + (static_cast<std::size_t>(b) * d.maxdeg + e) * N;
+                  for (int q = 0; q < nA; ++q) {
+                    const int s = V.alist[bn + q];
+                    const unsigned long long kk =
+                        (static_cast<unsigned long long>(d.aid[so + s]) << 32) | static_cast<unsigned>(s);
+                    int m = q - 1;
+                    while (m >= 0 && keys[m] > kk) {
+                      keys[m + 1] = keys[m];
+                      --m;
+                    }
+                    keys[m + 1] = kk;
+                  }
+                  const double vv = 0.0 - kMaskLarge;
+                  const double lzv = log(static_cast<double>(nA) * 1.0) + vv;
+                  const double logz = vv - lzv;
+                  double z2 = 0.0;
+                  for (int q = 0; q < nA; ++q) {
+                    const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
+                                            static_cast<std::uint64_t>(i), keys[q] >> 32);
+                    z2 += exp((logz + g) * d.kinv - x.y1);
+                  }
+                  double bp = -1.0;
+                  for (int q = 0; q < nA; ++q) {
+                    const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
+                                            static_cast<std::uint64_t>(i), keys[q] >> 32);
+                    const double pv = exp((logz + g) * d.kinv - x.y1) / z2;
+                    if (pv > bp) {
+                      bp = pv;
+                      ws = static_cast<int>(keys[q] & 0xffffffffull);
+                    }
+                  }
+                }
+                const int j = d.lnk[so + ws];
+                const int r = ws - offT[j];
+                bool mover;
+                const int ns = map_next(V, b, ws, j, r, offT, offN, &mover);
+                double ab;
+                if (mover) {
+                  ab = 0.0 * d.M + 0.0;
+                } else {
+                  const double xb = xbn[ns];
+                  ab = (i == j ? xb * d.M : 0.0 * d.M) + adm_bar(xb, V.x1[bn + ws], d.M);
+                }
+                V.lbar_a0[static_cast<std::size_t>(b) * d.maxdeg + e] = 0.0 + ab;
+              }
+            }
+          }
+        }
+        // position adjoint of layout t
+        for (int k = lg * kBT + tid; k < N; k += nblk * kBT) {
+          const int j = findl(offT, L, k);
+          const int base = offT[j], n = offT[j + 1] - base, r = k - base;
+          const double jam = d.jam[bl + j], dxf = d.dxf[bl + j], len = d.len[j];
+          const double x = d.pos[so + k];
+          const CfPick me = cf_step(x, r == 0 ? d.M : d.pos[so + k - 1] - x, jam, dxf, len);
+          const double x1b = x1_bar_p(V, b, k, j, r, me.x1, offT, offN, xbn);
+          const double xpb = d.tg ? x1b : (me.cap ? x1b : 0.0);
+          const double dxcb = me.cong ? xpb : 0.0;
+          const double dxfb = me.cong ? 0.0 : xpb;
+          const double gapb = me.gap >= 0.0 ? dxcb * 1.0 : 0.0;
+          double tb = 0.0;
+          if (r + 1 < n) {
+            const double xf = d.pos[so + k + 1];
+            const CfPick fo = cf_step(xf, x - xf, jam, dxf, len);
+            const double f1b = x1_bar_p(V, b, k + 1, j, r + 1, fo.x1, offT, offN, xbn);
+            const double fpb = d.tg ? f1b : (fo.cap ? f1b : 0.0);
+            const double fcb = fo.cong ? fpb : 0.0;
+            tb += (fo.gap >= 0.0 ? fcb * 1.0 : 0.0) * 1.0;
+          }
+          if (r > 0) tb += -(gapb * 1.0);
+          xbc[k] = xpb + tb * 1.0;
+          V.cu[bn + k] = (dxfb * d.dt) * 1.0;
+          V.cg[bn + k] = gapb;
+        }
+      }
+    bstamp(V, t, 5);
+    grid.sync();
+    bstamp(V, t, 6);
+    // ================= R4: link-choice VJP, reductions, resets =================
+    if (active)
+      for (int b = b0; b < d.B; b += bstep) {
+        if (!grouped) {
+          __syncthreads();
+          const int* og = d.off + oidx(d, t % d.S, b);
+          for (int j = tid; j <= L; j += kBT) offT[j] = og[j];
+          __syncthreads();
+        }
+        const std::size_t bn = static_cast<std::size_t>(b) * N, bl = static_cast<std::size_t>(b) * L;
+        const std::size_t so = sidx(d, t % d.S, b);
+        double* vbc = V.vbar + (static_cast<std::size_t>(par) * d.B * N + bn) * d.maxdeg;
+        const unsigned long long key = V.a0key[par * d.B + b];
+        const int a0s = key == ULLONG_MAX ? -1 : static_cast<int>(key & 0xffffffffull);
+        const int nA = V.acount[par * d.B + b];
+        for (int q = lg * kBT + tid; q < nA; q += nblk * kBT) {
+          const int s = V.alist[bn + q];
+          const int c = V.choice[bn + s];
+          if (c < 0) continue;
+          const int j = d.lnk[so + s];
+          const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
+          double bar[kMaxDeg], pi[kMaxDeg];
+          const double* lz = d.slogz + (bl + j) * d.maxdeg;
+          const double* lp = V.lpi + (bn + s) * d.maxdeg;
+          for (int e = 0; e < deg; ++e) {
+            bar[e] = 0.0;
+            pi[e] = lp[e];
+          }
+          const int ed = V.ched[bn + s];
+          if (V.vac[bl + c] && V.win[bl + c] >= 0) bar[ed] = V.lbar_row[bn + s];
+          if (s == a0s)
+            for (int e = 0; e < deg; ++e) bar[e] += V.lbar_a0[static_cast<std::size_t>(b) * d.maxdeg + e];
+          for (int e = 0; e < deg; ++e)
+            bar[e] = ((bar[e] * 1.0) * 1.0) * (V.vac[bl + d.succ[s0 + e]] ? 1.0 : 0.0);
+          two_softmax_vjp(deg, lz, pi, d.kinv, bar);
+          for (int e = 0; e < deg; ++e) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e];
+        }
+        // warp per link: u, kappa, alpha for step t
+        double* g5 = V.grads + static_cast<std::size_t>(b) * 5 * L;
+        const int nw = nblk * (kBT / 32);
+        for (int j = lg * (kBT / 32) + wid; j < L; j += nw) {
+          const int base = offT[j], n = offT[j + 1] - base;
+          double ub = 0.0, jb = 0.0;
+          for (int k = base + lane; k < base + n; k += 32) {
+            ub += V.cu[bn + k];
+            jb += -1.0 * V.cg[bn + k];
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            ub += __shfl_xor_sync(0xffffffffu, ub, o);
+            jb += __shfl_xor_sync(0xffffffffu, jb, o);
+          }
+          if (lane == 0) {
+            const double kap = d.kappa[bl + j];
+            if (n) {
+              g5[j] += 0.0 + ub;
+              g5[L + j] += 0.0 - jb * static_cast<double>(d.delta_n) / (kap * kap);
+            }
+            double ab = 0.0;
+            if (n) {
+              const int na = V.nA_cur[bl + j];
+              for (int r = 0; r < na; ++r) {
+                const int s = base + r;
+                const int ch = V.choice[bn + s];
+                if (ch >= 0 && V.vac[bl + ch] && V.win[bl + ch] >= 0) ab += 1.0 * V.prio_bar[bn + s];
+              }
+            }
+            g5[3 * L + j] += ab;
+          }
+        }
+        for (int i = lg * kBT + tid; i < L; i += nblk * kBT) {
+          V.ccnt[bl + i] = 0;
+          V.dep[bl + i] = 0;
+        }
+        if (lg == 0 && tid == 0) {
+          V.acount[(par ^ 1) * d.B + b] = 0;
+          V.a0key[(par ^ 1) * d.B + b] = ULLONG_MAX;
+        }
+      }
+    bstamp(V, t, 7);
+    grid.sync();
+  }
+  // deferred preference gradient of step 0
+  if (T > 0 && active)
+    for (int b = b0; b < d.B; b += bstep) {
+      __syncthreads();
+      const int* og = d.off + oidx(d, 0, b);
+      for (int j = tid; j <= L; j += kBT) offN[j] = og[j];
+      __syncthreads();
+      const std::size_t bn = static_cast<std::size_t>(b) * N, bl = static_cast<std::size_t>(b) * L;
+      double* g5 = V.grads + static_cast<std::size_t>(b) * 5 * L;
+      const int* nAn = V.nAb + bl;  // parity 0
+      const double* vbn = V.vbar + bn * d.maxdeg;
+      for (int i = lg * kBT + tid; i < L; i += nblk * kBT) {
+        double pb = 0.0;
+        for (int e = d.pred_off[i]; e < d.pred_off[i + 1]; ++e) {
+          const int p = d.pred[e];
+          const int pbse = offN[p];
+          if (offN[p + 1] == pbse) continue;
+          const int nap = nAn[p];
+          for (int r = 0; r < nap; ++r)
+            pb += vbn[static_cast<std::size_t>(pbse + r) * d.maxdeg + d.pred_pos[e]] * 1.0;
+        }
+        const double cst = d.cost[bl + i], be = d.beta[bl + i];
+        g5[2 * L + i] += 0.0 + pb / cst;
+        g5[4 * L + i] += 0.0 - pb * be / (cst * cst);
+      }
+    }
+}
+
+int backward_smem_bytes(int L, int maxdeg) {
+  return (2 * (L + 1) + 2) * 4 + (kBT / 32) * maxdeg * static_cast<int>(sizeof(T2)) + 16;
+}
+
+int backward_max_grid(int L, int maxdeg) {
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int smem = backward_smem_bytes(L, maxdeg);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(reinterpret_cast<void*>(k_backward_persistent),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<void*>(k_backward_persistent), kBT,
+                                                smem);
+  return occ * sms;
+}
+
+cudaError_t launch_backward_persistent(const BView& V, int grid, cudaStream_t st) {
+  void* args[] = {const_cast<BView*>(&V)};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_backward_persistent), dim3(grid), dim3(kBT),
+                                     args, backward_smem_bytes(V.d.L, V.d.maxdeg), st);
+}
+
+}  // namespace dtg

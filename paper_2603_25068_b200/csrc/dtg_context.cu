@@ -16,6 +16,7 @@
 #include "dtg_kernels.h"
 #include "dtg_persistent.h"
 #include "dtg_cluster.h"
+#include "dtg_backward.h"
 
 namespace {
 
@@ -93,6 +94,16 @@ struct dtg_ctx {
   DevBuf<double> snap_seed, cum_seed, x_seed;
   DevBuf<unsigned long long> sort_scratch;
   DevBuf<int> alist, acount;
+  // persistent backward
+  int bgrid_max = 0;
+  bool bwd_persistent = true;
+  DevBuf<double> bx1, btail, bmpi, bmlz, blpi;
+  DevBuf<int> bnA, bnAc, bwon, bdep, bwin, bccnt, bched, bchoice, balist, bacount;
+  DevBuf<unsigned char> bvac;
+  DevBuf<dtg::Cand> bcands;
+  DevBuf<unsigned long long> ba0key, bsort;
+  DevBuf<unsigned char> ba0part;
+  int last_bgrid = 0;
   DevBuf<int> tmp_link;
   DevBuf<double> tmp_pos;
   // last run
@@ -105,6 +116,8 @@ struct dtg_ctx {
   DevBuf<double> x1b, tailb;
   DevBuf<int> wonb, nAb, qnb, depb, winp, ccnt, clist;
   int last_grid = 0;
+  double* h_stage = nullptr;  // pinned staging for count read-back
+  std::size_t h_stage_n = 0;
   int mode = 0;          // 0 auto, 1 cluster, 2 grid-persistent, 3 step graph
   int cluster_cs_max = 0;
   bool stage_params = false;
@@ -190,6 +203,7 @@ struct dtg_ctx {
 
   ~dtg_ctx() {
     drop_graphs();
+    if (h_stage) cudaFreeHost(h_stage);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
@@ -416,6 +430,7 @@ int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
     c->ccnt.alloc(BL);
     c->clist.alloc(BL * dtg::kCandCap);
     c->pgrid_max = dtg::persistent_max_grid(L, nullptr);
+    c->bgrid_max = dtg::backward_max_grid(L, c->maxdeg);
     c->stage_params = dtg::cluster_smem_bytes(L, true) <= 200 * 1024;
     c->cluster_cs_max = dtg::cluster_smem_bytes(L, c->stage_params) <= 220 * 1024
                             ? dtg::cluster_max_size(L, c->stage_params)
@@ -497,8 +512,54 @@ int dtg_set_mode(dtg_ctx* c, int mode) {
 
 int dtg_last_mode(const dtg_ctx* c) { return c->last_mode * 100 + c->last_cs; }
 
+static void run_backward(dtg_ctx* c, const double* snap, const double* cum, const double* xs,
+                         cudaMemcpyKind kind);
+
+int dtg_profile_backward(dtg_ctx* c, double* phase_us, int* grid_out) {
+  return guarded(c, [&] {
+    if (c->last_T < 1 || !c->last_ckpt) throw std::runtime_error("needs a checkpointed forward");
+    c->want_stamps = true;
+    try {
+      run_backward(c, nullptr, nullptr, nullptr, cudaMemcpyHostToDevice);
+    } catch (...) {
+      c->want_stamps = false;
+      throw;
+    }
+    c->want_stamps = false;
+    c->sync_check();
+    const int T = c->last_T, G = c->last_bgrid;
+    std::vector<unsigned long long> s(static_cast<std::size_t>(T) * G * 8);
+    CK(cudaMemcpy(s.data(), c->stamps.p, s.size() * 8, cudaMemcpyDeviceToHost));
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int t = 0; t < T; ++t) {
+      unsigned long long mn[8], mx[8];
+      for (int w = 0; w < 8; ++w) {
+        mn[w] = ~0ull;
+        mx[w] = 0;
+      }
+      for (int g = 0; g < G; ++g)
+        for (int w = 0; w < 8; ++w) {
+          const unsigned long long v = s[(static_cast<std::size_t>(t) * G + g) * 8 + w];
+          mn[w] = std::min(mn[w], v);
+          mx[w] = std::max(mx[w], v);
+        }
+      // phase spans R1..R4 and the barrier after each
+      acc[0] += double(mx[1] - mn[0]);
+      acc[1] += double(mn[2] - mx[1]);
+      acc[2] += double(mx[3] - mn[2]);
+      acc[3] += double(mn[4] - mx[3]);
+      acc[4] += double(mx[5] - mn[4]);
+      acc[5] += double(mn[6] - mx[5]);
+      acc[6] += double(mx[7] - mn[6]);
+    }
+    for (int w = 0; w < 8; ++w) phase_us[w] = acc[w] / T / 1e3;
+    if (grid_out) *grid_out = G;
+  });
+}
+
 int dtg_set_persistent(dtg_ctx* c, int enabled) {
   c->persistent = enabled != 0;
+  c->bwd_persistent = enabled != 0;
   return DTG_OK;
 }
 
@@ -744,6 +805,29 @@ int dtg_read_cum(dtg_ctx* c, int scenario, double* cum) {
   });
 }
 
+int dtg_read_cum_all(dtg_ctx* c, double* cum) {
+  return guarded(c, [&] {
+    c->sync_check();
+    if (c->last_T < 0) throw std::runtime_error("no forward run");
+    const int T = c->last_T;
+    if (T == 0) return;
+    const std::size_t L = c->L, B = c->B, BL = B * L;
+    const std::size_t n = static_cast<std::size_t>(T) * BL;
+    if (c->h_stage_n < n) {
+      if (c->h_stage) cudaFreeHost(c->h_stage);
+      c->h_stage = nullptr;
+      c->h_stage_n = 0;
+      CK(cudaMallocHost(&c->h_stage, n * 8));
+      c->h_stage_n = n;
+    }
+    CK(cudaMemcpyAsync(c->h_stage, c->cumh.p + BL, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (std::size_t b = 0; b < B; ++b)
+      for (int t = 0; t < T; ++t)
+        std::memcpy(cum + (b * T + t) * L, c->h_stage + (t * B + b) * L, L * 8);
+  });
+}
+
 int dtg_read_state(dtg_ctx* c, int scenario, int step, int* link, double* pos) {
   return guarded(c, [&] {
     if (scenario < 0 || scenario >= c->B) throw std::invalid_argument("scenario index out of range");
@@ -768,6 +852,102 @@ int dtg_n_snapshots(const dtg_ctx* c) { return c->last_T < 0 ? 0 : c->last_K; }
 const double* dtg_device_cum(const dtg_ctx* c) { return c->cumh.p; }
 
 int64_t dtg_last_launches(const dtg_ctx* c) { return c->launches; }
+
+static void run_backward_persistent(dtg_ctx* c, cudaStream_t st) {
+  const int T = c->last_T, K = c->last_K, spi = c->last_spi;
+  const std::size_t B = c->B, L = c->L, N = c->N, BL = B * L, BN = B * N, MD = c->maxdeg;
+  const int want = (std::max(c->N, c->L) + 511) / 512;
+  int bps, grid;
+  if (static_cast<long long>(c->B) * want <= c->bgrid_max) {
+    bps = want;
+    grid = c->B * want;
+  } else if (c->B <= c->bgrid_max) {
+    bps = c->bgrid_max / c->B;
+    grid = bps * c->B;
+  } else {
+    bps = 0;
+    grid = c->bgrid_max;
+  }
+  const std::size_t nblk = bps > 0 ? bps : 1;
+  bool ch = false;
+  ch |= c->bx1.ensure(BN);
+  ch |= c->btail.ensure(BL);
+  ch |= c->bmpi.ensure(BL * dtg::kBwdCandCap);
+  ch |= c->bmlz.ensure(BL * dtg::kBwdCandCap);
+  ch |= c->blpi.ensure(BN * MD);
+  ch |= c->bnA.ensure(2 * BL);
+  ch |= c->bnAc.ensure(BL);
+  ch |= c->bwon.ensure(BN);
+  ch |= c->bdep.ensure(BL);
+  ch |= c->bwin.ensure(BL);
+  ch |= c->bccnt.ensure(BL);
+  ch |= c->bched.ensure(BN);
+  ch |= c->bchoice.ensure(BN);
+  ch |= c->balist.ensure(BN);
+  ch |= c->bacount.ensure(2 * B);
+  ch |= c->bvac.ensure(BL);
+  ch |= c->bcands.ensure(BL * dtg::kBwdCandCap);
+  ch |= c->ba0key.ensure(2 * B);
+  ch |= c->bsort.ensure(B * MD * N);
+  ch |= c->ba0part.ensure(B * nblk * MD * 32);
+  ch |= c->vbar.ensure(2 * BN * MD);
+  (void)ch;
+  CK(cudaMemsetAsync(c->bccnt.p, 0, BL * 4, st));
+  CK(cudaMemsetAsync(c->bdep.p, 0, BL * 4, st));
+  CK(cudaMemsetAsync(c->bacount.p, 0, 2 * B * 4, st));
+  CK(cudaMemsetAsync(c->ba0key.p, 0xff, 2 * B * 8, st));
+  CK(cudaMemsetAsync(c->errf.p, 0, B * 4, st));
+  dtg::BView V{};
+  V.d = c->view();
+  V.x1 = c->bx1.p;
+  V.nAb = c->bnA.p;
+  V.nA_cur = c->bnAc.p;
+  V.tail = c->btail.p;
+  V.won = c->bwon.p;
+  V.dep = c->bdep.p;
+  V.win = c->bwin.p;
+  V.vac = c->bvac.p;
+  V.ccnt = c->bccnt.p;
+  V.cands = c->bcands.p;
+  V.mpi = c->bmpi.p;
+  V.mlz = c->bmlz.p;
+  V.lpi = c->blpi.p;
+  V.ched = c->bched.p;
+  V.choice = c->bchoice.p;
+  V.alist = c->balist.p;
+  V.acount = c->bacount.p;
+  V.a0key = c->ba0key.p;
+  V.a0part = c->ba0part.p;
+  V.xbar = c->xbar.p;
+  V.cbar = c->cbar.p;
+  V.qbar = c->qbar.p;
+  V.qtot = c->qtot.p;
+  V.lbar_row = c->lbar_row.p;
+  V.prio_bar = c->prio_bar.p;
+  V.lbar_a0 = c->lbar_a0.p;
+  V.vbar = c->vbar.p;
+  V.cu = c->cu.p;
+  V.cg = c->cg.p;
+  V.grads = c->grads.p;
+  V.snap_seed = K ? c->snap_seed.p : nullptr;
+  V.cum_seed = c->cum_seed.p;
+  V.x_seed = c->x_seed.p;
+  V.sort_scratch = c->bsort.p;
+  V.K = K;
+  V.spi = spi;
+  V.T = T;
+  V.bps = bps;
+  V.force_slow = c->force_slow;
+  V.tstamp = nullptr;
+  if (c->want_stamps) {
+    c->stamps.ensure(static_cast<std::size_t>(T) * grid * 8);
+    V.tstamp = c->stamps.p;
+  }
+  c->last_bgrid = grid;
+  CK(dtg::launch_backward_persistent(V, grid, st));
+  c->launches = 1;
+  c->pending = true;
+}
 
 static void run_backward(dtg_ctx* c, const double* snap, const double* cum, const double* xs,
                          cudaMemcpyKind kind) {
@@ -804,6 +984,10 @@ static void run_backward(dtg_ctx* c, const double* snap, const double* cum, cons
   if (K) up(c->snap_seed.p, snap, B * K * L);
   up(c->cum_seed.p, cum, B * L);
   up(c->x_seed.p, xs, B * N);
+  if (c->bwd_persistent && c->bgrid_max > 0 && c->mode != 3 && T > 0) {
+    run_backward_persistent(c, st);
+    return;
+  }
   dtg::DevView d = c->view();
   d.alist = c->alist.p;
   d.acount = c->acount.p;

@@ -441,13 +441,16 @@ CompactState read_state(dtg_ctx* c, int b, int step, int N) {
   return st;
 }
 
-std::vector<std::vector<double>> read_cum(dtg_ctx* c, int b, int T, int L) {
-  std::vector<double> flat(static_cast<std::size_t>(T) * L);
-  check(c, dtg_read_cum(c, b, flat.data()));
-  std::vector<std::vector<double>> out(T);
-  for (int t = 0; t < T; ++t)
-    out[t].assign(flat.begin() + static_cast<std::size_t>(t) * L,
-                  flat.begin() + static_cast<std::size_t>(t + 1) * L);
+// Every scenario's per-step cumulative counts with one device->host copy.
+std::vector<std::vector<std::vector<double>>> read_cum_all(dtg_ctx* c, int B, int T, int L) {
+  std::vector<double> flat(static_cast<std::size_t>(B) * T * L);
+  if (T) check(c, dtg_read_cum_all(c, flat.data()));
+  std::vector<std::vector<std::vector<double>>> out(B, std::vector<std::vector<double>>(T));
+  for (int b = 0; b < B; ++b)
+    for (int t = 0; t < T; ++t) {
+      const auto it = flat.begin() + (static_cast<std::size_t>(b) * T + t) * L;
+      out[b][t].assign(it, it + L);
+    }
   return out;
 }
 
@@ -461,10 +464,11 @@ std::vector<Trajectory> simulate_forward_draws(const Scenario& s, const LinkPara
   const Prepared p = prepare(s, params, rng, its);
   check(p.ctx, dtg_forward(p.ctx, p.T, p.spi, record_states ? 1 : 0));
   std::vector<Trajectory> out(p.B);
+  auto cums = read_cum_all(p.ctx, p.B, p.T, p.L);
   for (int b = 0; b < p.B; ++b) {
     Trajectory& tr = out[b];
     tr.steps = p.T;
-    tr.cum_per_step = read_cum(p.ctx, b, p.T, p.L);
+    tr.cum_per_step = std::move(cums[b]);
     tr.final_state = read_state(p.ctx, b, p.T, p.N);
     tr.cum_final = p.T ? tr.cum_per_step.back() : std::vector<double>(p.L, 0.0);
     if (record_states)
@@ -498,9 +502,10 @@ std::vector<GradResult> simulate_gradient_draws(const Scenario& s, const LinkPar
   const std::size_t L = p.L, N = p.N;
   std::vector<double> snap_seed(static_cast<std::size_t>(p.B) * K * L, 0.0);
   std::vector<double> cum_seed(p.B * L, 0.0), x_seed(p.B * N, 0.0);
+  const auto cums = read_cum_all(p.ctx, p.B, p.T, p.L);
   for (int b = 0; b < p.B; ++b) {
     GradResult& g = res[b];
-    const auto cum = read_cum(p.ctx, b, p.T, p.L);
+    const auto& cum = cums[b];
     for (int t = 0; t < p.T; ++t)
       if ((t + 1) % p.spi == 0) g.snapshot_values.push_back(cum[t]);
     g.cum_final_values = p.T ? cum.back() : std::vector<double>(L, 0.0);

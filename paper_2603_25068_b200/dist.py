@@ -83,8 +83,7 @@ class ShardedGradient:
             e.set_noise(root_seed, noise_iterations[k], b)
         e.forward(T, spi, checkpoint=True)
         K = T // spi
-        cum = np.stack([e.read_cum(b) for b in range(len(self.mine))]) if T else \
-            np.zeros((len(self.mine), 0, sc.n_links))
+        cum = e.read_cum_all() if T else np.zeros((len(self.mine), 0, sc.n_links))
         snaps = cum[:, spi - 1::spi][:, :K]
         cum_final = cum[:, -1] if T else np.zeros((len(self.mine), sc.n_links))
         loss, snap_seeds, cum_seeds = seeds_fn(snaps, cum_final)

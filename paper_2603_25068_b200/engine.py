@@ -308,6 +308,14 @@ class Engine:
         self._check(self._lib.dtg_profile_persistent(self._h, T, steps_per_interval, ph, C.byref(g)))
         return dict(zip(["slot_phase", "barrier1", "link_phase", "barrier2"], ph.tolist())), g.value
 
+    def profile_backward(self):
+        """Mean per-step span (us) of the persistent reverse sweep's phases."""
+        ph = np.zeros(8)
+        g = C.c_int()
+        self._check(self._lib.dtg_profile_backward(self._h, ph, C.byref(g)))
+        names = ["R1", "bar1", "R2", "bar2", "R3", "bar3", "R4"]
+        return dict(zip(names, ph[:7].tolist())), g.value
+
     def force_slow_path(self, on: bool):
         self._check(self._lib.dtg_debug_force_slow_path(self._h, int(on)))
 
@@ -330,6 +338,12 @@ class Engine:
     def read_cum(self, scenario: int = 0) -> np.ndarray:
         out = np.zeros((self.T, self.L))
         self._check(self._lib.dtg_read_cum(self._h, scenario, out))
+        return out
+
+    def read_cum_all(self) -> np.ndarray:
+        """[B, T, L] cumulative counts of every scenario (one device copy)."""
+        out = np.zeros((self.B, self.T, self.L))
+        self._check(self._lib.dtg_read_cum_all(self._h, out))
         return out
 
     def read_state(self, scenario: int = 0, step: int = -1):

@@ -50,3 +50,34 @@ def test_persistent_equals_step_graph(n, length, veh, dn, T, B):
             assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), mode
         for x, y in zip(a[2], ref[2]):
             assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), mode
+
+
+@pytest.mark.parametrize("n,length,veh,dn,T,B,tg", [
+    (4, 400.0, 1000, 1, 600, 2, True),
+    (4, 400.0, 1000, 1, 300, 1, False),
+    (6, 300.0, 2400, 2, 300, 3, True),
+    (23, 1609.34, 1000020, 30, 60, 8, True),
+    (4, 400.0, 1000, 1, 100, 300, True),  # scenario loop in the persistent reverse sweep
+])
+def test_persistent_backward_equals_step_graph(n, length, veh, dn, T, B, tg):
+    sc = P.Scenario.grid(n, length, 42, 1000.0).configure(veh, dn, T, 300 if dn <= 2 else 300,
+                                                        trajectory_grafting=tg)
+    p = sc.sample_parameters(3)
+    spi = sc.steps_per_interval
+    K = T // spi
+    lk, ps = sc.seed_agents()
+    rng = np.random.default_rng(4)
+    snap = rng.normal(size=(B, K, sc.n_links))
+    cum = rng.normal(size=(B, sc.n_links))
+    xs = rng.normal(size=(B, sc.n_agents))
+    out = []
+    for mode in (0, 3):
+        e = P.Engine(sc, B, T)
+        e.set_mode(mode)
+        e.set_params(p)
+        e.set_state(lk, ps)
+        for b in range(B):
+            e.set_noise(7, 50 + b, b)
+        e.forward(T, spi, checkpoint=True)
+        out.append(e.backward(snap_seeds=snap if K else None, cum_seeds=cum, x_seeds=xs))
+    assert np.array_equal(out[0], out[1])
