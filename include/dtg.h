@@ -91,6 +91,9 @@ int dtg_set_mode(dtg_ctx* ctx, int mode);
  * R2, barrier, R3, barrier, R4 (and 0). */
 int dtg_profile_backward(dtg_ctx* ctx, double* phase_us, int* grid_out);
 int dtg_last_mode(const dtg_ctx* ctx);
+/* Tuning knobs: flag 0 = grid barrier implementation (1: release/acquire
+ * counter, default; 0: cooperative_groups grid.sync). */
+int dtg_set_flag(dtg_ctx* ctx, int flag, int value);
 /* Measurement hook: one persistent forward with %globaltimer stamps; returns
  * the mean per-step span (us) of [slot phase, barrier 1, link phase,
  * barrier 2] over all CTAs and the grid size used. */
@@ -133,6 +136,16 @@ int dtg_debug_force_slow_path(dtg_ctx* ctx, int on);
  * cols[i]), computed by the device code path (libdevice log). */
 int dtg_debug_gumbel(uint64_t seed, uint64_t key, int n, const uint64_t* rows,
                      const uint64_t* cols, double* out);
+
+/* Test hook: clock64 cycles per dependent primitive on the device
+ * (which: 0 Gumbel draw, 1 log, 2 exp, 3 division, 4 L2 pointer chase,
+ * 5 counter-RNG uniform; 100 = empty grid.sync with `grid` CTAs of 512). */
+int dtg_debug_microbench(int which, int n, int grid, double* result);
+/* Test hook: one fused forward recording, per step and warp, the slot-phase
+ * start, end of the offsets prologue, end of the slot loop (globaltimer ns)
+ * and the number of arrived agents in the warp: out[T][n_warps][4]. */
+int dtg_debug_warp_records(dtg_ctx* ctx, int n_steps, int steps_per_interval,
+                           unsigned long long* out, int* n_warps);
 
 /* Results of the last dtg_forward.
  * cum_per_step: n_steps x L cumulative counts (Trajectory::cum_per_step).

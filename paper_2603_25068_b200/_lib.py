@@ -66,6 +66,7 @@ SIGNATURES = [
     ("dtg_set_graphs", i32, [vp, i32]),
     ("dtg_set_persistent", i32, [vp, i32]),
     ("dtg_set_mode", i32, [vp, i32]),
+    ("dtg_set_flag", i32, [vp, i32, i32]),
     ("dtg_profile_backward", i32, [vp, _dp, C.POINTER(C.c_int)]),
     ("dtg_last_mode", i32, [vp]),
     ("dtg_profile_persistent", i32, [vp, i32, i32, _dp, C.POINTER(C.c_int)]),
@@ -108,6 +109,8 @@ SIGNATURES = [
     ("dtg_scenario_ctx", vp, [vp]),
     ("dtg_mse_loss", i32, [i32, i32, _dp, i32, _ip, i32, _dp, i32, _dp, _dp]),
     ("dtg_debug_gumbel", i32, [u64, u64, i32, _u64p, _u64p, _dp]),
+    ("dtg_debug_microbench", i32, [i32, i32, i32, _dp]),
+    ("dtg_debug_warp_records", i32, [vp, i32, i32, vp, C.POINTER(C.c_int)]),
     ("dtg_scenario_last_error", C.c_char_p, [vp]),
 ]
 

@@ -219,20 +219,26 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
             const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
             int c = -1;
             if (deg > 0) {
-              double g[kMaxDeg], pi[kMaxDeg];
+              double g[kMaxDeg], gm[kMaxDeg], pi[kMaxDeg];
+              int sc[kMaxDeg];
               const double* lz = d.slogz + (bl + j) * d.maxdeg;
-              for (int e = 0; e < deg; ++e)
-                g[e] = gumbel(d.seed_link[b], static_cast<std::uint64_t>(t), static_cast<std::uint64_t>(a),
-                              static_cast<std::uint64_t>(d.succ[s0 + e]));
+              const std::uint64_t h2l = rng_prefix2(rng_prefix1(d.seed_link[b], static_cast<std::uint64_t>(t)),
+                                                    static_cast<std::uint64_t>(a));
+              for (int e = 0; e < deg; ++e) {
+                sc[e] = d.succ[s0 + e];
+                g[e] = gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sc[e])));
+              }
               const int ed = softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi);
-              c = d.succ[s0 + ed];
+              c = sc[ed];
+              gm[ed] = gumbel_bits(rng_final(rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
+                                                         static_cast<std::uint64_t>(c)),
+                                             static_cast<std::uint64_t>(a)));
               double* lp = V.lpi + (bn + k) * d.maxdeg;
               for (int e = 0; e < deg; ++e) lp[e] = pi[e];
               V.ched[bn + k] = ed;
               Cand cd;
               cd.alpha = d.alpha[bl + j];
-              cd.g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t), static_cast<std::uint64_t>(c),
-                            static_cast<std::uint64_t>(a));
+              cd.g = gm[ed];
               cd.slot = k;
               cd.aid = a;
               cd.link = j;
@@ -347,12 +353,14 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           const double logz = vv - lzv;
           T2 tp[kMaxDeg];
           for (int e = 0; e < deg0; ++e) tp[e] = T2{-INFINITY, -INFINITY, INT_MAX, -1};
+          std::uint64_t h2r[kMaxDeg];  // row prefixes of the merge stream
+          const std::uint64_t h1m = rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t));
+          for (int e = 0; e < deg0; ++e) h2r[e] = rng_prefix2(h1m, static_cast<std::uint64_t>(d.succ[s0 + e]));
           for (int q = lg * kBT + tid; q < nA; q += nblk * kBT) {
             const int s = V.alist[bn + q];
             const int id = d.aid[so + s];
             for (int e = 0; e < deg0; ++e) {
-              const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
-                                      static_cast<std::uint64_t>(d.succ[s0 + e]), static_cast<std::uint64_t>(id));
+              const double g = gumbel_bits(rng_final(h2r[e], static_cast<std::uint64_t>(id)));
               t2_push(tp[e], (logz + g) * d.kinv, id, s);
             }
           }

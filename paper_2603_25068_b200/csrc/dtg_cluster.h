@@ -1,4 +1,4 @@
-// Cluster-per-scenario forward kernel (dtg_cluster.cu).
+// Fused forward kernel (dtg_fused.cu): shared types and launchers.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -36,11 +36,14 @@ struct CView {
   int cs;              // CTAs per cluster = per scenario
   int stage_params;    // per-link constants in shared memory
   unsigned long long* tstamp;  // optional [T][grid][4]
+  unsigned int* gbar;  // grid-barrier counter (null: cooperative_groups grid.sync)
+  unsigned long long* wstamp;  // optional per-warp slot-phase record [T][warps][4]
 };
 
-int cluster_smem_bytes(int L, bool stage_params);
-int cluster_max_size(int L, bool stage_params);
 void launch_pack_succ(const DevView& d, double* srec, cudaStream_t st);
-cudaError_t launch_forward_cluster(const CView& V, cudaStream_t st);
+int fused_smem_bytes(int L, bool stage_params);
+int fused_max_grid(int L, bool stage_params);
+int fused_max_cluster(int L, bool stage_params);
+cudaError_t launch_forward_fused(const CView& V, bool cluster, cudaStream_t st);
 
 }  // namespace dtg

@@ -14,7 +14,6 @@
 
 #include "../../include/dtg.h"
 #include "dtg_kernels.h"
-#include "dtg_persistent.h"
 #include "dtg_cluster.h"
 #include "dtg_backward.h"
 
@@ -69,7 +68,8 @@ struct dtg_ctx {
   int force_slow = 0;
   std::string err;
   // static network
-  DevBuf<int> succ_off, succ, pred_off, pred, pred_pos;
+  DevBuf<int> succ_off, succ, pred_off, pred, pred_pos, succ_pedge;
+  int E = 0;
   DevBuf<double> len, thr, ctr, sc;
   // parameters / seeds
   DevBuf<double> params;  // [5][B][L]
@@ -123,6 +123,10 @@ struct dtg_ctx {
   bool stage_params = false;
   int last_mode = 0, last_cs = 0;
   DevBuf<double> srec;
+  DevBuf<unsigned int> gbar;
+  bool custom_barrier = true;
+  bool want_wstamp = false;
+  DevBuf<unsigned long long> wst;
   DevBuf<dtg::Cand> cands;
   bool want_stamps = false;
   DevBuf<unsigned long long> stamps;
@@ -147,6 +151,7 @@ struct dtg_ctx {
     d.pred_off = pred_off.p;
     d.pred = pred.p;
     d.pred_pos = pred_pos.p;
+    d.succ_pedge = succ_pedge.p;
     d.len = len.p;
     d.thr = thr.p;
     d.ctr = ctr.p;
@@ -364,12 +369,13 @@ int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
       throw Unsupported("link out-degree " + std::to_string(c->maxdeg) + " exceeds " +
                         std::to_string(dtg::kMaxDeg));
     for (int j = 0; j < L; ++j) pcnt[j + 1] += pcnt[j];
-    std::vector<int> pr(E), pp(E), fill(pcnt.begin(), pcnt.end() - 1);
+    std::vector<int> pr(E), pp(E), spe(std::max(E, 1)), fill(pcnt.begin(), pcnt.end() - 1);
     for (int i = 0; i < L; ++i)  // ascending predecessor id per link
       for (int e = so[i]; e < so[i + 1]; ++e) {
         const int q = fill[su[e]]++;
         pr[q] = i;
         pp[q] = e - so[i];
+        spe[e] = q;  // global predecessor-edge index of successor edge e
       }
     std::vector<double> ln(net->length, net->length + L), th(L), ct(L), sc(L);
     for (int j = 0; j < L; ++j) {
@@ -385,6 +391,8 @@ int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
     h2d(c->pred_off, pcnt, st);
     h2d(c->pred, pr, st);
     h2d(c->pred_pos, pp, st);
+    h2d(c->succ_pedge, spe, st);
+    c->E = E;
     h2d(c->len, ln, st);
     h2d(c->thr, th, st);
     h2d(c->ctr, ct, st);
@@ -428,13 +436,12 @@ int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
     c->depb.alloc(2 * BL);
     c->winp.alloc(BL);
     c->ccnt.alloc(BL);
-    c->clist.alloc(BL * dtg::kCandCap);
-    c->pgrid_max = dtg::persistent_max_grid(L, nullptr);
+    c->clist.alloc(1);
+    c->stage_params = dtg::fused_smem_bytes(L, true) <= 200 * 1024;
+    c->pgrid_max = dtg::fused_max_grid(L, c->stage_params);
     c->bgrid_max = dtg::backward_max_grid(L, c->maxdeg);
-    c->stage_params = dtg::cluster_smem_bytes(L, true) <= 200 * 1024;
-    c->cluster_cs_max = dtg::cluster_smem_bytes(L, c->stage_params) <= 220 * 1024
-                            ? dtg::cluster_max_size(L, c->stage_params)
-                            : 0;
+    c->cluster_cs_max = dtg::fused_max_cluster(L, c->stage_params);
+    c->gbar.alloc(1);
     c->srec.alloc(BL * c->maxdeg);
     c->cands.alloc(BL * dtg::kClusterCandCap);
     c->ensure_history(std::max(1, max_steps), 0);
@@ -502,6 +509,31 @@ int dtg_profile_persistent(dtg_ctx* c, int T, int spi, double* phase_us, int* gr
     for (int w = 0; w < 4; ++w) phase_us[w] = acc[w] / T / 1e3;
     if (grid_out) *grid_out = G;
   });
+}
+
+// Measurement hook: per-warp slot-phase records [T][warps][4] (start, after
+// offsets, after slot loop, arrived agents in the warp).
+int dtg_debug_warp_records(dtg_ctx* c, int T, int spi, unsigned long long* out, int* n_warps) {
+  return guarded(c, [&] {
+    c->want_wstamp = true;
+    const int rc = dtg_forward(c, T, spi, 0);
+    c->want_wstamp = false;
+    if (rc) throw std::runtime_error(c->err);
+    c->sync_check();
+    const std::size_t nw = static_cast<std::size_t>(c->last_grid) * (dtg::kClusterThreads / 32);
+    *n_warps = static_cast<int>(nw);
+    if (out) CK(cudaMemcpy(out, c->wst.p, static_cast<std::size_t>(T) * nw * 4 * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int dtg_set_flag(dtg_ctx* c, int flag, int value) {
+  switch (flag) {
+    case 0:  // grid barrier: 1 release/acquire counter (default), 0 cooperative_groups grid.sync
+      c->custom_barrier = value != 0;
+      return DTG_OK;
+    default:
+      return fail(c, DTG_ERR_CONFIG, "unknown flag");
+  }
 }
 
 int dtg_set_mode(dtg_ctx* c, int mode) {
@@ -661,11 +693,10 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
     // auto: the persistent grid schedule measured fastest (profiles/r01/phase_*.log)
     if (mode == 0) mode = c->persistent ? 2 : 3;
     if (mode == 1 && !cluster_ok) mode = 2;
-    if (mode == 2 && c->pgrid_max <= 0) mode = 3;
+    if (mode == 2 && (c->pgrid_max <= 0 || c->B > c->pgrid_max)) mode = 3;
     if (!c->persistent && c->mode == 0) mode = 3;
     c->last_mode = mode;
-    if (mode == 1 && T > 0) {
-      if (cs < 1) cs = 1;
+    if ((mode == 1 || mode == 2) && T > 0) {
       dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
       dtg::launch_pack_succ(d, c->srec.p, st);
       CK(cudaMemcpyAsync(c->pos.p, c->pos0.p, BN * 8, cudaMemcpyDeviceToDevice, st));
@@ -678,6 +709,7 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       CK(cudaMemsetAsync(c->errf.p, 0, sizeof(int) * c->B, st));
       CK(cudaMemsetAsync(c->ccnt.p, 0, BL * 4, st));
       CK(cudaMemsetAsync(c->depb.p, 0, 2 * BL * 4, st));
+      CK(cudaMemsetAsync(c->gbar.p, 0, sizeof(unsigned int), st));
       dtg::CView V{};
       V.d = d;
       V.x1b = c->x1b.p;
@@ -691,70 +723,29 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       V.cands = c->cands.p;
       V.srec = c->srec.p;
       V.T = T;
-      V.cs = cs;
       V.stage_params = c->stage_params ? 1 : 0;
       V.tstamp = nullptr;
-      c->last_grid = c->B * cs;
-      c->last_cs = cs;
+      V.gbar = c->custom_barrier ? c->gbar.p : nullptr;
+      if (mode == 1) {
+        V.cs = cs;
+      } else {
+        // CTAs per scenario: one slot per thread, capped by the resident grid
+        const int want = (std::max(c->N, c->L) + dtg::kClusterThreads - 1) / dtg::kClusterThreads;
+        V.cs = std::max(1, std::min(want, c->pgrid_max / c->B));
+      }
+      c->last_grid = c->B * V.cs;
+      c->last_cs = V.cs;
+      V.wstamp = nullptr;
+      if (c->want_wstamp) {
+        c->wst.ensure(static_cast<std::size_t>(T) * c->B * V.cs * (dtg::kClusterThreads / 32) * 4 + 4);
+        V.wstamp = c->wst.p;
+      }
       if (c->want_stamps) {
         c->stamps.ensure(static_cast<std::size_t>(T) * c->last_grid * 4);
         V.tstamp = c->stamps.p;
       }
-      CK(dtg::launch_forward_cluster(V, st));
+      CK(dtg::launch_forward_fused(V, mode == 1, st));
       c->launches = 3;
-      c->last_T = T;
-      c->last_spi = spi;
-      c->last_ckpt = checkpoint;
-      c->last_K = T / spi;
-      c->pending = true;
-      return;
-    }
-    if (mode == 2 && T > 0) {
-      // setup copies, then ONE cooperative launch for all T steps
-      dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
-      dtg::launch_pack_succ(d, c->srec.p, st);
-      CK(cudaMemcpyAsync(c->pos.p, c->pos0.p, BN * 8, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(c->aid.p, c->aid0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(c->lnk.p, c->lnk0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(c->off.p, c->off0.p, static_cast<std::size_t>(c->B) * (c->L + 1) * 4,
-                         cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(c->qh.p, c->q0.p, BL * 8, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemsetAsync(c->cumh.p, 0, BL * 8, st));
-      CK(cudaMemsetAsync(c->errf.p, 0, sizeof(int) * c->B, st));
-      CK(cudaMemsetAsync(c->ccnt.p, 0, BL * 4, st));
-      CK(cudaMemsetAsync(c->depb.p, 0, 2 * BL * 4, st));
-      dtg::PView P{};
-      P.d = d;
-      P.x1b = c->x1b.p;
-      P.wonb = c->wonb.p;
-      P.nAb = c->nAb.p;
-      P.qnb = c->qnb.p;
-      P.tailb = c->tailb.p;
-      P.depb = c->depb.p;
-      P.win = c->winp.p;
-      P.ccnt = c->ccnt.p;
-      P.clist = c->clist.p;
-      P.T = T;
-      const int want = (std::max(c->N, c->L) + 511) / 512;  // CTAs per scenario
-      int grid;
-      if (static_cast<long long>(c->B) * want <= c->pgrid_max) {
-        P.bps = want;
-        grid = c->B * want;
-      } else if (c->B <= c->pgrid_max) {
-        P.bps = c->pgrid_max / c->B;
-        grid = P.bps * c->B;
-      } else {
-        P.bps = 0;
-        grid = c->pgrid_max;
-      }
-      c->last_grid = grid;
-      P.tstamp = nullptr;
-      if (c->want_stamps) {
-        c->stamps.ensure(static_cast<std::size_t>(T) * grid * 4);
-        P.tstamp = c->stamps.p;
-      }
-      CK(dtg::launch_forward_persistent(P, grid, st));
-      c->launches = 2;
       c->last_T = T;
       c->last_spi = spi;
       c->last_ckpt = checkpoint;

@@ -1,0 +1,508 @@
+// Fused forward engine: all T engine steps of all B scenarios in ONE launch,
+// two barriers per step.  One template, two schedules:
+//   kCluster = false  a cooperative grid; a scenario owns `nblk` CTAs and all
+//                     CTAs meet at grid barriers (default schedule);
+//   kCluster = true   one thread-block cluster per scenario with hardware
+//                     cluster barriers; independent clusters never wait for
+//                     each other.
+//
+// Step t (engine_step, src/engine.cpp:70-125):
+//   slot phase   each CTA derives layout t's segment offsets in shared memory
+//                from layout t-1's (kept in smem across steps) and step t-1's
+//                departures / entrants (staged in smem), pulls its slots of
+//                layout t from step t-1 (stable compaction, entrants at 0.0),
+//                writes the checkpoint, runs car-following with per-link
+//                constants from smem, writes the prefix-boundary counts; an
+//                arrived head draws its next link (first-stage log-softmax
+//                precomputed per link), draws its own merge Gumbel for that
+//                link and registers {alpha, g, slot, id, link} with one atomic.
+//   barrier
+//   link phase   count/cum update, vacancy, merge softmax over the registered
+//                records in ascending id, departures.
+//   barrier
+#include <cooperative_groups.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "dtg_cluster.h"
+#include "dtg_device.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dtg {
+
+namespace {
+
+constexpr int kBatch = 4;   // slots per thread in flight together
+
+// Link choice of one arrived head (node_model.cpp:45-97, first stage
+// precomputed per link) and its own merge noise for the chosen row; registers
+// the head as a merge column {alpha, g', slot, id, link} of that row.
+__device__ void head_choice(const CView& V, std::size_t bl, std::uint64_t h1l, std::uint64_t h1m, int k, int j,
+                            int a, const int* soff_s, const double* slz) {
+  const DevView& d = V.d;
+  const int sb = soff_s[j], deg = soff_s[j + 1] - sb;
+  double g[kMaxDeg], pi[kMaxDeg];
+  const std::uint64_t h2l = rng_prefix2(h1l, static_cast<std::uint64_t>(a));
+  for (int e = 0; e < deg; ++e) g[e] = gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(d.succ[sb + e])));
+  const int ed = softmax_stage2<kMaxDeg>(deg, slz + static_cast<std::size_t>(j) * d.maxdeg, g, d.kinv, pi);
+  const int c = d.succ[sb + ed];
+  Cand cd;
+  cd.alpha = d.alpha[bl + j];
+  cd.g = gumbel_bits(rng_final(rng_prefix2(h1m, static_cast<std::uint64_t>(c)), static_cast<std::uint64_t>(a)));
+  cd.slot = k;
+  cd.aid = a;
+  cd.link = j;
+  cd.pad = 0;
+  const int qq = atomicAdd(&V.ccnt[bl + c], 1);
+  if (qq < kClusterCandCap) V.cands[(bl + c) * kClusterCandCap + qq] = cd;
+}
+
+__device__ __forceinline__ int find_link_f(const int* off_s, int L, int k) {
+  int lo = 0, hi = L - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off_s[mid] <= k)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int pull_f(int j, int rn, const int* offA, const int* offB, const int* na_s,
+                                      const int* dep_s, const int* win_s, const int* wonp, bool* entrant) {
+  const int w = win_s[j];
+  if (w >= 0 && rn == offB[j + 1] - offB[j] - 1) {
+    *entrant = true;
+    return w;
+  }
+  *entrant = false;
+  const int ob = offA[j];
+  const int na = na_s[j];
+  const int dp = dep_s[j];
+  if (rn >= na - dp) return ob + rn + dp;
+  int c = -1;
+  for (int q = 0; q < na; ++q)
+    if (!wonp[ob + q] && ++c == rn) return ob + q;
+  return ob;
+}
+
+__device__ void scan_f(int* v, int n, int* tmp) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (n + nt - 1) / nt;
+  const int j0 = min(n, tid * per), j1 = min(n, j0 + per);
+  int s = 0;
+  for (int j = j0; j < j1; ++j) s += v[j];
+  const int lane = tid & 31, wid = tid >> 5;
+  int x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int w = lane < (nt >> 5) ? tmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    tmp[lane] = w;
+  }
+  __syncthreads();
+  int run = (wid ? tmp[wid - 1] : 0) + x - s;
+  const int total = tmp[(nt >> 5) - 1];
+  __syncthreads();
+  for (int j = j0; j < j1; ++j) {
+    const int c = v[j];
+    v[j] = run;
+    run += c;
+  }
+  if (tid == 0) v[n] = total;
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gnow() {
+  unsigned long long ns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  return ns;
+}
+
+__device__ __forceinline__ void fstamp(const CView& V, int t, int w) {
+  if (V.tstamp == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    V.tstamp[(static_cast<std::size_t>(t) * gridDim.x + blockIdx.x) * 4 + w] = ns;
+  }
+}
+
+// Grid barrier: one release-add per CTA on a monotone counter, acquire spin.
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    const unsigned int target = epoch * gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+template <bool kCluster>
+__global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  const DevView& d = V.d;
+  const int L = d.L, N = d.N;
+  int rank, b;
+  if (kCluster) {
+    rank = static_cast<int>(cg::this_cluster().block_rank());
+    b = blockIdx.x / V.cs;
+  } else {
+    rank = blockIdx.x % V.cs;
+    b = blockIdx.x / V.cs;
+  }
+  const bool active = b < d.B;
+  const int nthr = V.cs * blockDim.x;
+  const int gt0 = rank * blockDim.x + threadIdx.x;
+  unsigned int epoch = 0;
+  auto barrier = [&]() {
+    if (kCluster)
+      cg::this_cluster().sync();
+    else if (V.gbar)
+      grid_barrier(V.gbar, epoch);
+    else
+      cg::this_grid().sync();
+  };
+  // ---- shared memory layout ----
+  double *jam_s = nullptr, *dxf_s = nullptr, *len_s = nullptr;
+  double* dp = reinterpret_cast<double*>(sm_raw);
+  if (V.stage_params) {
+    jam_s = dp;
+    dxf_s = dp + L;
+    len_s = dp + 2 * L;
+    dp += 3 * L;
+  }
+  int* ip = reinterpret_cast<int*>(dp);
+  int* offA = ip;
+  int* offB = ip + (L + 1);
+  int* na_s = ip + 2 * (L + 1);
+  int* dep_s = na_s + L;
+  int* win_s = dep_s + L;
+  int* soff_s = win_s + L;  // succ_off, L + 1
+  int* poff_s = soff_s + (L + 1);  // pred_off, L + 1
+  int* tmp = poff_s + (L + 1);
+  const int bb = active ? b : 0;
+  const std::size_t bl = static_cast<std::size_t>(bb) * L;
+  const std::size_t bn = static_cast<std::size_t>(bb) * N;
+  const std::size_t BL = static_cast<std::size_t>(d.B) * L;
+  const std::size_t BN = static_cast<std::size_t>(d.B) * N;
+  if (active) {
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+      if (V.stage_params) {
+        jam_s[j] = d.jam[bl + j];
+        dxf_s[j] = d.dxf[bl + j];
+        len_s[j] = d.len[j];
+      }
+      soff_s[j] = d.succ_off[j];
+      poff_s[j] = d.pred_off[j];
+    }
+    if (threadIdx.x == 0) {
+      soff_s[L] = d.succ_off[L];
+      poff_s[L] = d.pred_off[L];
+    }
+    const int* og = d.off + oidx(d, 0, bb);
+    for (int j = threadIdx.x; j <= L; j += blockDim.x) offB[j] = og[j];
+  }
+  __syncthreads();
+  const std::uint64_t seed_link = d.seed_link[bb], seed_merge = d.seed_merge[bb];
+  const double* slz = d.slogz + bl * d.maxdeg;
+
+  for (int t = 0; t <= V.T; ++t) {
+    const bool last = t == V.T;
+    const int cur = t & 1, prv = cur ^ 1;
+    const std::uint64_t h1l = rng_prefix1(seed_link, static_cast<std::uint64_t>(t));
+    const std::uint64_t h1m = rng_prefix1(seed_merge, static_cast<std::uint64_t>(t));
+    if (!last) fstamp(V, t, 0);
+    const unsigned long long wst0 = V.wstamp ? gnow() : 0;
+    unsigned long long wt1 = 0;
+    int n_arr = 0;
+    if (active) {
+      // ---------------- slot phase ----------------
+      if (t > 0) {
+        int* sw = offA;
+        offA = offB;
+        offB = sw;
+        const int* nAp = V.nAb + prv * BL + bl;
+        const int* depp = V.depb + prv * BL + bl;
+#pragma unroll 8
+        for (int j = threadIdx.x; j < L; j += blockDim.x) {
+          const int nold = offA[j + 1] - offA[j];
+          const int na = nAp[j], dpv = depp[j], w = V.win[bl + j];
+          na_s[j] = nold ? na : 0;
+          dep_s[j] = dpv;
+          win_s[j] = w;
+          offB[j] = nold - dpv + (w >= 0 ? 1 : 0);
+        }
+        __syncthreads();
+        scan_f(offB, L, tmp);
+        if (rank == 0) {
+          int* on = d.off + oidx(d, t % d.S, bb);
+          for (int j = threadIdx.x; j <= L; j += blockDim.x) on[j] = offB[j];
+          if (threadIdx.x == 0 && offB[L] != N) atomicOr(&d.err[bb], kErrConservation);
+        }
+      }
+      const std::size_t so = sidx(d, t % d.S, bb);
+      const std::size_t sp = t > 0 ? sidx(d, (t - 1) % d.S, bb) : 0;
+      const double* x1p = V.x1b + prv * BN + bn;
+      const int* wonp = V.wonb + prv * BN + bn;
+      double* x1c = V.x1b + cur * BN + bn;
+      int* wonc = V.wonb + cur * BN + bn;
+      int* nAc = V.nAb + cur * BL + bl;
+      int* qnc = V.qnb + cur * BL + bl;
+      double* tailc = V.tailb + cur * BL + bl;
+      if (V.wstamp) wt1 = gnow();
+      // Each thread owns slots gt0, gt0 + nthr, ...; they are processed kBatch
+      // at a time so the pull loads of several slots are in flight together.
+      for (int k0 = gt0; k0 < N; k0 += kBatch * nthr) {
+        int kk[kBatch], jj[kBatch], rr[kBatch], nn[kBatch], aa[kBatch];
+        double xx[kBatch], xl[kBatch], xn[kBatch];
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) {  // segment lookup (smem)
+          const int k = k0 + q * nthr;
+          kk[q] = k;
+          const int j = k < N ? find_link_f(offB, L, k) : 0;
+          jj[q] = j;
+          rr[q] = k - offB[j];
+          nn[q] = offB[j + 1] - offB[j];
+        }
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) {  // pull (all loads issued before use)
+          const int k = kk[q], j = jj[q], r = rr[q], n = nn[q];
+          xl[q] = 0.0;
+          xn[q] = 0.0;
+          if (k >= N) {
+            xx[q] = 0.0;
+            aa[q] = 0;
+            continue;
+          }
+          if (t == 0) {
+            xx[q] = d.pos[so + k];
+            aa[q] = d.aid[so + k];
+            if (r > 0) xl[q] = d.pos[so + k - 1];
+            if (r + 1 < n) xn[q] = d.pos[so + k + 1];
+          } else {
+            bool e0, e1 = false, e2 = false;
+            const int s0 = pull_f(j, r, offA, offB, na_s, dep_s, win_s, wonp, &e0);
+            int s1 = s0, s2 = s0;
+            if (!last && r > 0) s1 = pull_f(j, r - 1, offA, offB, na_s, dep_s, win_s, wonp, &e1);
+            if (!last && r + 1 < n) s2 = pull_f(j, r + 1, offA, offB, na_s, dep_s, win_s, wonp, &e2);
+            const double v0 = x1p[s0], v1 = x1p[s1], v2 = x1p[s2];
+            aa[q] = d.aid[sp + s0];
+            xx[q] = e0 ? 0.0 : v0;  // entrant: -M + M == 0.0 exactly
+            xl[q] = e1 ? 0.0 : v1;
+            xn[q] = e2 ? 0.0 : v2;
+          }
+        }
+        if (t > 0) {
+#pragma unroll
+          for (int q = 0; q < kBatch; ++q)  // checkpoint of layout t
+            if (kk[q] < N) {
+              d.pos[so + kk[q]] = xx[q];
+              d.aid[so + kk[q]] = aa[q];
+              d.lnk[so + kk[q]] = jj[q];
+            }
+        }
+        if (last) continue;
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) {
+          const int k = kk[q];
+          if (k >= N) continue;
+          const int j = jj[q], r = rr[q], n = nn[q];
+          const double x = xx[q];
+          const double jam = V.stage_params ? jam_s[j] : d.jam[bl + j];
+          const double dxf = V.stage_params ? dxf_s[j] : d.dxf[bl + j];
+          const double len = V.stage_params ? len_s[j] : d.len[j];
+          const double ctr = 0.5 * len, thr = len - kArrivalTol;
+          const CfPick me = cf_step(x, r == 0 ? d.M : xl[q] - x, jam, dxf, len);
+          x1c[k] = me.x1;
+          bool fo_n = false, fa_n = false;
+          if (r + 1 < n) {
+            const CfPick nx = cf_step(xn[q], x - xn[q], jam, dxf, len);
+            fo_n = nx.x1 >= ctr;
+            fa_n = nx.x1 >= thr;
+          }
+          const bool fo = me.x1 >= ctr, fa = me.x1 >= thr;
+          if (r == 0 && !fo) qnc[j] = 0;
+          if (fo && !fo_n) qnc[j] = r + 1;
+          if (r == 0 && !fa) nAc[j] = 0;
+          if (fa && !fa_n) nAc[j] = r + 1;
+          if (r == n - 1) tailc[j] = me.x1;
+          if (!fa) continue;
+          ++n_arr;
+          wonc[k] = 0;
+          if (soff_s[j + 1] > soff_s[j]) head_choice(V, bl, h1l, h1m, k, j, aa[q], soff_s, slz);
+        }
+      }
+    }
+    if (V.wstamp && active && !last) {
+      const unsigned long long wt2 = gnow();
+      const int na = __reduce_add_sync(0xffffffffu, n_arr);
+      if ((threadIdx.x & 31) == 0) {
+        const std::size_t w = (static_cast<std::size_t>(t) * gridDim.x + blockIdx.x) * (blockDim.x / 32) +
+                              (threadIdx.x >> 5);
+        V.wstamp[w * 4 + 0] = wst0;
+        V.wstamp[w * 4 + 1] = wt1;
+        V.wstamp[w * 4 + 2] = wt2;
+        V.wstamp[w * 4 + 3] = static_cast<unsigned long long>(na);
+      }
+    }
+    if (last) break;
+    fstamp(V, t, 1);
+    barrier();
+    fstamp(V, t, 2);
+    if (active) {
+      // ---------------- link phase ----------------
+      double* tailc = V.tailb + cur * BL + bl;
+      const int* qnc = V.qnb + cur * BL + bl;
+      int* wonc = V.wonb + cur * BN + bn;
+      int* depc = V.depb + cur * BL + bl;
+      int* depn = V.depb + prv * BL + bl;
+      const double* qhp = d.qh + hidx(d, t, bb);
+      const double* chp = d.cumh + hidx(d, t, bb);
+      double* qhn = d.qh + hidx(d, t + 1, bb);
+      double* chn = d.cumh + hidx(d, t + 1, bb);
+      for (int i = gt0; i < L; i += nthr) {
+        const int n_i = offB[i + 1] - offB[i];
+        const int cnt = V.ccnt[bl + i];
+        const int qc = n_i ? qnc[i] : 0;
+        const double tx = n_i ? tailc[i] : d.M;
+        const double qpv = qhp[i], cpv = chp[i];
+        const double a = static_cast<double>(qc) - qpv;  // inc = relu(q - qprev)
+        chn[i] = cpv + (a >= 0.0 ? a : 0.0);
+        qhn[i] = static_cast<double>(qc);
+        const double jam = V.stage_params ? jam_s[i] : d.jam[bl + i];
+        const bool vacant = tx > jam;  // vacancy_from_state (node_model.cpp:27-41)
+        V.ccnt[bl + i] = 0;
+        depn[i] = 0;
+        int w = -1;
+        if (vacant && cnt > 0) {
+          if (cnt > kClusterCandCap) {
+            atomicOr(&d.err[bb], kErrCandOverflow);
+          } else {
+            Cand c[kClusterCandCap];
+            for (int e = 0; e < cnt; ++e) c[e] = V.cands[(bl + i) * kClusterCandCap + e];
+            for (int x = 1; x < cnt; ++x) {  // ascending agent id (merge columns)
+              const Cand key = c[x];
+              int m = x - 1;
+              while (m >= 0 && c[m].aid > key.aid) {
+                c[m + 1] = c[m];
+                --m;
+              }
+              c[m + 1] = key;
+            }
+            double v[kClusterCandCap], g[kClusterCandCap], lz[kClusterCandCap], pi[kClusterCandCap];
+            for (int e = 0; e < cnt; ++e) {
+              v[e] = c[e].alpha;
+              g[e] = c[e].g;
+              if (v[e] == 0.0) atomicOr(&d.err[bb], kErrZeroAlpha);
+            }
+            const int best = two_softmax<kClusterCandCap>(cnt, v, g, d.kinv, lz, pi);
+            w = c[best].slot;
+            wonc[w] = 1;
+            atomicAdd(&depc[c[best].link], 1);
+          }
+        }
+        V.win[bl + i] = w;
+      }
+    }
+    fstamp(V, t, 3);
+    barrier();
+  }
+}
+
+int fused_smem_bytes(int L, bool stage_params) {
+  return (stage_params ? 3 * L * 8 : 0) + (2 * (L + 1) + 3 * L + 2 * (L + 1) + 32) * 4;
+}
+
+cudaError_t launch_forward_fused(const CView& V, bool cluster, cudaStream_t st) {
+  const int smem = fused_smem_bytes(V.d.L, V.stage_params != 0);
+  const void* fn = cluster ? reinterpret_cast<const void*>(k_forward_fused<true>)
+                           : reinterpret_cast<const void*>(k_forward_fused<false>);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  if (cluster) {
+    if (V.cs > 8) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(V.d.B * V.cs);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = V.cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_forward_fused<true>, V);
+  }
+  void* args[] = {const_cast<CView*>(&V)};
+  return cudaLaunchCooperativeKernel(fn, dim3(V.d.B * V.cs), dim3(kClusterThreads), args, smem, st);
+}
+
+int fused_max_grid(int L, bool stage_params) {
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int smem = fused_smem_bytes(L, stage_params);
+  const void* fn = reinterpret_cast<const void*>(k_forward_fused<false>);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kClusterThreads, smem);
+  return occ * sms;
+}
+
+int fused_max_cluster(int L, bool stage_params) {
+  const int smem = fused_smem_bytes(L, stage_params);
+  const void* fn = reinterpret_cast<const void*>(k_forward_fused<true>);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (int cs = 16; cs >= 1; cs >>= 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n > 0) return cs;
+  }
+  cudaGetLastError();
+  return 0;
+}
+
+}  // namespace dtg

@@ -23,9 +23,6 @@ void launch_derive(const DevView& d, double* jam, double* dxf, double* pref,
 void launch_gumbel_batch(std::uint64_t seed, std::uint64_t key, const std::uint64_t* rows,
                          const std::uint64_t* cols, int n, double* out, cudaStream_t st);
 
-struct PView;
-int persistent_smem_bytes(int L);
-int persistent_max_grid(int L, int* per_sm);
 
 constexpr int kFwdKernels = 4;
 constexpr int kBwdKernels = 8;

@@ -35,6 +35,22 @@ DTG_HD std::uint64_t rng_bits(std::uint64_t seed, std::uint64_t a,
   return h;
 }
 
+/// bits(a, b, c) split into its three chained stages, so a common prefix can be
+/// reused across many draws: bits(a, b, c) == rng_final(rng_prefix2(
+/// rng_prefix1(seed, a), b), c).
+DTG_HD std::uint64_t rng_prefix1(std::uint64_t seed, std::uint64_t a) {
+  return rng_mix(seed ^ rng_mix(a));
+}
+DTG_HD std::uint64_t rng_prefix2(std::uint64_t h1, std::uint64_t b) {
+  return rng_mix(h1 ^ rng_mix(b ^ 0x6a09e667f3bcc909ULL));
+}
+DTG_HD std::uint64_t rng_final(std::uint64_t h2, std::uint64_t c) {
+  return rng_mix(h2 ^ rng_mix(c ^ 0xbb67ae8584caa73bULL));
+}
+DTG_HD double rng_unit(std::uint64_t bits) {
+  return (static_cast<double>(bits >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+}
+
 /// Uniform strictly inside (0, 1).
 DTG_HD double rng_uniform(std::uint64_t seed, std::uint64_t a, std::uint64_t b,
                           std::uint64_t c) {

@@ -294,6 +294,9 @@ class Engine:
         """0 auto, 1 cluster per scenario, 2 persistent grid, 3 step graph."""
         self._check(self._lib.dtg_set_mode(self._h, mode))
 
+    def set_flag(self, flag: int, value: int):
+        self._check(self._lib.dtg_set_flag(self._h, flag, value))
+
     @property
     def last_mode(self) -> int:
         return int(self._lib.dtg_last_mode(self._h))
