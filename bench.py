@@ -392,73 +392,57 @@ def run_throughput(P, torch, sc, p, lk0, ps0, args, B=64):
 
 
 def run_gradient(P, torch, world, rank, args):
-    """C4 calibration iteration (calibrate(), optimization.cpp:122-219): the
-    8 noise draws sharded over the GPUs, each rank's draws in one batched
-    forward(checkpoint) + adjoint pass, MSE loss seeds on the host (the
-    reference's host loss tape, engine.cpp:369-385), NCCL all-gather of the
-    per-draw gradients + fixed-order sum, BoundedTransform chain rule + AdamW."""
+    """C4 calibration (calibrate(), optimization.cpp:122-219) through the
+    product API: every iteration runs the 8 noise draws (sharded over the GPUs)
+    as one batched forward(checkpoint) + reverse sweep per rank, the MSE loss,
+    its seeds and the draw-ordered gradient sum on the device, an NCCL
+    all-gather of the per-draw rows for N > 1, and the BoundedTransform chain
+    rule + AdamW on the host over the reduced O(L) row."""
     if args.no_gradient:
         return None
-    from paper_2603_25068_b200.dist import ShardedGradient, calibration_draws
+    from paper_2603_25068_b200.dist import calibrate_sharded
 
     T = int(CAL_MIN * 60 / DT)  # 60
     sc = build_scenario(P, horizon_steps=T)
     truth = sc.sample_parameters(NET_SEED)  # truth = sample_parameters(root)
-    start = sc.sample_parameters(0, mean_mode=True)  # calibration start = midpoints
     L = sc.n_links
     K = T // SPI
     obs_ids = np.array([j for j in range(L) if j % 5 != 0], dtype=np.int32)  # 80% coverage
     tr = P.simulate_forward(sc, truth, seed=SIM_SEED)
     obs_vals = tr.cum_per_step[SPI - 1::SPI][:K][:, obs_ids] * DELTA_N
-    sg = ShardedGradient(sc, CAL_DRAWS, world, rank, stream_ptr=torch.cuda.current_stream().cuda_stream)
-    lo = np.array([13.9, 0.18, 0.0, 0.01])
-    hi = np.array([22.2, 0.22, 5.0, 5.0])
-    raw = np.zeros((4, L))
-    m = np.zeros_like(raw)
-    v = np.zeros_like(raw)
-    scl = 1.0 / (K * len(obs_ids))
+    stream = torch.cuda.Stream()
 
-    def seeds_fn(snaps, cum_final):  # mse_loss_builder value + seeds per draw
-        d = snaps[:, :, obs_ids] * DELTA_N - obs_vals[None]
-        loss = (d * d).sum(axis=(1, 2)) * scl
-        seeds = np.zeros_like(snaps)
-        seeds[:, :, obs_ids] = ((0.0 + scl * d) + scl * d) * DELTA_N
-        return loss, seeds, None
+    def run(n):
+        cfg = P.OptimizeConfig(max_iterations=n, patience=10 ** 6, noise_draws=CAL_DRAWS)
+        return calibrate_sharded(sc, obs_ids, obs_vals, SIM_SEED, cfg=cfg, world=world, rank=rank,
+                                 stream=stream)
 
-    def iteration(it):
-        s = np.where(raw >= 0, 1.0 / (1.0 + np.exp(-raw)), np.exp(raw) / (1.0 + np.exp(raw)))
-        vals = lo[:, None] + (hi - lo)[:, None] * s
-        params = P.LinkParams(vals[0], vals[1], vals[2], vals[3], start.cost)
-        loss, gsum, _ = sg(params, SIM_SEED, calibration_draws(it, CAL_DRAWS), seeds_fn)
-        rg = gsum[:4] / CAL_DRAWS * ((hi - lo)[:, None] * s * (1.0 - s))
-        t_ = it + 1  # AdamW, optimization.cpp:10-25
-        m[:] = 0.9 * m + (1.0 - 0.9) * rg
-        v[:] = 0.999 * v + (1.0 - 0.999) * rg * rg
-        raw[:] -= 0.1 * ((m / (1 - 0.9 ** t_)) / (np.sqrt(v / (1 - 0.999 ** t_)) + 1e-8) + 1e-5 * raw)
-        return loss
-
-    for it in range(2):
-        iteration(it)
-    n_it = max(3, args.steps // 4)
+    run(2)  # warm-up: context, graphs, loss buffers
+    n_it = max(5, args.steps)
     barrier(world)
     torch.cuda.synchronize()
     t = time.perf_counter()
-    losses = [iteration(it) for it in range(2, 2 + n_it)]
+    res = run(n_it)
     torch.cuda.synchronize()
     s_iter = max_over_ranks((time.perf_counter() - t) / n_it, world)
     # device time of the two passes (CUDA events on the engine's stream)
-    eng = sg.engine
-    st = torch.cuda.current_stream()
-    seeds = torch.zeros((len(sg.mine), K, L), dtype=torch.float64, device="cuda")
-    gbuf = torch.empty((len(sg.mine), 5, L), dtype=torch.float64, device="cuda")
+    local = CAL_DRAWS // world
+    eng = P.Engine(sc, n_scenarios=local, max_steps=T)
+    eng.set_stream(stream.cuda_stream)
+    lk, ps = sc.seed_agents()
+    eng.set_params(truth)
+    eng.set_state(lk, ps)
+    for b in range(local):
+        eng.set_noise(SIM_SEED, rank * local + b + 1, b)
+    eng.set_loss_mse(obs_ids, obs_vals)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     fwd_ms, adj_ms = [], []
     for _ in range(3):
-        ev[0].record(st)
+        ev[0].record(stream)
         eng.forward(T, SPI, checkpoint=True)
-        ev[1].record(st)
-        eng.backward_device(seeds.data_ptr(), 0, 0, gbuf.data_ptr())
-        ev[2].record(st)
+        ev[1].record(stream)
+        eng.gradient_device_loss()
+        ev[2].record(stream)
         torch.cuda.synchronize()
         fwd_ms.append(ev[0].elapsed_time(ev[1]))
         adj_ms.append(ev[1].elapsed_time(ev[2]))
@@ -466,14 +450,16 @@ def run_gradient(P, torch, world, rank, args):
     phases_f, _ = eng.profile_persistent(T, SPI)
     eng.forward(T, SPI, checkpoint=True)
     phases_b, grid_b = eng.profile_backward()
-    return {"s_per_iter": s_iter, "draws": CAL_DRAWS, "draws_per_gpu": len(sg.mine), "steps": T,
-            "iterations_timed": n_it, "params": 4 * L, "loss_last": losses[-1],
+    return {"s_per_iter": s_iter, "draws": CAL_DRAWS, "draws_per_gpu": local, "steps": T,
+            "iterations_timed": n_it, "params": 4 * L, "loss_first": float(res.loss_curve[0]),
+            "loss_last": float(res.loss_curve[-1]),
             "projected_200_iter_s": 200 * s_iter,
             "paper_calibration_s": 455.3,
             "fwd_ckpt_ms_per_pass": statistics.median(fwd_ms), "adj_ms_per_pass": statistics.median(adj_ms),
             "fwd_phase_us_per_step": {k: round(x, 2) for k, x in phases_f.items()},
             "adj_phase_us_per_step": {k: round(x, 2) for k, x in phases_b.items()},
-            "timing": "wall clock per full iteration (host loss + H2D/D2H + NCCL gather + AdamW included)"}
+            "timing": "wall clock per calibrate() iteration through the public API (device loss/seeds/draw sum, "
+                      "NCCL row gather for N>1, host transform + AdamW, 1 sync per iteration)"}
 
 
 # ---- reference arm -----------------------------------------------------------------------

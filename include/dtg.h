@@ -175,6 +175,33 @@ int dtg_backward_device(dtg_ctx* ctx, const double* d_snap_seeds,
                         const double* d_cum_seeds, const double* d_x_seeds,
                         double* d_grads);
 
+/* ---- Device losses ---------------------------------
+ * The two losses of the reference's optimisation loops, evaluated on the
+ * device from the count history of the last checkpointed forward, so an
+ * optimisation iteration needs no host round trip of snapshots and seeds:
+ *   MSE     mse_loss_builder (optimization.cpp:83-101): obs_values[k_obs][n_obs]
+ *           in vehicles for link_ids[n_obs] (duplicates allowed);
+ *   control optimize_control's (cum_final[target] * delta_n - desired)^2
+ *           (optimization.cpp:234-240). */
+int dtg_set_loss_mse(dtg_ctx* ctx, int k_obs, int n_obs, const int* link_ids,
+                     const double* obs_values);
+int dtg_set_loss_control(dtg_ctx* ctx, int target_link, double desired_count);
+/* After dtg_forward(checkpoint=1): loss + seeds on the device, the reverse
+ * sweep, and one row per scenario written to d_rows [B][5L+2] (device
+ * pointer; NULL = the context's own buffer):
+ *   [grads u | kappa | beta | alpha | cost (5L), loss, extra]
+ * extra = cum_final[target] * delta_n for the control loss, else 0.
+ * Stream-ordered, no host synchronisation (an NCCL all-gather of the rows
+ * can follow on the same stream). */
+int dtg_gradient_device_loss(dtg_ctx* ctx, double* d_rows);
+/* Draw-ordered reduction of n_draws rows (device pointer d_rows, or NULL =
+ * the context's own B rows) into out[5L+2] (host), synchronising:
+ *   mode 0 (calibrate, optimization.cpp:176-193): g_0 + g_1 + ...
+ *   mode 1 (control,   optimization.cpp:262-264): 0 + g_0/D + g_1/D + ...
+ *   loss and extra: 0 + x_0/D + x_1/D + ... in both modes. */
+int dtg_reduce_draw_rows(dtg_ctx* ctx, int n_draws, const double* d_rows,
+                         int mode, double* out);
+
 /* Measurement hook: run n_steps of the forward (backward != 0: the reverse
  * sweep of the preceding checkpointed forward) without graphs, bracketing
  * every kernel with CUDA events on the context stream.  ms_out[w] receives
@@ -278,6 +305,72 @@ int dtg_simulate_gradient_mse(dtg_scenario* sc, const double* u,
                               const int* obs_ids, int k_obs,
                               const double* obs_values, double* loss,
                               double* grads);
+
+/* AdamWConfig + OptimizeConfig (optimization.hpp:18-24, 72-82). */
+typedef struct {
+  double lr;            /* 0.1   */
+  double weight_decay;  /* 1e-5  */
+  double beta1;         /* 0.9   */
+  double beta2;         /* 0.999 */
+  double eps;           /* 1e-8  */
+  int patience;         /* 20    */
+  int max_iterations;   /* 200   */
+  int resample_noise;   /* 1     */
+  int noise_draws;      /* 1     */
+} dtg_optimize_config;
+
+/* ParamRanges (engine.hpp / network.cpp sample_parameters bounds). */
+typedef struct {
+  double u_lo, u_hi, kappa_lo, kappa_hi, beta_lo, beta_hi, alpha_lo, alpha_hi;
+} dtg_param_ranges;
+
+/* Multi-GPU draw exchange.  With world > 1 this rank runs
+ * draws [rank*D/world, (rank+1)*D/world) of each iteration, writes their
+ * rows [D/world][5L+2] (see dtg_gradient_device_loss) to d_local, calls
+ * gather(user) — which must all-gather d_local of every rank, rank-major,
+ * into d_full [D][5L+2], ordered on `stream` (e.g. NCCL all_gather) — and
+ * reduces all D rows in draw order, so every rank gets the single-GPU result
+ * bit for bit.  The context runs on `stream` (cudaStream_t, may be NULL). */
+typedef int (*dtg_gather_fn)(void* user);
+typedef struct {
+  int world;
+  int rank;
+  double* d_local;
+  double* d_full;
+  void* stream;
+  dtg_gather_fn gather;
+  void* user;
+} dtg_draw_exchange;
+
+/* calibrate (optimization.cpp:122-219) with the device iteration: per
+ * iteration one batched forward + reverse sweep over the noise draws, MSE
+ * loss/seeds and the draw sum on the device, transform + AdamW on the host.
+ * init_* may be NULL (start from raw 0 = range midpoints, cost 1);
+ * init_cost may be NULL alone.  loss_curve has room for max_iterations.
+ * Returns DTG_ERR_DIVERGENCE on a non-finite loss. */
+int dtg_calibrate(dtg_scenario* sc, int n_obs, const int* obs_ids, int k_obs,
+                  const double* obs_values, const dtg_param_ranges* bounds,
+                  const dtg_optimize_config* cfg, uint64_t root_seed,
+                  const double* init_u, const double* init_kappa,
+                  const double* init_beta, const double* init_alpha,
+                  const double* init_cost, double* best_u, double* best_kappa,
+                  double* best_beta, double* best_alpha, double* best_cost,
+                  double* best_loss, int* best_iteration, int* iterations,
+                  double* loss_curve, double* wall_seconds,
+                  const dtg_draw_exchange* exchange /* NULL: one GPU */);
+
+/* optimize_control (optimization.cpp:221-295): fit per-link route costs
+ * (LowerBoundTransform with cost_floor) so cum_final[target] * delta_n
+ * approaches desired.  cost_out[L]; loss_curve has room for max_iterations. */
+int dtg_optimize_control(dtg_scenario* sc, const double* u, const double* kappa,
+                         const double* beta, const double* alpha,
+                         const double* cost, int target_link, double desired,
+                         const dtg_optimize_config* cfg, double cost_floor,
+                         uint64_t root_seed, double* cost_out, double* achieved,
+                         double* gap_fraction, double* best_loss,
+                         int* iterations, double* loss_curve,
+                         int* zero_gradient_stall, double* wall_seconds,
+                         const dtg_draw_exchange* exchange /* NULL: one GPU */);
 
 /* Device context a scenario uses (for dtg_set_stream / dtg_last_launches);
  * NULL before the first simulate call. */

@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -182,6 +183,123 @@ LossBuilder control_loss_builder(int target_link, double desired_count, int delt
 LossBuilder linear_quadratic_loss(std::vector<double> ws, std::vector<double> qs,
                                   std::vector<double> wc, std::vector<double> qc,
                                   std::vector<double> wx);
+// ---- optimisation loops (optimization.hpp:18-128, optimization.cpp:10-295) ----------
+/// Raised when a loop sees a non-finite loss (DivergenceError, config.hpp).
+struct DivergenceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct AdamWConfig {
+  double lr = 0.1;
+  double weight_decay = 1e-5;
+  double beta1 = 0.9;
+  double beta2 = 0.999;
+  double eps = 1e-8;
+};
+
+/// AdamW with decoupled weight decay on the raw parameters (optimization.cpp:10-25).
+class AdamW {
+ public:
+  AdamW(int n, const AdamWConfig& cfg) : cfg_(cfg), m_(n, 0.0), v_(n, 0.0) {}
+  void step(std::vector<double>& params, const std::vector<double>& grads);
+  int iterations() const { return t_; }
+
+ private:
+  AdamWConfig cfg_;
+  std::vector<double> m_, v_;
+  int t_ = 0;
+};
+
+/// lo + (hi - lo) * sigmoid(raw) (optimization.cpp:27-46).
+class BoundedTransform {
+ public:
+  BoundedTransform(double lo, double hi) : lo_(lo), hi_(hi) {}
+  double value(double raw) const;
+  double dvalue(double raw) const;
+  double raw_of(double value) const;
+
+ private:
+  double lo_, hi_;
+};
+
+/// floor + softplus(raw) (optimization.cpp:48-59).
+class LowerBoundTransform {
+ public:
+  explicit LowerBoundTransform(double floor) : floor_(floor) {}
+  double value(double raw) const;
+  double dvalue(double raw) const;
+  double raw_of(double value) const;
+
+ private:
+  double floor_;
+};
+
+struct OptimizeConfig {
+  AdamWConfig adam;
+  int patience = 20;
+  int max_iterations = 200;
+  bool resample_noise = true;
+  int noise_draws = 1;
+  GradMode grad_mode = GradMode::Checkpointed;
+};
+
+struct CalibrationResult {
+  LinkParams best_params;
+  double best_loss = 0.0;
+  int best_iteration = -1;
+  int iterations = 0;
+  std::vector<double> loss_curve;
+  double wall_seconds = 0.0;
+};
+
+/// Multi-GPU draw exchange for the optimisation loops: this
+/// rank runs draws [rank * D/world, (rank+1) * D/world) of every iteration,
+/// writes their rows [D/world][5L+2] to d_local, `gather` all-gathers them
+/// (rank-major, i.e. draw order) into d_full [D][5L+2] ordered on `stream`,
+/// and every rank reduces all D rows in draw order — bit-identical for any
+/// world size.
+struct DrawExchange {
+  int world = 1;
+  int rank = 0;
+  double* d_local = nullptr;
+  double* d_full = nullptr;
+  void* stream = nullptr;  // cudaStream_t of the context and the gather
+  std::function<void()> gather;
+};
+
+/// Gradient fit of (u, kappa, beta, alpha) to observed counts; costs fixed
+/// (optimization.cpp:122-219).  All draws of an iteration run as one batched
+/// device forward + reverse sweep with the MSE loss, its seeds and the
+/// draw-ordered gradient sum on the device; the host keeps the O(L) transform
+/// and AdamW arithmetic (glibc exp/pow, so parameters match the reference bit
+/// for bit).
+CalibrationResult calibrate(const Scenario& s, const CountSeries& obs, const ParamRanges& bounds,
+                            const OptimizeConfig& cfg, const RngStream& rng,
+                            const LinkParams* init = nullptr, const DrawExchange* ex = nullptr);
+
+struct ControlConfig {
+  OptimizeConfig opt;
+  double cost_floor = 0.05;
+};
+
+struct ControlResult {
+  std::vector<double> cost;
+  double desired = 0.0;
+  double achieved = 0.0;
+  double gap_fraction = 0.0;
+  double best_loss = 0.0;
+  int iterations = 0;
+  std::vector<double> loss_curve;
+  bool zero_gradient_stall = false;
+  double wall_seconds = 0.0;
+};
+
+/// Route-cost control toward a desired count on one link
+/// (optimization.cpp:221-295), same device iteration as calibrate.
+ControlResult optimize_control(const Scenario& s, const LinkParams& calibrated, int target_link,
+                               double desired_count, const ControlConfig& cfg,
+                               const RngStream& rng, const DrawExchange* ex = nullptr);
+
 /// series_from_levels (observation.cpp:27-44).
 CountSeries series_from_levels(const std::vector<std::vector<double>>& cum_per_step,
                                const std::vector<int>& link_ids, int interval_s,

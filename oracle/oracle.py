@@ -114,6 +114,10 @@ class RefLib:
         L.ref_gradient.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, u64, u64, C.c_int,
                                    vp, vp, vp, vp, vp, vp, _dp, vp, vp, vp, vp, vp, vp]
         L.ref_gradient_mse.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, u64, u64, C.c_int, _ip, C.c_int, _dp, vp, _dp]
+        L.ref_calibrate.argtypes = [vp, C.c_int, _ip, C.c_int, _dp, _dp, _dp, _ip, u64, vp, vp, vp, vp, vp,
+                                    _dp, _dp, _ip, _ip, _dp]
+        L.ref_optimize_control.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_double, _dp, _ip,
+                                           C.c_double, u64, _dp, _dp, _ip, _ip, _dp]
 
     def err(self) -> str:
         return self.lib.ref_last_error().decode()
@@ -249,6 +253,57 @@ class RefScenario:
                                                      obs_ids, obs_vals.shape[0], obs_vals.ravel(),
                                                      _ptr(loss), grads))
         return float(loss[0]), grads.reshape(5, Ln)
+
+
+    # ---- optimisation loops (src/optimization.cpp:122-295) -----------------
+    @staticmethod
+    def _opt(cfg: dict):
+        d = dict(lr=0.1, weight_decay=1e-5, beta1=0.9, beta2=0.999, eps=1e-8, patience=20,
+                 max_iterations=200, resample_noise=True, noise_draws=1)
+        d.update(cfg or {})
+        opt = np.array([d["lr"], d["weight_decay"], d["beta1"], d["beta2"], d["eps"]])
+        iopt = np.array([d["patience"], d["max_iterations"], int(d["resample_noise"]), d["noise_draws"]], np.int32)
+        return d, opt, iopt
+
+    def calibrate(self, obs_ids, obs_vals, seed: int, bounds=None, cfg: dict = None, init: "Params" = None):
+        """The reference's calibrate(); returns the CalibrationResult fields.
+        bounds = (u_lo, u_hi, kappa_lo, kappa_hi, beta_lo, beta_hi, alpha_lo, alpha_hi)."""
+        Ln = self.n_links
+        d, opt, iopt = self._opt(cfg)
+        b = np.ascontiguousarray(bounds if bounds is not None else
+                                 (13.9, 22.2, 0.18, 0.22, 0.0, 5.0, 0.01, 5.0), np.float64)
+        ids = np.ascontiguousarray(obs_ids, np.int32)
+        vals = np.ascontiguousarray(obs_vals, np.float64).reshape(-1, len(ids))
+        best = np.zeros(5 * Ln)
+        bl = np.zeros(1)
+        bi, its = np.zeros(1, np.int32), np.zeros(1, np.int32)
+        curve = np.zeros(max(d["max_iterations"], 1))
+        ia = init.arrays() if init is not None else [None] * 5
+        rc = self.lib.lib.ref_calibrate(self.h, len(ids), ids, vals.shape[0], vals.ravel(), b, opt, iopt, seed,
+                                        *(_ptr(a) for a in ia), best, bl, bi, its, curve)
+        if rc == 3:
+            raise FloatingPointError(self.lib.err())
+        self.lib.check(rc)
+        n = int(its[0])
+        return dict(best=best.reshape(5, Ln), best_loss=float(bl[0]), best_iteration=int(bi[0]),
+                    iterations=n, loss_curve=curve[:n].copy())
+
+    def optimize_control(self, p: "Params", target: int, desired: float, seed: int, cfg: dict = None,
+                         cost_floor: float = 0.05):
+        Ln = self.n_links
+        d, opt, iopt = self._opt(cfg)
+        cost = np.zeros(Ln)
+        out3 = np.zeros(3)
+        its, stall = np.zeros(1, np.int32), np.zeros(1, np.int32)
+        curve = np.zeros(max(d["max_iterations"], 1))
+        rc = self.lib.lib.ref_optimize_control(self.h, *p.arrays(), target, desired, opt, iopt, cost_floor, seed,
+                                               cost, out3, its, stall, curve)
+        if rc == 3:
+            raise FloatingPointError(self.lib.err())
+        self.lib.check(rc)
+        n = int(its[0])
+        return dict(cost=cost, achieved=float(out3[0]), gap_fraction=float(out3[1]), best_loss=float(out3[2]),
+                    iterations=n, zero_gradient_stall=bool(stall[0]), loss_curve=curve[:n].copy())
 
 
 # ---------------------------------------------------------------------------

@@ -10,6 +10,7 @@
 //   simulate_gradient  include/dtsim/engine.hpp:105-107 (src/engine.cpp:303-429)
 // so the outputs ARE the reference's outputs.  Used by tests/ (golden
 // generation, oracle pinning) and by bench.py's `--impl reference` arm.
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -378,6 +379,113 @@ int ref_gradient_mse(void* h, const double* u, const double* k,
     std::memcpy(grads + 3 * L, g.grads.alpha.data(), L * 8);
     std::memcpy(grads + 4 * L, g.grads.cost.data(), L * 8);
   });
+}
+
+// ---- optimisation loops (src/optimization.cpp:122-295) ---------------------
+// opt = {lr, weight_decay, beta1, beta2, eps}; iopt = {patience,
+// max_iterations, resample_noise, noise_draws}; bounds = ParamRanges fields in
+// declaration order.  Returns 3 on DivergenceError.
+static OptimizeConfig make_opt(const double* opt, const int* iopt) {
+  OptimizeConfig o;
+  o.adam.lr = opt[0];
+  o.adam.weight_decay = opt[1];
+  o.adam.beta1 = opt[2];
+  o.adam.beta2 = opt[3];
+  o.adam.eps = opt[4];
+  o.patience = iopt[0];
+  o.max_iterations = iopt[1];
+  o.resample_noise = iopt[2] != 0;
+  o.noise_draws = iopt[3];
+  o.grad_mode = GradMode::Checkpointed;
+  return o;
+}
+
+int ref_calibrate(void* h, int n_obs, const int* obs_ids, int K,
+                  const double* obs_vals, const double* bounds,
+                  const double* opt, const int* iopt, uint64_t seed,
+                  const double* iu, const double* ik, const double* ib,
+                  const double* ia, const double* ic, double* best /* 5L */,
+                  double* best_loss, int* best_it, int* iterations,
+                  double* curve) {
+  try {
+    const auto& s = static_cast<RefScn*>(h)->s;
+    const int L = s.net.n_links();
+    CountSeries obs;
+    obs.link_ids.assign(obs_ids, obs_ids + n_obs);
+    obs.interval_s = s.obs_interval_s;
+    for (int kk = 0; kk < K; ++kk)
+      obs.values.emplace_back(obs_vals + kk * n_obs, obs_vals + (kk + 1) * n_obs);
+    ParamRanges r;
+    r.u_lo = bounds[0];
+    r.u_hi = bounds[1];
+    r.kappa_lo = bounds[2];
+    r.kappa_hi = bounds[3];
+    r.beta_lo = bounds[4];
+    r.beta_hi = bounds[5];
+    r.alpha_lo = bounds[6];
+    r.alpha_hi = bounds[7];
+    LinkParams init;
+    const bool have = iu != nullptr;
+    if (have) {
+      init.u.assign(iu, iu + L);
+      init.kappa.assign(ik, ik + L);
+      init.beta.assign(ib, ib + L);
+      init.alpha.assign(ia, ia + L);
+      if (ic) init.cost.assign(ic, ic + L);
+    }
+    const CalibrationResult res = calibrate(s, obs, r, make_opt(opt, iopt),
+                                            RngStream(seed), have ? &init : nullptr);
+    const auto& bp = res.best_params;
+    if (!bp.u.empty()) {
+      std::memcpy(best + 0 * L, bp.u.data(), L * 8);
+      std::memcpy(best + 1 * L, bp.kappa.data(), L * 8);
+      std::memcpy(best + 2 * L, bp.beta.data(), L * 8);
+      std::memcpy(best + 3 * L, bp.alpha.data(), L * 8);
+      std::memcpy(best + 4 * L, bp.cost.data(), L * 8);
+    }
+    *best_loss = res.best_loss;
+    *best_it = res.best_iteration;
+    *iterations = res.iterations;
+    std::copy(res.loss_curve.begin(), res.loss_curve.end(), curve);
+    return 0;
+  } catch (const DivergenceError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+int ref_optimize_control(void* h, const double* u, const double* k,
+                         const double* b, const double* a, const double* c,
+                         int target, double desired, const double* opt,
+                         const int* iopt, double cost_floor, uint64_t seed,
+                         double* cost_out, double* out3 /* achieved, gap, best_loss */,
+                         int* iterations, int* stall, double* curve) {
+  try {
+    const auto& s = static_cast<RefScn*>(h)->s;
+    const int L = s.net.n_links();
+    ControlConfig cc;
+    cc.opt = make_opt(opt, iopt);
+    cc.cost_floor = cost_floor;
+    const ControlResult res = optimize_control(
+        s, make_params(L, u, k, b, a, c), target, desired, cc, RngStream(seed));
+    if (!res.cost.empty()) std::memcpy(cost_out, res.cost.data(), L * 8);
+    out3[0] = res.achieved;
+    out3[1] = res.gap_fraction;
+    out3[2] = res.best_loss;
+    *iterations = res.iterations;
+    *stall = res.zero_gradient_stall ? 1 : 0;
+    std::copy(res.loss_curve.begin(), res.loss_curve.end(), curve);
+    return 0;
+  } catch (const DivergenceError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
 }
 
 }  // extern "C"

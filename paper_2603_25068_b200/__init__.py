@@ -7,16 +7,22 @@ midpoint counting) and its checkpointed reverse-mode adjoint run as
 hand-written sm_100a kernels in ``libdtg.so``; the host API mirrors the
 reference's ``simulate_forward`` / ``simulate_gradient``.
 """
-from ._lib import ConfigError, DtgError, UnsupportedError, load  # noqa: F401
+from ._lib import ConfigError, DivergenceError, DtgError, UnsupportedError, load  # noqa: F401
 from .engine import (  # noqa: F401
     PHYSICAL,
     VIRTUAL_INFLOW,
     VIRTUAL_OUTFLOW,
+    CalibrationResult,
+    ControlResult,
     Engine,
     GradResult,
     LinkParams,
+    OptimizeConfig,
+    ParamRanges,
     Scenario,
     Trajectory,
+    calibrate,
+    optimize_control,
     simulate_forward,
     simulate_gradient,
     simulate_gradient_mse,

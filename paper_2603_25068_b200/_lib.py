@@ -34,10 +34,15 @@ class ConfigError(DtgError):
     pass
 
 
+class DivergenceError(DtgError):
+    """Non-finite loss in an optimisation loop (DivergenceError, config.hpp)."""
+
+
 def raise_for(code: int, msg: str):
     if code == DTG_OK:
         return
-    cls = {DTG_ERR_UNSUPPORTED: UnsupportedError, DTG_ERR_CONFIG: ConfigError}.get(code, DtgError)
+    cls = {DTG_ERR_UNSUPPORTED: UnsupportedError, DTG_ERR_CONFIG: ConfigError,
+           DTG_ERR_DIVERGENCE: DivergenceError}.get(code, DtgError)
     raise cls(code, msg)
 
 
@@ -48,6 +53,26 @@ class SimConfig(C.Structure):
 
 class NetDesc(C.Structure):
     _fields_ = [("n_links", C.c_int), ("succ_off", C.c_void_p), ("succ", C.c_void_p), ("length", C.c_void_p)]
+
+
+class OptimizeConfig(C.Structure):
+    """AdamWConfig + OptimizeConfig (optimization.hpp:18-24, 72-82)."""
+    _fields_ = [("lr", C.c_double), ("weight_decay", C.c_double), ("beta1", C.c_double),
+                ("beta2", C.c_double), ("eps", C.c_double), ("patience", C.c_int),
+                ("max_iterations", C.c_int), ("resample_noise", C.c_int), ("noise_draws", C.c_int)]
+
+
+class ParamRangesC(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("u_lo", "u_hi", "kappa_lo", "kappa_hi", "beta_lo",
+                                          "beta_hi", "alpha_lo", "alpha_hi")]
+
+
+GatherFn = C.CFUNCTYPE(C.c_int, C.c_void_p)
+
+
+class DrawExchange(C.Structure):
+    _fields_ = [("world", C.c_int), ("rank", C.c_int), ("d_local", C.c_void_p), ("d_full", C.c_void_p),
+                ("stream", C.c_void_p), ("gather", GatherFn), ("user", C.c_void_p)]
 
 
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
@@ -82,6 +107,10 @@ SIGNATURES = [
     ("dtg_n_snapshots", i32, [vp]),
     ("dtg_backward", i32, [vp, vp, vp, vp, _dp]),
     ("dtg_backward_device", i32, [vp, vp, vp, vp, vp]),
+    ("dtg_set_loss_mse", i32, [vp, i32, i32, _ip, _dp]),
+    ("dtg_set_loss_control", i32, [vp, i32, C.c_double]),
+    ("dtg_gradient_device_loss", i32, [vp, vp]),
+    ("dtg_reduce_draw_rows", i32, [vp, i32, vp, i32, _dp]),
     ("dtg_device_cum", vp, [vp]),
     ("dtg_profile_kernels", i32, [vp, i32, i32, i32, _dp, C.POINTER(C.c_int64)]),
     ("dtg_kernel_name", C.c_char_p, [i32, i32]),
@@ -106,6 +135,10 @@ SIGNATURES = [
                                     vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     ("dtg_simulate_gradient_mse", i32, [vp, _dp, _dp, _dp, _dp, _dp, u64, i32, _u64p,
                                         i32, _ip, i32, _dp, vp, vp]),
+    ("dtg_calibrate", i32, [vp, i32, _ip, i32, _dp, vp, vp, u64, vp, vp, vp, vp, vp,
+                            _dp, _dp, _dp, _dp, _dp, vp, vp, vp, _dp, vp, vp]),
+    ("dtg_optimize_control", i32, [vp, _dp, _dp, _dp, _dp, _dp, i32, C.c_double, vp,
+                                   C.c_double, u64, _dp, vp, vp, vp, vp, _dp, vp, vp, vp]),
     ("dtg_scenario_ctx", vp, [vp]),
     ("dtg_mse_loss", i32, [i32, i32, _dp, i32, _ip, i32, _dp, i32, _dp, _dp]),
     ("dtg_debug_gumbel", i32, [u64, u64, i32, _u64p, _u64p, _dp]),

@@ -16,6 +16,7 @@
 #include "dtg_kernels.h"
 #include "dtg_cluster.h"
 #include "dtg_backward.h"
+#include "dtg_loss.h"
 
 namespace {
 
@@ -130,6 +131,12 @@ struct dtg_ctx {
   DevBuf<dtg::Cand> cands;
   bool want_stamps = false;
   DevBuf<unsigned long long> stamps;
+  // device losses (dtg_loss.h)
+  int loss_kind = 0, loss_kobs = 0, loss_nobs = 0, loss_target = -1;
+  double loss_desired = 0.0;
+  DevBuf<int> loss_ids, loss_first, loss_next;
+  DevBuf<double> loss_obs, loss_val, loss_extra, rows, red;
+  double* h_red = nullptr;
   // graphs
   cudaGraphExec_t fwd_exec = nullptr, bwd_exec = nullptr;
   long long fwd_key = -1, bwd_key = -1;
@@ -209,6 +216,7 @@ struct dtg_ctx {
   ~dtg_ctx() {
     drop_graphs();
     if (h_stage) cudaFreeHost(h_stage);
+    if (h_red) cudaFreeHost(h_red);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
@@ -545,7 +553,7 @@ int dtg_set_mode(dtg_ctx* c, int mode) {
 int dtg_last_mode(const dtg_ctx* c) { return c->last_mode * 100 + c->last_cs; }
 
 static void run_backward(dtg_ctx* c, const double* snap, const double* cum, const double* xs,
-                         cudaMemcpyKind kind);
+                         cudaMemcpyKind kind, bool seeds_ready = false);
 
 int dtg_profile_backward(dtg_ctx* c, double* phase_us, int* grid_out) {
   return guarded(c, [&] {
@@ -606,8 +614,21 @@ int dtg_set_params(dtg_ctx* c, int scenario, const double* u, const double* kapp
     if (scenario >= c->B) throw std::invalid_argument("scenario index out of range");
     const double* src[5] = {u, kappa, beta, alpha, cost};
     const std::size_t L = c->L, BL = static_cast<std::size_t>(c->B) * L;
-    for (int b = 0; b < c->B; ++b) {
-      if (scenario >= 0 && b != scenario) continue;
+    if (scenario < 0) {
+      // one upload, then doubling device copies to the other scenarios
+      for (int q = 0; q < 5; ++q) {
+        double* base = c->params.p + q * BL;
+        CK(cudaMemcpyAsync(base, src[q], L * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        for (std::size_t have = 1; have < static_cast<std::size_t>(c->B); have *= 2) {
+          const std::size_t n = std::min<std::size_t>(have, c->B - have);
+          CK(cudaMemcpyAsync(base + have * L, base, n * L * sizeof(double),
+                             cudaMemcpyDeviceToDevice, c->stream));
+        }
+      }
+      for (int b = 0; b < c->B; ++b) c->have_params[b] = 1;
+    }
+    for (int b = 0; b < c->B && scenario >= 0; ++b) {
+      if (b != scenario) continue;
       for (int q = 0; q < 5; ++q)
         CK(cudaMemcpyAsync(c->params.p + q * BL + b * L, src[q], L * sizeof(double),
                            cudaMemcpyHostToDevice, c->stream));
@@ -941,7 +962,7 @@ static void run_backward_persistent(dtg_ctx* c, cudaStream_t st) {
 }
 
 static void run_backward(dtg_ctx* c, const double* snap, const double* cum, const double* xs,
-                         cudaMemcpyKind kind) {
+                         cudaMemcpyKind kind, bool seeds_ready) {
   if (c->last_T < 0 || !c->last_ckpt)
     throw std::runtime_error("dtg_backward needs a preceding dtg_forward with checkpoint=1");
   const int T = c->last_T, K = c->last_K, spi = c->last_spi;
@@ -972,9 +993,11 @@ static void run_backward(dtg_ctx* c, const double* snap, const double* cum, cons
     else
       CK(cudaMemsetAsync(dst, 0, n * 8, st));
   };
-  if (K) up(c->snap_seed.p, snap, B * K * L);
-  up(c->cum_seed.p, cum, B * L);
-  up(c->x_seed.p, xs, B * N);
+  if (!seeds_ready) {
+    if (K) up(c->snap_seed.p, snap, B * K * L);
+    up(c->cum_seed.p, cum, B * L);
+    up(c->x_seed.p, xs, B * N);
+  }
   if (c->bwd_persistent && c->bgrid_max > 0 && c->mode != 3 && T > 0) {
     run_backward_persistent(c, st);
     return;
@@ -1032,6 +1055,130 @@ int dtg_backward_device(dtg_ctx* c, const double* snap, const double* cum, const
     run_backward(c, snap, cum, xs, cudaMemcpyDeviceToDevice);
     const std::size_t n = static_cast<std::size_t>(c->B) * 5 * c->L;
     CK(cudaMemcpyAsync(d_grads, c->grads.p, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  });
+}
+
+// ---- device losses and the draw reduction -------------------
+
+int dtg_set_loss_mse(dtg_ctx* c, int k_obs, int n_obs, const int* link_ids,
+                     const double* values) {
+  return guarded(c, [&] {
+    if (k_obs < 0 || n_obs < 1 || !link_ids || (k_obs > 0 && !values))
+      throw std::invalid_argument("loss: no observed links");
+    std::vector<int> first(n_obs, 1), next(n_obs, -1);
+    for (int q = 0; q < n_obs; ++q) {
+      if (link_ids[q] < 0 || link_ids[q] >= c->L)
+        throw std::invalid_argument("loss: observed link missing from simulation");
+      for (int r = q + 1; r < n_obs; ++r)
+        if (link_ids[r] == link_ids[q]) {
+          next[q] = r;
+          first[r] = 0;
+          break;
+        }
+    }
+    c->loss_ids.ensure(n_obs);
+    c->loss_first.ensure(n_obs);
+    c->loss_next.ensure(n_obs);
+    c->loss_obs.ensure(std::max<std::size_t>(1, static_cast<std::size_t>(k_obs) * n_obs));
+    CK(cudaMemcpy(c->loss_ids.p, link_ids, sizeof(int) * n_obs, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->loss_first.p, first.data(), sizeof(int) * n_obs, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->loss_next.p, next.data(), sizeof(int) * n_obs, cudaMemcpyHostToDevice));
+    if (k_obs)
+      CK(cudaMemcpy(c->loss_obs.p, values, sizeof(double) * k_obs * n_obs,
+                    cudaMemcpyHostToDevice));
+    c->loss_kind = dtg::kLossMse;
+    c->loss_kobs = k_obs;
+    c->loss_nobs = n_obs;
+  });
+}
+
+int dtg_set_loss_control(dtg_ctx* c, int target_link, double desired_count) {
+  return guarded(c, [&] {
+    if (target_link < 0 || target_link >= c->L)
+      throw std::invalid_argument("control: target link out of range");
+    c->loss_kind = dtg::kLossControl;
+    c->loss_target = target_link;
+    c->loss_desired = desired_count;
+  });
+}
+
+int dtg_gradient_device_loss(dtg_ctx* c, double* d_rows) {
+  return guarded(c, [&] {
+    if (c->loss_kind == dtg::kLossNone)
+      throw std::invalid_argument("no device loss set (dtg_set_loss_mse / dtg_set_loss_control)");
+    if (c->last_T < 0 || !c->last_ckpt)
+      throw std::runtime_error("dtg_gradient_device_loss needs a preceding dtg_forward with checkpoint=1");
+    if (c->loss_kind == dtg::kLossMse && c->last_K < c->loss_kobs)
+      throw std::runtime_error("loss: fewer snapshots than observations");
+    const std::size_t B = c->B, L = c->L, N = c->N;
+    const int K = c->last_K;
+    cudaStream_t st = c->stream;
+    bool changed = false;
+    changed |= c->snap_seed.ensure(std::max<std::size_t>(1, B * K * L));
+    changed |= c->cum_seed.ensure(B * L);
+    changed |= c->x_seed.ensure(B * N);
+    if (changed) c->drop_graphs();
+    c->loss_val.ensure(B);
+    c->loss_extra.ensure(B);
+    const std::size_t R = 5 * L + 2;
+    c->rows.ensure(B * R);
+    if (K) CK(cudaMemsetAsync(c->snap_seed.p, 0, B * K * L * 8, st));
+    CK(cudaMemsetAsync(c->cum_seed.p, 0, B * L * 8, st));
+    CK(cudaMemsetAsync(c->x_seed.p, 0, B * N * 8, st));
+    dtg::LossView v{};
+    v.kind = c->loss_kind;
+    v.B = c->B;
+    v.L = c->L;
+    v.N = c->N;
+    v.T = c->last_T;
+    v.spi = c->last_spi;
+    v.K = K;
+    v.dn = static_cast<double>(c->cfg.delta_n);
+    v.cumh = c->cumh.p;
+    v.kobs = c->loss_kobs;
+    v.nobs = c->loss_nobs;
+    v.ids = c->loss_ids.p;
+    v.first = c->loss_first.p;
+    v.next = c->loss_next.p;
+    v.obs = c->loss_obs.p;
+    v.sc = 1.0 / (static_cast<double>(c->loss_kobs) * c->loss_nobs);
+    v.target = c->loss_target;
+    v.desired = c->loss_desired;
+    v.snap_seed = c->snap_seed.p;
+    v.cum_seed = c->cum_seed.p;
+    v.loss = c->loss_val.p;
+    v.extra = c->loss_extra.p;
+    dtg::launch_device_loss(v, st);
+    CK(cudaGetLastError());
+    if (c->last_T > 0) {
+      run_backward(c, nullptr, nullptr, nullptr, cudaMemcpyDeviceToDevice, true);
+    } else {
+      c->grads.ensure(B * 5 * L);
+      CK(cudaMemsetAsync(c->grads.p, 0, B * 5 * L * 8, st));
+    }
+    dtg::launch_pack_rows(c->B, c->L, c->grads.p, c->loss_val.p, c->loss_extra.p,
+                          d_rows ? d_rows : c->rows.p, st);
+    CK(cudaGetLastError());
+    c->launches += 2;
+    c->pending = true;
+  });
+}
+
+int dtg_reduce_draw_rows(dtg_ctx* c, int n_draws, const double* d_rows, int mode, double* out) {
+  return guarded(c, [&] {
+    if (mode != 0 && mode != 1) throw std::invalid_argument("reduce mode must be 0 or 1");
+    if (n_draws < 1) throw std::invalid_argument("no noise draws");
+    if (!d_rows && n_draws > c->B)
+      throw std::invalid_argument("internal draw rows hold only B scenarios");
+    const std::size_t R = 5 * static_cast<std::size_t>(c->L) + 2;
+    c->red.ensure(R);
+    if (!c->h_red) CK(cudaMallocHost(&c->h_red, R * 8));
+    cudaStream_t st = c->stream;
+    dtg::launch_reduce_rows(n_draws, c->L, d_rows ? d_rows : c->rows.p, mode, c->red.p, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->h_red, c->red.p, R * 8, cudaMemcpyDeviceToHost, st));
+    c->sync_check();
+    std::memcpy(out, c->h_red, R * 8);
   });
 }
 

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <limits>
 #include <map>
 #include <memory>
 #include <queue>
@@ -645,6 +646,267 @@ LossBuilder linear_quadratic_loss(std::vector<double> ws, std::vector<double> qs
   };
 }
 
+// ---- optimisation loops -------------------------------------------------------------
+void AdamW::step(std::vector<double>& params, const std::vector<double>& grads) {
+  if (params.size() != m_.size() || grads.size() != m_.size())
+    throw std::runtime_error("AdamW: size mismatch");
+  ++t_;
+  const double bc1 = 1.0 - std::pow(cfg_.beta1, t_);
+  const double bc2 = 1.0 - std::pow(cfg_.beta2, t_);
+  for (std::size_t i = 0; i < params.size(); ++i) {
+    m_[i] = cfg_.beta1 * m_[i] + (1.0 - cfg_.beta1) * grads[i];
+    v_[i] = cfg_.beta2 * v_[i] + (1.0 - cfg_.beta2) * grads[i] * grads[i];
+    const double mhat = m_[i] / bc1;
+    const double vhat = v_[i] / bc2;
+    params[i] -= cfg_.lr * (mhat / (std::sqrt(vhat) + cfg_.eps) + cfg_.weight_decay * params[i]);
+  }
+}
+
+namespace {
+double sigmoid_branchy(double raw) {
+  return raw >= 0.0 ? 1.0 / (1.0 + std::exp(-raw)) : std::exp(raw) / (1.0 + std::exp(raw));
+}
+}  // namespace
+
+double BoundedTransform::value(double raw) const {
+  return lo_ + (hi_ - lo_) * sigmoid_branchy(raw);
+}
+double BoundedTransform::dvalue(double raw) const {
+  const double s = sigmoid_branchy(raw);
+  return (hi_ - lo_) * s * (1.0 - s);
+}
+double BoundedTransform::raw_of(double value) const {
+  if (hi_ == lo_) return 0.0;
+  double f = (value - lo_) / (hi_ - lo_);
+  f = std::clamp(f, 1e-9, 1.0 - 1e-9);
+  return std::log(f / (1.0 - f));
+}
+double LowerBoundTransform::value(double raw) const {
+  const double sp = raw > 30.0 ? raw : std::log1p(std::exp(raw));
+  return floor_ + sp;
+}
+double LowerBoundTransform::dvalue(double raw) const { return sigmoid_branchy(raw); }
+double LowerBoundTransform::raw_of(double value) const {
+  const double y = std::max(value - floor_, 1e-12);
+  return y > 30.0 ? y : std::log(std::expm1(y));
+}
+
+namespace {
+
+// One optimisation iteration's device work: every noise draw of the iteration
+// is one scenario of a batched context; the initial state is uploaded once per
+// loop, parameters and noise seeds once per iteration.
+class DeviceLoop {
+ public:
+  DeviceLoop(const Scenario& s, int draws, const DrawExchange* ex) : s_(s), draws_(draws), ex_(ex) {
+    spi_ = steps_per_interval(s);
+    const InitialState init = seed_agents(s);
+    N_ = static_cast<int>(init.link.size());
+    L_ = s.net.n_links();
+    if (s.net.succ_off.size() != static_cast<std::size_t>(L_ + 1))
+      throw std::runtime_error("network CSR is stale (call rebuild_csr)");
+    if (s.cfg.soft_choices)
+      throw std::runtime_error(
+          "checkpointed backward requires discrete choices (compact state snapshots are exact "
+          "only for one-link-per-agent states)");
+    const int world = ex ? ex->world : 1;
+    if (world < 1 || (ex && (ex->rank < 0 || ex->rank >= world)))
+      throw std::invalid_argument("draw exchange: bad world size / rank");
+    if (draws % world)
+      throw std::invalid_argument("noise draws must divide evenly over the ranks");
+    local_ = draws / world;
+    first_ = ex ? ex->rank * local_ : 0;
+    if (ex && world > 1 && (!ex->d_local || !ex->d_full || !ex->gather))
+      throw std::invalid_argument("draw exchange needs d_local, d_full and gather");
+    ctx_ = detail::context_for(s, N_, local_, s.horizon_steps);
+    if (ex && ex->stream) check(ctx_, dtg_set_stream(ctx_, ex->stream));
+    check(ctx_, dtg_set_state(ctx_, -1, init.link.data(), init.pos.data()));
+    red_.resize(5 * static_cast<std::size_t>(L_) + 2);
+  }
+  dtg_ctx* ctx() const { return ctx_; }
+
+  /// Runs this rank's draws of one iteration; returns the draw-reduced row over
+  /// all draws [grads u|kappa|beta|alpha|cost, loss, extra] (dtg_reduce_draw_rows).
+  const std::vector<double>& run(const LinkParams& p, const RngStream& rng,
+                                 const std::vector<std::uint64_t>& its, int mode) {
+    check(ctx_, dtg_set_params(ctx_, -1, p.u.data(), p.kappa.data(), p.beta.data(),
+                               p.alpha.data(), p.cost.data()));
+    for (int b = 0; b < local_; ++b)
+      check(ctx_, dtg_set_noise(ctx_, b, rng.seed(), its[first_ + b]));
+    check(ctx_, dtg_forward(ctx_, s_.horizon_steps, spi_, 1));
+    const bool shared = ex_ && ex_->world > 1;
+    check(ctx_, dtg_gradient_device_loss(ctx_, shared ? ex_->d_local : nullptr));
+    if (shared) ex_->gather();
+    check(ctx_, dtg_reduce_draw_rows(ctx_, draws_, shared ? ex_->d_full : nullptr, mode,
+                                     red_.data()));
+    return red_;
+  }
+
+ private:
+  const Scenario& s_;
+  int draws_, local_ = 1, first_ = 0, spi_ = 1, N_ = 0, L_ = 0;
+  const DrawExchange* ex_;
+  dtg_ctx* ctx_ = nullptr;
+  std::vector<double> red_;
+};
+
+bool all_finite(const double* v, std::size_t n) {
+  for (std::size_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
+// nan_block (optimization.cpp:107-118) over the reduced gradient row.
+std::string nan_block_of(const std::vector<double>& red, int L) {
+  static const char* names[5] = {"u", "kappa", "beta", "alpha", "cost"};
+  for (int q = 0; q < 5; ++q)
+    if (!all_finite(red.data() + static_cast<std::size_t>(q) * L, L)) return names[q];
+  return "loss";
+}
+
+std::vector<std::uint64_t> iteration_noise(const OptimizeConfig& cfg, int it, int draws) {
+  std::vector<std::uint64_t> its(draws, 0);
+  if (cfg.resample_noise)
+    for (int k = 0; k < draws; ++k) its[k] = static_cast<std::uint64_t>(it * draws + k + 1);
+  return its;
+}
+
+}  // namespace
+
+CalibrationResult calibrate(const Scenario& s, const CountSeries& obs, const ParamRanges& bounds,
+                            const OptimizeConfig& cfg, const RngStream& rng,
+                            const LinkParams* init, const DrawExchange* ex) {
+  const auto t0 = Clock::now();
+  const int L = s.net.n_links();
+  if (obs.link_ids.empty()) throw std::runtime_error("loss: no observed links");
+  const BoundedTransform tu(bounds.u_lo, bounds.u_hi);
+  const BoundedTransform tk(bounds.kappa_lo, bounds.kappa_hi);
+  const BoundedTransform tb(bounds.beta_lo, bounds.beta_hi);
+  const BoundedTransform ta(bounds.alpha_lo, bounds.alpha_hi);
+  std::vector<double> raw(4 * static_cast<std::size_t>(L), 0.0);
+  if (init)
+    for (int l = 0; l < L; ++l) {
+      raw[l] = tu.raw_of(init->u[l]);
+      raw[L + l] = tk.raw_of(init->kappa[l]);
+      raw[2 * L + l] = tb.raw_of(init->beta[l]);
+      raw[3 * L + l] = ta.raw_of(init->alpha[l]);
+    }
+  const std::vector<double> fixed_cost =
+      init && !init->cost.empty() ? init->cost : std::vector<double>(L, 1.0);
+  auto realize = [&](const std::vector<double>& r) {
+    LinkParams p;
+    p.u.resize(L);
+    p.kappa.resize(L);
+    p.beta.resize(L);
+    p.alpha.resize(L);
+    p.cost = fixed_cost;
+    for (int l = 0; l < L; ++l) {
+      p.u[l] = tu.value(r[l]);
+      p.kappa[l] = tk.value(r[L + l]);
+      p.beta[l] = tb.value(r[2 * L + l]);
+      p.alpha[l] = ta.value(r[3 * L + l]);
+    }
+    return p;
+  };
+  const int draws = cfg.resample_noise ? std::max(1, cfg.noise_draws) : 1;
+  DeviceLoop loop(s, draws, ex);
+  {
+    std::vector<double> flat;
+    for (const auto& row : obs.values) {
+      if (row.size() != obs.link_ids.size())
+        throw std::runtime_error("loss: observation row width differs from the link list");
+      flat.insert(flat.end(), row.begin(), row.end());
+    }
+    check(loop.ctx(), dtg_set_loss_mse(loop.ctx(), obs.n_intervals(),
+                                       static_cast<int>(obs.link_ids.size()),
+                                       obs.link_ids.data(), flat.data()));
+  }
+  AdamW adam(4 * L, cfg.adam);
+  CalibrationResult res;
+  res.best_loss = std::numeric_limits<double>::infinity();
+  int since_best = 0;
+  for (int it = 0; it < cfg.max_iterations; ++it) {
+    const LinkParams params = realize(raw);
+    const auto& red = loop.run(params, rng, iteration_noise(cfg, it, draws), 0);
+    const double loss = red[5 * static_cast<std::size_t>(L)];
+    res.loss_curve.push_back(loss);
+    res.iterations = it + 1;
+    if (!std::isfinite(loss))
+      throw DivergenceError("calibration diverged at iteration " + std::to_string(it) +
+                            " (non-finite " + nan_block_of(red, L) + ")");
+    if (loss < res.best_loss) {
+      res.best_loss = loss;
+      res.best_params = params;
+      res.best_iteration = it;
+      since_best = 0;
+    } else if (++since_best >= cfg.patience) {
+      break;
+    }
+    std::vector<double> rg(4 * static_cast<std::size_t>(L));
+    for (int l = 0; l < L; ++l) {
+      rg[l] = red[l] / draws * tu.dvalue(raw[l]);
+      rg[L + l] = red[L + l] / draws * tk.dvalue(raw[L + l]);
+      rg[2 * L + l] = red[2 * L + l] / draws * tb.dvalue(raw[2 * L + l]);
+      rg[3 * L + l] = red[3 * L + l] / draws * ta.dvalue(raw[3 * L + l]);
+    }
+    adam.step(raw, rg);
+  }
+  res.wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+  return res;
+}
+
+ControlResult optimize_control(const Scenario& s, const LinkParams& calibrated, int target_link,
+                               double desired_count, const ControlConfig& cfg,
+                               const RngStream& rng, const DrawExchange* ex) {
+  const auto t0 = Clock::now();
+  const int L = s.net.n_links();
+  if (target_link < 0 || target_link >= L)
+    throw std::runtime_error("control: target link out of range");
+  const LowerBoundTransform tc(cfg.cost_floor);
+  std::vector<double> raw(L);
+  for (int l = 0; l < L; ++l) raw[l] = tc.raw_of(calibrated.cost[l]);
+  const int draws = cfg.opt.resample_noise ? std::max(1, cfg.opt.noise_draws) : 1;
+  DeviceLoop loop(s, draws, ex);
+  check(loop.ctx(), dtg_set_loss_control(loop.ctx(), target_link, desired_count));
+  AdamW adam(L, cfg.opt.adam);
+  ControlResult res;
+  res.desired = desired_count;
+  res.best_loss = std::numeric_limits<double>::infinity();
+  int since_best = 0;
+  bool any_nonzero_grad = false;
+  for (int it = 0; it < cfg.opt.max_iterations; ++it) {
+    LinkParams params = calibrated;
+    for (int l = 0; l < L; ++l) params.cost[l] = tc.value(raw[l]);
+    const auto& red = loop.run(params, rng, iteration_noise(cfg.opt, it, draws), 1);
+    const double loss = red[5 * static_cast<std::size_t>(L)];
+    const double achieved = red[5 * static_cast<std::size_t>(L) + 1];
+    res.loss_curve.push_back(loss);
+    res.iterations = it + 1;
+    if (!std::isfinite(loss))
+      throw DivergenceError("control diverged at iteration " + std::to_string(it));
+    if (loss < res.best_loss) {
+      res.best_loss = loss;
+      res.cost = params.cost;
+      res.achieved = achieved;
+      since_best = 0;
+    } else if (++since_best >= cfg.opt.patience) {
+      break;
+    }
+    std::vector<double> rg(L);
+    for (int l = 0; l < L; ++l) {
+      rg[l] = red[4 * static_cast<std::size_t>(L) + l] * tc.dvalue(raw[l]);
+      if (rg[l] != 0.0) any_nonzero_grad = true;
+    }
+    adam.step(raw, rg);
+  }
+  res.zero_gradient_stall = !any_nonzero_grad;
+  res.gap_fraction = desired_count != 0.0
+                         ? std::abs(res.achieved - desired_count) / std::abs(desired_count)
+                         : std::abs(res.achieved - desired_count);
+  res.wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+  return res;
+}
+
 CountSeries series_from_levels(const std::vector<std::vector<double>>& cum_per_step,
                                const std::vector<int>& link_ids, int interval_s, double dt,
                                int delta_n) {
@@ -687,6 +949,9 @@ int scn_guard(dtg_scenario* sc, F&& f) {
   } catch (const dtg::ApiError& e) {
     if (sc) sc->err = e.what();
     return e.code;
+  } catch (const dtg::DivergenceError& e) {
+    if (sc) sc->err = e.what();
+    return DTG_ERR_DIVERGENCE;
   } catch (const std::invalid_argument& e) {
     if (sc) sc->err = e.what();
     return DTG_ERR_CONFIG;
@@ -987,3 +1252,123 @@ int dtg_mse_loss(int k_snap, int n_links, const double* snapshots, int n_obs, co
 }
 
 }  // extern "C"
+
+namespace {
+dtg::OptimizeConfig optimize_config(const dtg_optimize_config* c) {
+  dtg::OptimizeConfig o;
+  if (!c) return o;
+  o.adam.lr = c->lr;
+  o.adam.weight_decay = c->weight_decay;
+  o.adam.beta1 = c->beta1;
+  o.adam.beta2 = c->beta2;
+  o.adam.eps = c->eps;
+  o.patience = c->patience;
+  o.max_iterations = c->max_iterations;
+  o.resample_noise = c->resample_noise != 0;
+  o.noise_draws = c->noise_draws;
+  return o;
+}
+
+dtg::DrawExchange draw_exchange(const dtg_draw_exchange* e) {
+  dtg::DrawExchange x;
+  if (!e) return x;
+  x.world = e->world;
+  x.rank = e->rank;
+  x.d_local = e->d_local;
+  x.d_full = e->d_full;
+  x.stream = e->stream;
+  if (e->gather) {
+    const dtg_gather_fn fn = e->gather;
+    void* user = e->user;
+    x.gather = [fn, user] {
+      if (fn(user) != 0) throw std::runtime_error("draw exchange: gather callback failed");
+    };
+  }
+  return x;
+}
+}  // namespace
+
+int dtg_calibrate(dtg_scenario* sc, int n_obs, const int* obs_ids, int k_obs,
+                  const double* obs_values, const dtg_param_ranges* bounds,
+                  const dtg_optimize_config* cfg, uint64_t root_seed, const double* init_u,
+                  const double* init_kappa, const double* init_beta, const double* init_alpha,
+                  const double* init_cost, double* best_u, double* best_kappa,
+                  double* best_beta, double* best_alpha, double* best_cost, double* best_loss,
+                  int* best_iteration, int* iterations, double* loss_curve,
+                  double* wall_seconds, const dtg_draw_exchange* exc) {
+  return scn_guard(sc, [&] {
+    const dtg::DrawExchange ex = draw_exchange(exc);
+    const int L = sc->s.net.n_links();
+    dtg::CountSeries obs;
+    if (n_obs > 0) obs.link_ids.assign(obs_ids, obs_ids + n_obs);
+    obs.interval_s = sc->s.obs_interval_s;
+    for (int q = 0; q < k_obs; ++q)
+      obs.values.emplace_back(obs_values + static_cast<std::size_t>(q) * n_obs,
+                              obs_values + static_cast<std::size_t>(q + 1) * n_obs);
+    dtg::ParamRanges r;
+    if (bounds) {
+      r.u_lo = bounds->u_lo;
+      r.u_hi = bounds->u_hi;
+      r.kappa_lo = bounds->kappa_lo;
+      r.kappa_hi = bounds->kappa_hi;
+      r.beta_lo = bounds->beta_lo;
+      r.beta_hi = bounds->beta_hi;
+      r.alpha_lo = bounds->alpha_lo;
+      r.alpha_hi = bounds->alpha_hi;
+    }
+    dtg::LinkParams init;
+    const bool have_init = init_u && init_kappa && init_beta && init_alpha;
+    if (have_init) {
+      init.u.assign(init_u, init_u + L);
+      init.kappa.assign(init_kappa, init_kappa + L);
+      init.beta.assign(init_beta, init_beta + L);
+      init.alpha.assign(init_alpha, init_alpha + L);
+      if (init_cost) init.cost.assign(init_cost, init_cost + L);
+    }
+    const dtg::CalibrationResult res =
+        dtg::calibrate(sc->s, obs, r, optimize_config(cfg), dtg::RngStream(root_seed),
+                       have_init ? &init : nullptr, exc ? &ex : nullptr);
+    sc->last_ctx = dtg::detail::g_last_ctx;
+    const auto& bp = res.best_params;
+    if (!bp.u.empty()) {
+      if (best_u) std::copy(bp.u.begin(), bp.u.end(), best_u);
+      if (best_kappa) std::copy(bp.kappa.begin(), bp.kappa.end(), best_kappa);
+      if (best_beta) std::copy(bp.beta.begin(), bp.beta.end(), best_beta);
+      if (best_alpha) std::copy(bp.alpha.begin(), bp.alpha.end(), best_alpha);
+      if (best_cost) std::copy(bp.cost.begin(), bp.cost.end(), best_cost);
+    }
+    if (best_loss) *best_loss = res.best_loss;
+    if (best_iteration) *best_iteration = res.best_iteration;
+    if (iterations) *iterations = res.iterations;
+    if (loss_curve) std::copy(res.loss_curve.begin(), res.loss_curve.end(), loss_curve);
+    if (wall_seconds) *wall_seconds = res.wall_seconds;
+  });
+}
+
+int dtg_optimize_control(dtg_scenario* sc, const double* u, const double* kappa,
+                         const double* beta, const double* alpha, const double* cost,
+                         int target_link, double desired, const dtg_optimize_config* cfg,
+                         double cost_floor, uint64_t root_seed, double* cost_out,
+                         double* achieved, double* gap_fraction, double* best_loss,
+                         int* iterations, double* loss_curve, int* zero_gradient_stall,
+                         double* wall_seconds, const dtg_draw_exchange* exc) {
+  return scn_guard(sc, [&] {
+    const dtg::DrawExchange ex = draw_exchange(exc);
+    const int L = sc->s.net.n_links();
+    dtg::ControlConfig cc;
+    cc.opt = optimize_config(cfg);
+    cc.cost_floor = cost_floor;
+    const dtg::ControlResult res =
+        dtg::optimize_control(sc->s, make_params(L, u, kappa, beta, alpha, cost), target_link,
+                              desired, cc, dtg::RngStream(root_seed), exc ? &ex : nullptr);
+    sc->last_ctx = dtg::detail::g_last_ctx;
+    if (cost_out && !res.cost.empty()) std::copy(res.cost.begin(), res.cost.end(), cost_out);
+    if (achieved) *achieved = res.achieved;
+    if (gap_fraction) *gap_fraction = res.gap_fraction;
+    if (best_loss) *best_loss = res.best_loss;
+    if (iterations) *iterations = res.iterations;
+    if (loss_curve) std::copy(res.loss_curve.begin(), res.loss_curve.end(), loss_curve);
+    if (zero_gradient_stall) *zero_gradient_stall = res.zero_gradient_stall ? 1 : 0;
+    if (wall_seconds) *wall_seconds = res.wall_seconds;
+  });
+}

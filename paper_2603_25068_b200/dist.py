@@ -96,3 +96,66 @@ class ShardedGradient:
         full, total = gather_ordered_sum(local, self.world, group)
         total = total.cpu().numpy()
         return float(total[-1]), total[:-1].reshape(5, sc.n_links), full.cpu().numpy()
+
+
+class DeviceDrawExchange:
+    """NCCL draw exchange for the device-resident optimisation loops
+    (include/dtg.h dtg_draw_exchange): this rank's per-draw rows
+    [D/world, 5L+2] are all-gathered, rank-major (= draw order), into
+    [D, 5L+2] on `stream`, and every rank reduces all D rows in draw order on
+    its device, so calibrate / optimize_control return the single-GPU result
+    bit for bit for any world size.  Only O(L) bytes per draw cross NVLink per
+    iteration; nothing goes through host memory except the reduced row."""
+
+    def __init__(self, n_links: int, n_draws: int, world: int, rank: int, group=None, stream=None):
+        import torch
+        import torch.distributed as dist
+
+        from ._lib import DrawExchange, GatherFn
+
+        shard(n_draws, world, rank)  # validates divisibility
+        R = 5 * n_links + 2
+        self.stream = stream or torch.cuda.Stream()
+        self.local = torch.zeros((n_draws // world, R), dtype=torch.float64, device="cuda")
+        self.full = torch.zeros((n_draws, R), dtype=torch.float64, device="cuda")
+        self.group = group
+        self.calls = 0
+
+        def _gather(_user):
+            try:
+                with torch.cuda.stream(self.stream):
+                    if world > 1:
+                        dist.all_gather_into_tensor(self.full, self.local, group=self.group)
+                    else:
+                        self.full.copy_(self.local)
+                self.calls += 1
+                return 0
+            except Exception:  # reported as a runtime error by the C++ loop
+                return 1
+
+        self._cb = GatherFn(_gather)  # keep the trampoline alive
+        self.c = DrawExchange(world, rank, self.local.data_ptr(), self.full.data_ptr(),
+                              self.stream.cuda_stream, self._cb, None)
+
+
+def calibrate_sharded(sc, obs_ids, obs_values, seed: int, cfg=None, bounds=None, init=None,
+                      world: int = 1, rank: int = 0, group=None, stream=None):
+    """calibrate() with the iteration's noise draws sharded over `world` GPUs."""
+    from .engine import OptimizeConfig, calibrate
+
+    cfg = cfg or OptimizeConfig()
+    draws = max(1, cfg.noise_draws) if cfg.resample_noise else 1
+    ex = DeviceDrawExchange(sc.n_links, draws, world, rank, group, stream)
+    return calibrate(sc, obs_ids, obs_values, seed, bounds=bounds, cfg=cfg, init=init, exchange=ex.c)
+
+
+def optimize_control_sharded(sc, calibrated, target_link: int, desired: float, seed: int, cfg=None,
+                             cost_floor: float = 0.05, world: int = 1, rank: int = 0, group=None, stream=None):
+    """optimize_control() with the iteration's noise draws sharded over `world` GPUs."""
+    from .engine import OptimizeConfig, optimize_control
+
+    cfg = cfg or OptimizeConfig()
+    draws = max(1, cfg.noise_draws) if cfg.resample_noise else 1
+    ex = DeviceDrawExchange(sc.n_links, draws, world, rank, group, stream)
+    return optimize_control(sc, calibrated, target_link, desired, seed, cfg=cfg, cost_floor=cost_floor,
+                            exchange=ex.c)

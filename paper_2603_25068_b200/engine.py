@@ -16,7 +16,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from ._lib import NetDesc, SimConfig, load, ptr, raise_for
+from ._lib import NetDesc, OptimizeConfig as _OptC, ParamRangesC, SimConfig, load, ptr, raise_for
 
 PHYSICAL, VIRTUAL_INFLOW, VIRTUAL_OUTFLOW = 0, 1, 2
 
@@ -252,6 +252,116 @@ def simulate_gradient_mse(sc: Scenario, params: LinkParams, seed: int, obs_ids, 
     return loss, grads
 
 
+@dataclass
+class ParamRanges:
+    """ParamRanges (network.hpp) — sampling and calibration bounds."""
+
+    u_lo: float = 13.9
+    u_hi: float = 22.2
+    kappa_lo: float = 0.18
+    kappa_hi: float = 0.22
+    beta_lo: float = 0.0
+    beta_hi: float = 5.0
+    alpha_lo: float = 0.01
+    alpha_hi: float = 5.0
+
+    def c(self) -> ParamRangesC:
+        return ParamRangesC(self.u_lo, self.u_hi, self.kappa_lo, self.kappa_hi, self.beta_lo,
+                            self.beta_hi, self.alpha_lo, self.alpha_hi)
+
+
+@dataclass
+class OptimizeConfig:
+    """AdamWConfig + OptimizeConfig (optimization.hpp:18-24, 72-82)."""
+
+    lr: float = 0.1
+    weight_decay: float = 1e-5
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    patience: int = 20
+    max_iterations: int = 200
+    resample_noise: bool = True
+    noise_draws: int = 1
+
+    def c(self) -> _OptC:
+        return _OptC(self.lr, self.weight_decay, self.beta1, self.beta2, self.eps, self.patience,
+                     self.max_iterations, int(self.resample_noise), self.noise_draws)
+
+
+@dataclass
+class CalibrationResult:
+    """CalibrationResult (optimization.hpp:84-91)."""
+
+    best_params: Optional[LinkParams]
+    best_loss: float
+    best_iteration: int
+    iterations: int
+    loss_curve: np.ndarray
+    wall_seconds: float
+
+
+@dataclass
+class ControlResult:
+    """ControlResult (optimization.hpp:106-116)."""
+
+    cost: np.ndarray
+    desired: float
+    achieved: float
+    gap_fraction: float
+    best_loss: float
+    iterations: int
+    loss_curve: np.ndarray
+    zero_gradient_stall: bool
+    wall_seconds: float
+
+
+def calibrate(sc: Scenario, obs_ids, obs_values, seed: int, bounds: Optional[ParamRanges] = None,
+              cfg: Optional[OptimizeConfig] = None, init: Optional[LinkParams] = None,
+              exchange=None) -> CalibrationResult:
+    """calibrate (optimization.cpp:122-219): AdamW fit of (u, kappa, beta, alpha)
+    to counts obs_values [K_obs, n_obs] on links obs_ids; each iteration is one
+    batched device forward + reverse sweep over its noise draws with the MSE loss
+    and the draw sum on the device.  Raises DivergenceError on a non-finite loss."""
+    bounds = bounds or ParamRanges()
+    cfg = cfg or OptimizeConfig()
+    L = sc.n_links
+    ids = np.ascontiguousarray(obs_ids, np.int32)
+    vals = np.ascontiguousarray(obs_values, np.float64).reshape(-1, max(len(ids), 1))
+    best = [np.zeros(L) for _ in range(5)]
+    bl, bi, its, wall = C.c_double(), C.c_int(), C.c_int(), C.c_double()
+    curve = np.zeros(max(cfg.max_iterations, 1))
+    ia = init.arrays() if init is not None else [None] * 5
+    bc, oc = bounds.c(), cfg.c()
+    sc._check(sc._lib.dtg_calibrate(sc._h, len(ids), ids, vals.shape[0] if len(ids) else 0, vals.ravel(),
+                                    C.byref(bc), C.byref(oc), seed, *(ptr(a) for a in ia), *best,
+                                    C.byref(bl), C.byref(bi), C.byref(its), curve, C.byref(wall),
+                                    None if exchange is None else C.byref(exchange)))
+    n = its.value
+    return CalibrationResult(LinkParams(*best) if bi.value >= 0 else None, bl.value, bi.value, n,
+                             curve[:n].copy(), wall.value)
+
+
+def optimize_control(sc: Scenario, calibrated: LinkParams, target_link: int, desired: float, seed: int,
+                     cfg: Optional[OptimizeConfig] = None, cost_floor: float = 0.05,
+                     exchange=None) -> ControlResult:
+    """optimize_control (optimization.cpp:221-295) with the device iteration."""
+    cfg = cfg or OptimizeConfig()
+    L = sc.n_links
+    cost = np.zeros(L)
+    ach, gap, bl, wall = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+    its, stall = C.c_int(), C.c_int()
+    curve = np.zeros(max(cfg.max_iterations, 1))
+    oc = cfg.c()
+    sc._check(sc._lib.dtg_optimize_control(sc._h, *calibrated.arrays(), target_link, desired, C.byref(oc),
+                                           cost_floor, seed, cost, C.byref(ach), C.byref(gap), C.byref(bl),
+                                           C.byref(its), curve, C.byref(stall), C.byref(wall),
+                                           None if exchange is None else C.byref(exchange)))
+    n = its.value
+    return ControlResult(cost, desired, ach.value, gap.value, bl.value, n, curve[:n].copy(),
+                         bool(stall.value), wall.value)
+
+
 class Engine:
     """Level-1 device context: B scenarios of one network on one GPU."""
 
@@ -368,6 +478,26 @@ class Engine:
         """Device pointers (ints, e.g. torch.Tensor.data_ptr()); no host sync."""
         self._check(self._lib.dtg_backward_device(self._h, C.c_void_p(d_snap), C.c_void_p(d_cum),
                                                   C.c_void_p(d_x), C.c_void_p(d_grads)))
+
+    def set_loss_mse(self, obs_ids, obs_values):
+        """Device MSE loss (mse_loss_builder): obs_values [K_obs, n_obs] in vehicles."""
+        ids = np.ascontiguousarray(obs_ids, np.int32)
+        vals = np.ascontiguousarray(obs_values, np.float64).reshape(-1, max(len(ids), 1))
+        self._check(self._lib.dtg_set_loss_mse(self._h, vals.shape[0], len(ids), ids, vals.ravel()))
+
+    def set_loss_control(self, target_link: int, desired: float):
+        self._check(self._lib.dtg_set_loss_control(self._h, target_link, desired))
+
+    def gradient_device_loss(self, d_rows: int = 0):
+        """Loss + seeds + reverse sweep on the device; rows [B, 5L+2] into the
+        device pointer d_rows (0 = the context's own buffer).  No host sync."""
+        self._check(self._lib.dtg_gradient_device_loss(self._h, C.c_void_p(d_rows or None)))
+
+    def reduce_draw_rows(self, n_draws: int, d_rows: int = 0, mode: int = 0) -> np.ndarray:
+        """Draw-ordered sum of n_draws rows -> [5L+2] host array (grads, loss, extra)."""
+        out = np.zeros(5 * self.L + 2)
+        self._check(self._lib.dtg_reduce_draw_rows(self._h, n_draws, C.c_void_p(d_rows or None), mode, out))
+        return out
 
     def profile_kernels(self, T: int, steps_per_interval: int, backward: bool = False):
         """Per-kernel-kind device time (ms, CUDA events) of one forward (or the

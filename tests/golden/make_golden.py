@@ -136,6 +136,43 @@ def chain_net(phys_len=200.0, virt_len=400.0):
             np.array([virt_len, phys_len, phys_len, virt_len]), np.array([1, 0, 0, 2], np.int32), 5)
 
 
+def optim_cases():
+    """calibrate / optimize_control (optimization.cpp:122-295) on a 3x3 grid."""
+    rs = RefScenario.grid(R, 3, 300.0, 42, 600.0).configure(300, 1, 120, 30)
+    truth = rs.sample_parameters(42)
+    tr = rs.forward(truth, 7, 0)
+    obs_ids = np.array([j for j in range(rs.n_links) if rs.links()[3][j] == 0], np.int32)
+    obs = tr["cum_per_step"][29::30][:, obs_ids] * 1.0
+    cfg = dict(max_iterations=6, patience=3, noise_draws=3, lr=0.1)
+    cal = rs.calibrate(obs_ids, obs, 5, cfg=cfg)
+    L = rs.n_links
+    f, t, ln, k = rs.links()
+    lk0, ps0 = rs.seed_agents()
+    net = dict(frm=f, to=t, length=ln, kind=k, n_nodes=np.int32(rs.n_nodes), link0=lk0, pos0=ps0,
+               truth=params_arrays(truth))
+    cfgv = np.array([cfg["max_iterations"], cfg["patience"], cfg["noise_draws"], cfg["lr"]], np.float64)
+    save("calib_grid3", obs_ids=obs_ids, obs=obs, cfg=cfgv, best=cal["best"], best_loss=np.float64(cal["best_loss"]),
+         best_iteration=np.int32(cal["best_iteration"]), iterations=np.int32(cal["iterations"]),
+         loss_curve=cal["loss_curve"], meta=np.array([5, 0, 120, 30, 1, 1], np.float64), **net)
+    # the same from a given init (raw_of path), one draw, fixed noise
+    init = rs.sample_parameters(3)
+    cfg1 = dict(max_iterations=4, patience=20, noise_draws=1, resample_noise=False, lr=0.05)
+    cal1 = rs.calibrate(obs_ids, obs, 9, cfg=cfg1, init=init)
+    save("calib_grid3_init", init=params_arrays(init), best=cal1["best"], best_loss=np.float64(cal1["best_loss"]),
+         best_iteration=np.int32(cal1["best_iteration"]), iterations=np.int32(cal1["iterations"]),
+         loss_curve=cal1["loss_curve"])
+    # control toward 1.5x the achieved count on a busy physical link
+    cum_final = tr["cum_per_step"][-1]
+    target = int(obs_ids[np.argmax(cum_final[obs_ids])])
+    desired = float(cum_final[target]) * 1.5
+    cfgc = dict(max_iterations=5, patience=3, noise_draws=2, lr=0.2)
+    ctl = rs.optimize_control(truth, target, desired, 7, cfg=cfgc)
+    save("control_grid3", params=params_arrays(truth), target=np.int32(target), desired=np.float64(desired),
+         cost=ctl["cost"], achieved=np.float64(ctl["achieved"]), gap_fraction=np.float64(ctl["gap_fraction"]),
+         best_loss=np.float64(ctl["best_loss"]), iterations=np.int32(ctl["iterations"]),
+         zero_gradient_stall=np.int32(ctl["zero_gradient_stall"]), loss_curve=ctl["loss_curve"])
+
+
 def main():
     # RNG known-answer values (include/dtsim/rng.hpp, tensor.cpp:682-699)
     seeds = np.array([0, 1, 7, 42, 2**63 + 5, 0xDEADBEEF], np.uint64)
@@ -197,4 +234,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["optim"]:
+        optim_cases()
+    else:
+        main()
+        optim_cases()

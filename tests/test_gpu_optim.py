@@ -1,0 +1,158 @@
+"""Device-resident optimisation iteration on the GPU.
+
+* device loss + seeds + draw reduction == the host loss path, bit for bit;
+* calibrate / optimize_control through the C-ABI vs the reference's own
+  recorded runs (tests/golden/{calib_grid3,calib_grid3_init,control_grid3}).
+
+Tolerances: the device adjoint sums in a different order than the reference
+tape (gradients agree to ~1e-15 normwise, tests/test_gpu_golden.py), so raw
+parameters after AdamW can differ in the last bits; loss values are count
+based and must agree to 1e-12 relative, parameters to 1e-9 relative.
+"""
+import numpy as np
+import pytest
+
+from golden_cases import load
+
+P = pytest.importorskip("paper_2603_25068_b200")
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _scenario(d):
+    sc = P.Scenario.grid(3, 300.0, 42, 600.0).configure(300, 1, 120, 30)
+    f, t, ln, k = sc.links()
+    assert np.array_equal(f, d["frm"]) and np.array_equal(ln, d["length"])
+    lk, ps = sc.seed_agents()
+    assert np.array_equal(lk, d["link0"]) and np.array_equal(ps, d["pos0"])
+    return sc
+
+
+def test_device_loss_rows_match_host_loss_path():
+    d = load("calib_grid3")
+    sc = _scenario(d)
+    p = P.LinkParams(*d["truth"])
+    its = [3, 4, 5, 6]
+    host_loss, host_grads = P.simulate_gradient_mse(sc, p, 5, d["obs_ids"], d["obs"], noise_iterations=its)
+    eng = P.Engine(sc, n_scenarios=len(its), max_steps=120)
+    stream = torch.cuda.Stream()
+    eng.set_stream(stream.cuda_stream)
+    lk, ps = sc.seed_agents()
+    eng.set_params(p)
+    eng.set_state(lk, ps)
+    for b, it in enumerate(its):
+        eng.set_noise(5, it, b)
+    eng.forward(120, sc.steps_per_interval, checkpoint=True)
+    eng.set_loss_mse(d["obs_ids"], d["obs"])
+    rows = torch.zeros((len(its), 5 * sc.n_links + 2), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    eng.gradient_device_loss(rows.data_ptr())
+    stream.synchronize()
+    r = rows.cpu().numpy()
+    L = sc.n_links
+    np.testing.assert_array_equal(r[:, 5 * L], host_loss)
+    np.testing.assert_array_equal(r[:, :5 * L].reshape(len(its), 5, L), host_grads)
+    red = eng.reduce_draw_rows(len(its), rows.data_ptr(), mode=0)
+    g = host_grads[0].copy()
+    for k in range(1, len(its)):
+        g = g + host_grads[k]
+    np.testing.assert_array_equal(red[:5 * L].reshape(5, L), g)
+    loss = 0.0
+    for v in host_loss:
+        loss += v / len(its)
+    assert red[5 * L] == loss
+
+
+def test_device_control_rows():
+    d = load("control_grid3")
+    sc = _scenario(load("calib_grid3"))
+    p = P.LinkParams(*d["params"])
+    target, desired = int(d["target"]), float(d["desired"])
+    L = sc.n_links
+    eng = P.Engine(sc, n_scenarios=2, max_steps=120)
+    lk, ps = sc.seed_agents()
+    eng.set_params(p)
+    eng.set_state(lk, ps)
+    eng.set_noise(7, 1, 0)
+    eng.set_noise(7, 2, 1)
+    eng.forward(120, sc.steps_per_interval, checkpoint=True)
+    cum = eng.read_cum_all()
+    eng.set_loss_control(target, desired)
+    eng.gradient_device_loss()
+    red = eng.reduce_draw_rows(2, mode=1)
+    wc = np.zeros(L)
+    host = P.simulate_gradient(sc, p, 7, noise_iterations=[1, 2], wc=wc)  # snapshots / cum_final
+    loss, ach = 0.0, 0.0
+    for b in range(2):
+        c = cum[b, -1, target]
+        assert c == host[b].cum_final[target]
+        dd = c * 1 + (-desired)
+        loss += dd * dd / 2
+        ach += c * 1 / 2
+    assert red[5 * L] == loss
+    assert red[5 * L + 1] == ach
+
+
+def test_calibrate_matches_reference_fixture():
+    d = load("calib_grid3")
+    sc = _scenario(d)
+    it, pat, draws, lr = d["cfg"]
+    cfg = P.OptimizeConfig(max_iterations=int(it), patience=int(pat), noise_draws=int(draws), lr=float(lr))
+    res = P.calibrate(sc, d["obs_ids"], d["obs"], 5, cfg=cfg)
+    assert res.iterations == int(d["iterations"])
+    assert res.best_iteration == int(d["best_iteration"])
+    np.testing.assert_allclose(res.loss_curve, d["loss_curve"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(np.stack(res.best_params.arrays()), d["best"], rtol=1e-9, atol=0)
+
+
+def test_calibrate_from_init_matches_reference_fixture():
+    base = load("calib_grid3")
+    d = load("calib_grid3_init")
+    sc = _scenario(base)
+    cfg = P.OptimizeConfig(max_iterations=4, patience=20, noise_draws=1, resample_noise=False, lr=0.05)
+    res = P.calibrate(sc, base["obs_ids"], base["obs"], 9, cfg=cfg, init=P.LinkParams(*d["init"]))
+    np.testing.assert_allclose(res.loss_curve, d["loss_curve"], rtol=1e-12, atol=0)
+    assert res.best_iteration == int(d["best_iteration"])
+    np.testing.assert_allclose(np.stack(res.best_params.arrays()), d["best"], rtol=1e-9, atol=0)
+
+
+def test_control_matches_reference_fixture():
+    d = load("control_grid3")
+    sc = _scenario(load("calib_grid3"))
+    cfg = P.OptimizeConfig(max_iterations=5, patience=3, noise_draws=2, lr=0.2)
+    res = P.optimize_control(sc, P.LinkParams(*d["params"]), int(d["target"]), float(d["desired"]), 7, cfg=cfg)
+    np.testing.assert_allclose(res.loss_curve, d["loss_curve"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(res.cost, d["cost"], rtol=1e-9, atol=0)
+    assert res.achieved == float(d["achieved"])
+    assert res.iterations == int(d["iterations"])
+    assert res.zero_gradient_stall == bool(d["zero_gradient_stall"])
+
+
+def test_calibrate_divergence_raises():
+    d = load("calib_grid3")
+    sc = _scenario(d)
+    obs = d["obs"].copy()
+    obs[0, 0] = np.inf
+    with pytest.raises(P.DivergenceError):
+        P.calibrate(sc, d["obs_ids"], obs, 5, cfg=P.OptimizeConfig(max_iterations=2))
+
+
+def test_sharded_exchange_world1_is_bit_identical():
+    """The NCCL draw-exchange path (callback gather into device rows) gives the
+    single-GPU loop's result bit for bit (world 1: the gather is a copy)."""
+    from paper_2603_25068_b200.dist import calibrate_sharded
+
+    d = load("calib_grid3")
+    sc = _scenario(d)
+    cfg = P.OptimizeConfig(max_iterations=3, patience=3, noise_draws=3, lr=0.1)
+    a = P.calibrate(sc, d["obs_ids"], d["obs"], 5, cfg=cfg)
+    b = calibrate_sharded(sc, d["obs_ids"], d["obs"], 5, cfg=cfg)
+    np.testing.assert_array_equal(a.loss_curve, b.loss_curve)
+    np.testing.assert_array_equal(np.stack(a.best_params.arrays()), np.stack(b.best_params.arrays()))
