@@ -92,7 +92,8 @@ int dtg_set_mode(dtg_ctx* ctx, int mode);
 int dtg_profile_backward(dtg_ctx* ctx, double* phase_us, int* grid_out);
 int dtg_last_mode(const dtg_ctx* ctx);
 /* Tuning knobs: flag 0 = grid barrier implementation (1: release/acquire
- * counter, default; 0: cooperative_groups grid.sync). */
+ * counter, default; 0: cooperative_groups grid.sync); flag 1 = fused
+ * forward slot mapping (-1 auto, 0 interleaved blocks, 1 contiguous). */
 int dtg_set_flag(dtg_ctx* ctx, int flag, int value);
 /* Measurement hook: one persistent forward with %globaltimer stamps; returns
  * the mean per-step span (us) of [slot phase, barrier 1, link phase,

@@ -38,6 +38,7 @@ struct CView {
   unsigned long long* tstamp;  // optional [T][grid][4]
   unsigned int* gbar;  // grid-barrier counter (null: cooperative_groups grid.sync)
   unsigned long long* wstamp;  // optional per-warp slot-phase record [T][warps][4]
+  int contig;          // 1: contiguous slot range per CTA, 0: interleaved 512-slot blocks
 };
 
 void launch_pack_succ(const DevView& d, double* srec, cudaStream_t st);

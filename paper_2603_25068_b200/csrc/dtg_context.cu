@@ -126,6 +126,7 @@ struct dtg_ctx {
   DevBuf<double> srec;
   DevBuf<unsigned int> gbar;
   bool custom_barrier = true;
+  int contig_mode = -1;  // -1 auto, 0 interleaved, 1 contiguous (fused forward slot mapping)
   bool want_wstamp = false;
   DevBuf<unsigned long long> wst;
   DevBuf<dtg::Cand> cands;
@@ -539,6 +540,9 @@ int dtg_set_flag(dtg_ctx* c, int flag, int value) {
     case 0:  // grid barrier: 1 release/acquire counter (default), 0 cooperative_groups grid.sync
       c->custom_barrier = value != 0;
       return DTG_OK;
+    case 1:  // fused forward slot mapping: -1 auto, 0 interleaved, 1 contiguous
+      c->contig_mode = value < 0 ? -1 : (value ? 1 : 0);
+      return DTG_OK;
     default:
       return fail(c, DTG_ERR_CONFIG, "unknown flag");
   }
@@ -754,6 +758,9 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
         const int want = (std::max(c->N, c->L) + dtg::kClusterThreads - 1) / dtg::kClusterThreads;
         V.cs = std::max(1, std::min(want, c->pgrid_max / c->B));
       }
+      // interleaved 512-slot blocks by default (measured faster at C3 dn30
+      // B=1/8 and dn1: spreads dense runs of arrived heads over the CTAs)
+      V.contig = c->contig_mode >= 0 ? c->contig_mode : 0;
       c->last_grid = c->B * V.cs;
       c->last_cs = V.cs;
       V.wstamp = nullptr;

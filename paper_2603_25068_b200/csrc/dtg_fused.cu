@@ -36,18 +36,59 @@ namespace {
 
 constexpr int kBatch = 4;   // slots per thread in flight together
 
+constexpr int kFastDeg = 5;  // successor counts up to this take the unrolled head path
+
 // Link choice of one arrived head (node_model.cpp:45-97, first stage
 // precomputed per link) and its own merge noise for the chosen row; registers
 // the head as a merge column {alpha, g', slot, id, link} of that row.
-__device__ void head_choice(const CView& V, std::size_t bl, std::uint64_t h1l, std::uint64_t h1m, int k, int j,
-                            int a, const int* soff_s, const double* slz) {
+//
+// For deg <= kFastDeg the successor draws are fully unrolled so their RNG/log
+// chains are independent instructions the scheduler interleaves (the heads are
+// the critical path of the slot phase); the softmax runs on registers with the
+// same operations in the same order as softmax_stage2.
+__device__ __forceinline__ void head_choice(const CView& V, std::size_t bl, std::uint64_t h1l,
+                                            std::uint64_t h1m, int k, int j, int a, const int* soff_s,
+                                            const double* slz) {
   const DevView& d = V.d;
   const int sb = soff_s[j], deg = soff_s[j + 1] - sb;
-  double g[kMaxDeg], pi[kMaxDeg];
+  const double* lz = slz + static_cast<std::size_t>(j) * d.maxdeg;
   const std::uint64_t h2l = rng_prefix2(h1l, static_cast<std::uint64_t>(a));
-  for (int e = 0; e < deg; ++e) g[e] = gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(d.succ[sb + e])));
-  const int ed = softmax_stage2<kMaxDeg>(deg, slz + static_cast<std::size_t>(j) * d.maxdeg, g, d.kinv, pi);
-  const int c = d.succ[sb + ed];
+  int c;
+  if (deg <= kFastDeg) {
+    int sj[kFastDeg];
+    double y[kFastDeg], ex[kFastDeg];
+#pragma unroll
+    for (int e = 0; e < kFastDeg; ++e) sj[e] = d.succ[sb + (e < deg ? e : 0)];
+#pragma unroll
+    for (int e = 0; e < kFastDeg; ++e)
+      y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sj[e])))) * d.kinv;
+    double m2 = y[0];
+#pragma unroll
+    for (int e = 1; e < kFastDeg; ++e)
+      if (e < deg && m2 < y[e]) m2 = y[e];
+    double z2 = 0.0;
+#pragma unroll
+    for (int e = 0; e < kFastDeg; ++e) {
+      ex[e] = exp(y[e] - m2);
+      if (e < deg) z2 += ex[e];
+    }
+    int best = 0;
+    double pb = ex[0] / z2;
+#pragma unroll
+    for (int e = 1; e < kFastDeg; ++e)
+      if (e < deg) {
+        const double pv = ex[e] / z2;
+        if (pv > pb) {
+          pb = pv;
+          best = e;
+        }
+      }
+    c = sj[best];
+  } else {
+    double g[kMaxDeg], pi[kMaxDeg];
+    for (int e = 0; e < deg; ++e) g[e] = gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(d.succ[sb + e])));
+    c = d.succ[sb + softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi)];
+  }
   Cand cd;
   cd.alpha = d.alpha[bl + j];
   cd.g = gumbel_bits(rng_final(rng_prefix2(h1m, static_cast<std::uint64_t>(c)), static_cast<std::uint64_t>(a)));
@@ -59,8 +100,8 @@ __device__ void head_choice(const CView& V, std::size_t bl, std::uint64_t h1l, s
   if (qq < kClusterCandCap) V.cands[(bl + c) * kClusterCandCap + qq] = cd;
 }
 
-__device__ __forceinline__ int find_link_f(const int* off_s, int L, int k) {
-  int lo = 0, hi = L - 1;
+// Link of slot k: the last j in [lo, hi] with off_s[j] <= k.
+__device__ __forceinline__ int find_link_w(const int* off_s, int lo, int hi, int k) {
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (off_s[mid] <= k)
@@ -271,17 +312,39 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
       int* nAc = V.nAb + cur * BL + bl;
       int* qnc = V.qnb + cur * BL + bl;
       double* tailc = V.tailb + cur * BL + bl;
+      // Slot mapping.  Contiguous: this CTA owns [ka, kb) (32-aligned, so no
+      // warp straddles two CTAs) and the link search is narrowed to the links
+      // that range covers.  Interleaved: 512-slot blocks round-robin over the
+      // scenario's CTAs, which spreads dense runs of arrived heads when every
+      // thread owns several slots.
+      int off0, stride, limit, jA = 0, jB = L - 1;
+      if (V.contig) {
+        const int per = ((N + V.cs - 1) / V.cs + 31) & ~31;
+        off0 = min(N, rank * per);
+        limit = min(N, off0 + per);
+        stride = blockDim.x;
+        int* win2 = tmp + 32;
+        if (threadIdx.x == 0) win2[0] = off0 < limit ? find_link_w(offB, 0, L - 1, off0) : 0;
+        if (threadIdx.x == 32) win2[1] = off0 < limit ? find_link_w(offB, 0, L - 1, limit - 1) : 0;
+        __syncthreads();
+        jA = win2[0];
+        jB = win2[1];
+      } else {
+        off0 = rank * blockDim.x;
+        limit = N;
+        stride = nthr;
+      }
       if (V.wstamp) wt1 = gnow();
-      // Each thread owns slots gt0, gt0 + nthr, ...; they are processed kBatch
-      // at a time so the pull loads of several slots are in flight together.
-      for (int k0 = gt0; k0 < N; k0 += kBatch * nthr) {
+      const int lane = threadIdx.x & 31;
+      for (int k0 = off0 + static_cast<int>(threadIdx.x); k0 - lane < limit; k0 += kBatch * stride) {
         int kk[kBatch], jj[kBatch], rr[kBatch], nn[kBatch], aa[kBatch];
         double xx[kBatch], xl[kBatch], xn[kBatch];
 #pragma unroll
         for (int q = 0; q < kBatch; ++q) {  // segment lookup (smem)
-          const int k = k0 + q * nthr;
-          kk[q] = k;
-          const int j = k < N ? find_link_f(offB, L, k) : 0;
+          const int k = k0 + q * stride;
+          const bool on = k < limit;
+          kk[q] = on ? k : N;
+          const int j = on ? find_link_w(offB, jA, jB, k) : 0;
           jj[q] = j;
           rr[q] = k - offB[j];
           nn[q] = offB[j + 1] - offB[j];
@@ -289,8 +352,10 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
 #pragma unroll
         for (int q = 0; q < kBatch; ++q) {  // pull (all loads issued before use)
           const int k = kk[q], j = jj[q], r = rr[q], n = nn[q];
+          // the warp's edge lanes also pull the neighbour outside the warp
+          const bool need_l = !last && lane == 0 && r > 0;
+          const bool need_n = !last && lane == 31 && r + 1 < n;
           xl[q] = 0.0;
-          xn[q] = 0.0;
           if (k >= N) {
             xx[q] = 0.0;
             aa[q] = 0;
@@ -299,19 +364,27 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
           if (t == 0) {
             xx[q] = d.pos[so + k];
             aa[q] = d.aid[so + k];
-            if (r > 0) xl[q] = d.pos[so + k - 1];
-            if (r + 1 < n) xn[q] = d.pos[so + k + 1];
+            if (need_l || need_n) xl[q] = d.pos[so + k + (need_l ? -1 : 1)];
           } else {
-            bool e0, e1 = false, e2 = false;
+            bool e0, e1 = false;
             const int s0 = pull_f(j, r, offA, offB, na_s, dep_s, win_s, wonp, &e0);
-            int s1 = s0, s2 = s0;
-            if (!last && r > 0) s1 = pull_f(j, r - 1, offA, offB, na_s, dep_s, win_s, wonp, &e1);
-            if (!last && r + 1 < n) s2 = pull_f(j, r + 1, offA, offB, na_s, dep_s, win_s, wonp, &e2);
-            const double v0 = x1p[s0], v1 = x1p[s1], v2 = x1p[s2];
+            int s1 = s0;
+            if (need_l || need_n) s1 = pull_f(j, need_l ? r - 1 : r + 1, offA, offB, na_s, dep_s, win_s, wonp, &e1);
+            const double v0 = x1p[s0], v1 = x1p[s1];
             aa[q] = d.aid[sp + s0];
             xx[q] = e0 ? 0.0 : v0;  // entrant: -M + M == 0.0 exactly
             xl[q] = e1 ? 0.0 : v1;
-            xn[q] = e2 ? 0.0 : v2;
+          }
+        }
+        if (!last) {
+          // neighbours in the same link are lanes -+1 of this batch
+#pragma unroll
+          for (int q = 0; q < kBatch; ++q) {
+            const double up = __shfl_up_sync(0xffffffffu, xx[q], 1);
+            const double dn = __shfl_down_sync(0xffffffffu, xx[q], 1);
+            const double edge = xl[q];
+            xl[q] = lane == 0 ? edge : up;
+            xn[q] = lane == 31 ? edge : dn;
           }
         }
         if (t > 0) {
@@ -432,7 +505,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
 }
 
 int fused_smem_bytes(int L, bool stage_params) {
-  return (stage_params ? 3 * L * 8 : 0) + (2 * (L + 1) + 3 * L + 2 * (L + 1) + 32) * 4;
+  return (stage_params ? 3 * L * 8 : 0) + (2 * (L + 1) + 3 * L + 2 * (L + 1) + 36) * 4;
 }
 
 cudaError_t launch_forward_fused(const CView& V, bool cluster, cudaStream_t st) {
