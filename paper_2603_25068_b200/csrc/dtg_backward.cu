@@ -35,6 +35,9 @@ namespace dtg {
 namespace {
 
 constexpr int kBT = 512;  // threads per CTA
+constexpr int kFastDeg = 5;  // successor counts up to this take unrolled register paths
+constexpr int kHeadCap = 1024;  // deferred arrived heads per CTA (overflow runs inline)
+constexpr int kB3 = 2;  // R3 slots per thread in flight
 
 __device__ __forceinline__ int findl(const int* off_s, int L, int k) {
   int lo = 0, hi = L - 1;
@@ -131,6 +134,76 @@ __device__ __forceinline__ void bstamp(const BView& V, int t, int w) {
   }
 }
 
+// Link-choice replay of one arrived head in R1 (pi kept for R4) and its
+// registration as a merge candidate of the chosen row.
+__device__ __forceinline__ void replay_head(const BView& V, int b, int t, int k, int j, int a) {
+  const DevView& d = V.d;
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N, bl = static_cast<std::size_t>(b) * d.L;
+  const int s0 = d.succ_off[j], deg = (V.dbg & 1) ? 0 : d.succ_off[j + 1] - s0;
+  int c = -1;
+  if (deg > 0) {
+    const double* lz = d.slogz + (bl + j) * d.maxdeg;
+    const std::uint64_t h2l =
+        rng_prefix2(rng_prefix1(d.seed_link[b], static_cast<std::uint64_t>(t)), static_cast<std::uint64_t>(a));
+    double* lp = V.lpi + (bn + k) * d.maxdeg;
+    int ed;
+    if (deg <= kFastDeg) {  // unrolled: independent draw chains interleave
+      int sc[kFastDeg];
+      double y[kFastDeg], ex[kFastDeg];
+#pragma unroll
+      for (int e = 0; e < kFastDeg; ++e) sc[e] = d.succ[s0 + (e < deg ? e : 0)];
+#pragma unroll
+      for (int e = 0; e < kFastDeg; ++e)
+        y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sc[e])))) * d.kinv;
+      double m2 = y[0];
+#pragma unroll
+      for (int e = 1; e < kFastDeg; ++e)
+        if (e < deg && m2 < y[e]) m2 = y[e];
+      double z2 = 0.0;
+#pragma unroll
+      for (int e = 0; e < kFastDeg; ++e) {
+        ex[e] = exp(y[e] - m2);
+        if (e < deg) z2 += ex[e];
+      }
+      ed = 0;
+      double pb = ex[0] / z2;
+      lp[0] = pb;
+#pragma unroll
+      for (int e = 1; e < kFastDeg; ++e)
+        if (e < deg) {
+          const double pv = ex[e] / z2;
+          lp[e] = pv;
+          if (pv > pb) {
+            pb = pv;
+            ed = e;
+          }
+        }
+      c = sc[ed];
+    } else {
+      double g[kMaxDeg], pi[kMaxDeg];
+      for (int e = 0; e < deg; ++e) g[e] = gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(d.succ[s0 + e])));
+      ed = softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi);
+      c = d.succ[s0 + ed];
+      for (int e = 0; e < deg; ++e) lp[e] = pi[e];
+    }
+    const double gmc =
+        gumbel_bits(rng_final(rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
+                                          static_cast<std::uint64_t>(c)),
+                              static_cast<std::uint64_t>(a)));
+    V.ched[bn + k] = ed;
+    Cand cd;
+    cd.alpha = d.alpha[bl + j];
+    cd.g = gmc;
+    cd.slot = k;
+    cd.aid = a;
+    cd.link = j;
+    cd.pad = 0;
+    const int qq = atomicAdd(&V.ccnt[bl + c], 1);
+    if (qq < kBwdCandCap) V.cands[(bl + c) * kBwdCandCap + qq] = cd;
+  }
+  V.choice[bn + k] = c;
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
@@ -141,6 +214,8 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
   int* offT = smb;
   int* offN = smb + (L + 1);
   T2* red = reinterpret_cast<T2*>(smb + 2 * (L + 1) + ((2 * (L + 1)) & 1));  // [kBT/32][maxdeg]
+  int* hcnt = reinterpret_cast<int*>(red + (kBT / 32) * d.maxdeg);  // deferred-head count
+  int* hq = hcnt + 4;  // [3][kHeadCap] deferred heads: slot, link, agent
   const bool grouped = V.bps > 0;
   const int b0 = grouped ? blockIdx.x / V.bps : blockIdx.x;
   const int lg = grouped ? blockIdx.x % V.bps : 0;
@@ -186,68 +261,87 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         const std::size_t so = sidx(d, t % d.S, b);
         int* nAc = V.nA_cur + bl;  // nA of layout t (parity slot par)
         int* nAw = V.nAb + static_cast<std::size_t>(par) * d.B * L + bl;
-        for (int k = lg * kBT + tid; k < N; k += nblk * kBT) {
-          const int j = findl(offT, L, k);
-          const int base = offT[j], n = offT[j + 1] - base, r = k - base;
-          const double jam = d.jam[bl + j], dxf = d.dxf[bl + j], len = d.len[j];
-          const double thr = d.thr[j];
-          const double x = d.pos[so + k];
-          const CfPick me = cf_step(x, r == 0 ? d.M : d.pos[so + k - 1] - x, jam, dxf, len);
-          V.x1[bn + k] = me.x1;
-          bool fa_n = false;
-          if (r + 1 < n) {
-            const double xn = d.pos[so + k + 1];
-            fa_n = cf_step(xn, x - xn, jam, dxf, len).x1 >= thr;
+        // several slots per thread: queue the arrived heads in shared memory
+        // and replay their link choices after the slot loop, one per thread
+        const bool defer = N - lg * kBT > nblk * kBT;
+        if (tid == 0) *hcnt = 0;
+        __syncthreads();
+        // kB3 slots per thread in flight; a slot's follower arrival flag is the
+        // next lane's own (lanes are consecutive slots), so only a warp's last
+        // lane replays its follower's car-following itself.
+        const int stride1 = nblk * kBT;
+        for (int k0 = lg * kBT + tid; k0 - lane < N; k0 += kB3 * stride1) {
+          int kk[kB3], jj[kB3], rr[kB3], nn[kB3];
+          double xx[kB3], xp[kB3], xf[kB3];
+#pragma unroll
+          for (int q = 0; q < kB3; ++q) {
+            const int k = k0 + q * stride1;
+            const bool on = k < N;
+            kk[q] = k;
+            const int j = on ? d.lnk[so + k] : 0;
+            jj[q] = j;
+            const int base = offT[j];
+            rr[q] = k - base;
+            nn[q] = offT[j + 1] - base;
+            xx[q] = on ? d.pos[so + k] : 0.0;
+            xp[q] = (on && rr[q] > 0) ? d.pos[so + k - 1] : 0.0;
+            xf[q] = (on && lane == 31 && rr[q] + 1 < nn[q]) ? d.pos[so + k + 1] : 0.0;
           }
-          const bool fa = me.x1 >= thr;
-          if (r == 0 && !fa) {
-            nAw[j] = 0;
-            nAc[j] = 0;
-          }
-          if (fa && !fa_n) {
-            nAw[j] = r + 1;
-            nAc[j] = r + 1;
-          }
-          if (r == n - 1) V.tail[bl + j] = me.x1;
-          if (fa) {
-            V.won[bn + k] = 0;
-            const int a = d.aid[so + k];
-            const int q = atomicAdd(&V.acount[par * d.B + b], 1);
-            V.alist[bn + q] = k;
-            atomicMin(&V.a0key[par * d.B + b],
-                      (static_cast<unsigned long long>(a) << 32) | static_cast<unsigned>(k));
-            const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
-            int c = -1;
-            if (deg > 0) {
-              double g[kMaxDeg], gm[kMaxDeg], pi[kMaxDeg];
-              int sc[kMaxDeg];
-              const double* lz = d.slogz + (bl + j) * d.maxdeg;
-              const std::uint64_t h2l = rng_prefix2(rng_prefix1(d.seed_link[b], static_cast<std::uint64_t>(t)),
-                                                    static_cast<std::uint64_t>(a));
-              for (int e = 0; e < deg; ++e) {
-                sc[e] = d.succ[s0 + e];
-                g[e] = gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sc[e])));
-              }
-              const int ed = softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi);
-              c = sc[ed];
-              gm[ed] = gumbel_bits(rng_final(rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
-                                                         static_cast<std::uint64_t>(c)),
-                                             static_cast<std::uint64_t>(a)));
-              double* lp = V.lpi + (bn + k) * d.maxdeg;
-              for (int e = 0; e < deg; ++e) lp[e] = pi[e];
-              V.ched[bn + k] = ed;
-              Cand cd;
-              cd.alpha = d.alpha[bl + j];
-              cd.g = gm[ed];
-              cd.slot = k;
-              cd.aid = a;
-              cd.link = j;
-              cd.pad = 0;
-              const int qq = atomicAdd(&V.ccnt[bl + c], 1);
-              if (qq < kBwdCandCap) V.cands[(bl + c) * kBwdCandCap + qq] = cd;
+#pragma unroll
+          for (int q = 0; q < kB3; ++q) {
+            const int k = kk[q], j = jj[q], r = rr[q], n = nn[q];
+            const bool on = k < N;
+            bool fa = false, fa_n = false;
+            double x1 = 0.0;
+            if (on) {
+              const double jam = d.jam[bl + j], dxf = d.dxf[bl + j], len = d.len[j];
+              const double thr = d.thr[j];
+              const double x = xx[q];
+              x1 = cf_step(x, r == 0 ? d.M : xp[q] - x, jam, dxf, len).x1;
+              fa = x1 >= thr;
+              if (lane == 31 && r + 1 < n) fa_n = cf_step(xf[q], x - xf[q], jam, dxf, len).x1 >= thr;
             }
-            V.choice[bn + k] = c;
+            const bool fdown = __shfl_down_sync(0xffffffffu, fa, 1);
+            if (!on) continue;
+            if (lane < 31) fa_n = r + 1 < n && fdown;
+            V.x1[bn + k] = x1;
+            if (r == 0 && !fa) {
+              nAw[j] = 0;
+              nAc[j] = 0;
+            }
+            if (fa && !fa_n) {
+              nAw[j] = r + 1;
+              nAc[j] = r + 1;
+            }
+            if (r == n - 1) V.tail[bl + j] = x1;
+            if (fa) {
+              V.won[bn + k] = 0;
+              const int a = d.aid[so + k];
+              if (!(V.dbg & 4)) {
+                const int qa = atomicAdd(&V.acount[par * d.B + b], 1);
+                V.alist[bn + qa] = k;
+                atomicMin(&V.a0key[par * d.B + b],
+                          (static_cast<unsigned long long>(a) << 32) | static_cast<unsigned>(k));
+              }
+              if (defer) {
+                const int hi = atomicAdd(hcnt, 1);
+                if (hi < kHeadCap) {
+                  hq[hi] = k;
+                  hq[kHeadCap + hi] = j;
+                  hq[2 * kHeadCap + hi] = a;
+                } else {
+                  replay_head(V, b, t, k, j, a);
+                }
+              } else {
+                replay_head(V, b, t, k, j, a);
+              }
+            }
           }
+        }
+        if (defer) {
+          __syncthreads();
+          const int nh = min(*hcnt, kHeadCap);
+          for (int i = tid; i < nh; i += kBT) replay_head(V, b, t, hq[i], hq[kHeadCap + i], hq[2 * kHeadCap + i]);
         }
       }
     bstamp(V, t, 1);
@@ -272,7 +366,11 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         double* g5 = V.grads + static_cast<std::size_t>(b) * 5 * L;
         const int* nAn = V.nAb + static_cast<std::size_t>(par ^ 1) * d.B * L + bl;  // layout t+1
         const double* vbn = V.vbar + (static_cast<std::size_t>(par ^ 1) * d.B * N + bn) * d.maxdeg;
-        for (int i = lg * kBT + tid; i < L; i += nblk * kBT) {
+        // the CTA's two halves run concurrently: warps [0, 8) the per-link work,
+        // warps [8, 16) the A[0] row partials over the arrived list
+        constexpr int kHalf = kBT / 2;
+        if (tid < kHalf) {
+        for (int i = lg * kHalf + tid; i < L; i += nblk * kHalf) {
           if (snap_k >= 0 && V.snap_seed)
             V.cbar[bl + i] += V.snap_seed[(static_cast<std::size_t>(b) * V.K + snap_k) * L + i];
           const double cb = V.cbar[bl + i];
@@ -341,6 +439,8 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           }
           (void)sn;
         }
+        } else {
+        const int ta = tid - kHalf, wa = ta >> 5;
         // A[0]'s rows: per-row top-2 over the arrived list
         const unsigned long long key = V.a0key[par * d.B + b];
         const int nA = V.acount[par * d.B + b];
@@ -356,12 +456,35 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           std::uint64_t h2r[kMaxDeg];  // row prefixes of the merge stream
           const std::uint64_t h1m = rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t));
           for (int e = 0; e < deg0; ++e) h2r[e] = rng_prefix2(h1m, static_cast<std::uint64_t>(d.succ[s0 + e]));
-          for (int q = lg * kBT + tid; q < nA; q += nblk * kBT) {
-            const int s = V.alist[bn + q];
-            const int id = d.aid[so + s];
-            for (int e = 0; e < deg0; ++e) {
-              const double g = gumbel_bits(rng_final(h2r[e], static_cast<std::uint64_t>(id)));
-              t2_push(tp[e], (logz + g) * d.kinv, id, s);
+          if (deg0 <= kFastDeg) {  // unrolled rows: independent draw chains interleave
+            T2 tf[kFastDeg];
+            std::uint64_t hf[kFastDeg];
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e) {
+              tf[e] = T2{-INFINITY, -INFINITY, INT_MAX, -1};
+              hf[e] = h2r[e < deg0 ? e : 0];
+            }
+            for (int q = lg * kHalf + ta; q < nA; q += nblk * kHalf) {
+              const int s = V.alist[bn + q];
+              const int id = d.aid[so + s];
+#pragma unroll
+              for (int e = 0; e < kFastDeg; ++e)
+                if (e < deg0) {
+                  const double g = gumbel_bits(rng_final(hf[e], static_cast<std::uint64_t>(id)));
+                  t2_push(tf[e], (logz + g) * d.kinv, id, s);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e)
+              if (e < deg0) tp[e] = tf[e];
+          } else {
+            for (int q = lg * kHalf + ta; q < nA; q += nblk * kHalf) {
+              const int s = V.alist[bn + q];
+              const int id = d.aid[so + s];
+              for (int e = 0; e < deg0; ++e) {
+                const double g = gumbel_bits(rng_final(h2r[e], static_cast<std::uint64_t>(id)));
+                t2_push(tp[e], (logz + g) * d.kinv, id, s);
+              }
             }
           }
           for (int e = 0; e < deg0; ++e) {
@@ -375,15 +498,16 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               y.s1 = __shfl_xor_sync(0xffffffffu, x.s1, o);
               t2_merge(x, y);
             }
-            if (lane == 0) red[wid * d.maxdeg + e] = x;
+            if (lane == 0) red[wa * d.maxdeg + e] = x;
           }
-          __syncthreads();
-          if (tid < deg0) {
-            T2 x = red[tid];
-            for (int w2 = 1; w2 < kBT / 32; ++w2) t2_merge(x, red[w2 * d.maxdeg + tid]);
-            static_cast<T2*>(V.a0part)[(static_cast<std::size_t>(b) * nblk + lg) * d.maxdeg + tid] = x;
+          asm volatile("bar.sync 1, %0;" ::"r"(kHalf) : "memory");  // the A[0] half only
+          if (ta < deg0) {
+            T2 x = red[ta];
+            for (int w2 = 1; w2 < kHalf / 32; ++w2) t2_merge(x, red[w2 * d.maxdeg + ta]);
+            static_cast<T2*>(V.a0part)[(static_cast<std::size_t>(b) * nblk + lg) * d.maxdeg + ta] = x;
           }
-          __syncthreads();
+          asm volatile("bar.sync 1, %0;" ::"r"(kHalf) : "memory");
+        }
         }
       }
     bstamp(V, t, 3);
@@ -516,31 +640,61 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
             }
           }
         }
-        // position adjoint of layout t
-        for (int k = lg * kBT + tid; k < N; k += nblk * kBT) {
-          const int j = findl(offT, L, k);
-          const int base = offT[j], n = offT[j + 1] - base, r = k - base;
-          const double jam = d.jam[bl + j], dxf = d.dxf[bl + j], len = d.len[j];
-          const double x = d.pos[so + k];
-          const CfPick me = cf_step(x, r == 0 ? d.M : d.pos[so + k - 1] - x, jam, dxf, len);
-          const double x1b = x1_bar_p(V, b, k, j, r, me.x1, offT, offN, xbn);
-          const double xpb = d.tg ? x1b : (me.cap ? x1b : 0.0);
-          const double dxcb = me.cong ? xpb : 0.0;
-          const double dxfb = me.cong ? 0.0 : xpb;
-          const double gapb = me.gap >= 0.0 ? dxcb * 1.0 : 0.0;
-          double tb = 0.0;
-          if (r + 1 < n) {
-            const double xf = d.pos[so + k + 1];
-            const CfPick fo = cf_step(xf, x - xf, jam, dxf, len);
-            const double f1b = x1_bar_p(V, b, k + 1, j, r + 1, fo.x1, offT, offN, xbn);
-            const double fpb = d.tg ? f1b : (fo.cap ? f1b : 0.0);
-            const double fcb = fo.cong ? fpb : 0.0;
-            tb += (fo.gap >= 0.0 ? fcb * 1.0 : 0.0) * 1.0;
+        // position adjoint of layout t: kB3 slots per thread in flight; the
+        // follower's headway term is the follower lane's own gap adjoint
+        // (lanes are consecutive slots), so only a warp's last lane evaluates
+        // its follower's x1 adjoint itself.
+        const int stride3 = nblk * kBT;
+        for (int k0 = lg * kBT + tid; k0 - lane < N; k0 += kB3 * stride3) {
+          int kk[kB3], jj[kB3], rr[kB3], nn[kB3];
+          double xx[kB3], xp[kB3], xf[kB3];
+#pragma unroll
+          for (int q = 0; q < kB3; ++q) {
+            const int k = k0 + q * stride3;
+            const bool on = k < N;
+            kk[q] = k;
+            const int j = on ? d.lnk[so + k] : 0;
+            jj[q] = j;
+            const int base = offT[j];
+            rr[q] = k - base;
+            nn[q] = offT[j + 1] - base;
+            xx[q] = on ? d.pos[so + k] : 0.0;
+            xp[q] = (on && rr[q] > 0) ? d.pos[so + k - 1] : 0.0;
+            xf[q] = (on && lane == 31 && rr[q] + 1 < nn[q]) ? d.pos[so + k + 1] : 0.0;
           }
-          if (r > 0) tb += -(gapb * 1.0);
-          xbc[k] = xpb + tb * 1.0;
-          V.cu[bn + k] = (dxfb * d.dt) * 1.0;
-          V.cg[bn + k] = gapb;
+#pragma unroll
+          for (int q = 0; q < kB3; ++q) {
+            const int k = kk[q], j = jj[q], r = rr[q], n = nn[q];
+            const bool on = k < N;
+            double gapb = 0.0, xpb = 0.0, dxfb = 0.0, gnext = 0.0;
+            if (on) {
+              const double jam = d.jam[bl + j], dxf = d.dxf[bl + j], len = d.len[j];
+              const double x = xx[q];
+              const CfPick me = cf_step(x, r == 0 ? d.M : xp[q] - x, jam, dxf, len);
+              const double x1b = x1_bar_p(V, b, k, j, r, me.x1, offT, offN, xbn);
+              xpb = d.tg ? x1b : (me.cap ? x1b : 0.0);
+              const double dxcb = me.cong ? xpb : 0.0;
+              dxfb = me.cong ? 0.0 : xpb;
+              gapb = me.gap >= 0.0 ? dxcb * 1.0 : 0.0;
+              if (lane == 31 && r + 1 < n) {
+                const CfPick fo = cf_step(xf[q], x - xf[q], jam, dxf, len);
+                const double f1b = x1_bar_p(V, b, k + 1, j, r + 1, fo.x1, offT, offN, xbn);
+                const double fpb = d.tg ? f1b : (fo.cap ? f1b : 0.0);
+                const double fcb = fo.cong ? fpb : 0.0;
+                gnext = fo.gap >= 0.0 ? fcb * 1.0 : 0.0;
+              }
+            }
+            const double gdown = __shfl_down_sync(0xffffffffu, gapb, 1);
+            if (lane < 31) gnext = gdown;
+            if (on) {
+              double tb = 0.0;
+              if (r + 1 < n) tb += gnext * 1.0;
+              if (r > 0) tb += -(gapb * 1.0);
+              xbc[k] = xpb + tb * 1.0;
+              V.cu[bn + k] = (dxfb * d.dt) * 1.0;
+              V.cg[bn + k] = gapb;
+            }
+          }
         }
       }
     bstamp(V, t, 5);
@@ -567,42 +721,106 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           if (c < 0) continue;
           const int j = d.lnk[so + s];
           const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
-          double bar[kMaxDeg], pi[kMaxDeg];
           const double* lz = d.slogz + (bl + j) * d.maxdeg;
           const double* lp = V.lpi + (bn + s) * d.maxdeg;
-          for (int e = 0; e < deg; ++e) {
-            bar[e] = 0.0;
-            pi[e] = lp[e];
-          }
           const int ed = V.ched[bn + s];
-          if (V.vac[bl + c] && V.win[bl + c] >= 0) bar[ed] = V.lbar_row[bn + s];
-          if (s == a0s)
-            for (int e = 0; e < deg; ++e) bar[e] += V.lbar_a0[static_cast<std::size_t>(b) * d.maxdeg + e];
-          for (int e = 0; e < deg; ++e)
-            bar[e] = ((bar[e] * 1.0) * 1.0) * (V.vac[bl + d.succ[s0 + e]] ? 1.0 : 0.0);
-          two_softmax_vjp(deg, lz, pi, d.kinv, bar);
-          for (int e = 0; e < deg; ++e) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e];
+          const double lrow = (V.vac[bl + c] && V.win[bl + c] >= 0) ? V.lbar_row[bn + s] : 0.0;
+          const bool hit = V.vac[bl + c] && V.win[bl + c] >= 0;
+          const double* la0 = V.lbar_a0 + static_cast<std::size_t>(b) * d.maxdeg;
+          if (deg <= kFastDeg) {  // registers, same operation order as two_softmax_vjp
+            double bar[kFastDeg], pi[kFastDeg];
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e) {
+              const bool on = e < deg;
+              pi[e] = on ? lp[e] : 0.0;
+              double v = (hit && e == ed) ? lrow : 0.0;
+              if (on && s == a0s) v += la0[e];
+              bar[e] = on ? ((v * 1.0) * 1.0) * (V.vac[bl + d.succ[s0 + e]] ? 1.0 : 0.0) : 0.0;
+            }
+            double dot = 0.0;
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e)
+              if (e < deg) dot += bar[e] * pi[e];
+            double gs = 0.0;
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e)
+              if (e < deg) {
+                bar[e] = (pi[e] * (bar[e] - dot)) * d.kinv;
+                gs += bar[e];
+              }
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e)
+              if (e < deg) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e] - exp(lz[e]) * gs;
+          } else {
+            double bar[kMaxDeg], pi[kMaxDeg];
+            for (int e = 0; e < deg; ++e) {
+              bar[e] = 0.0;
+              pi[e] = lp[e];
+            }
+            if (hit) bar[ed] = lrow;
+            if (s == a0s)
+              for (int e = 0; e < deg; ++e) bar[e] += la0[e];
+            for (int e = 0; e < deg; ++e)
+              bar[e] = ((bar[e] * 1.0) * 1.0) * (V.vac[bl + d.succ[s0 + e]] ? 1.0 : 0.0);
+            two_softmax_vjp(deg, lz, pi, d.kinv, bar);
+            for (int e = 0; e < deg; ++e) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e];
+          }
         }
         // warp per link: u, kappa, alpha for step t
         double* g5 = V.grads + static_cast<std::size_t>(b) * 5 * L;
+        // warp per link for the segment sums (fixed xor tree); the per-link
+        // epilogues (parameter loads, gradient updates, alpha over the arrived
+        // prefix) of up to 32 links then run in parallel, one per lane.
         const int nw = nblk * (kBT / 32);
-        for (int j = lg * (kBT / 32) + wid; j < L; j += nw) {
-          const int base = offT[j], n = offT[j + 1] - base;
-          double ub = 0.0, jb = 0.0;
-          for (int k = base + lane; k < base + n; k += 32) {
-            ub += V.cu[bn + k];
-            jb += -1.0 * V.cg[bn + k];
-          }
+        const int j0w = lg * (kBT / 32) + wid;
+        const int nmine = j0w < L ? (L - 1 - j0w) / nw + 1 : 0;
+        for (int i0 = 0; i0 < nmine; i0 += 32) {
+          int my_j = -1;
+          double my_ub = 0.0, my_jb = 0.0;
+          const int cnt = min(32, nmine - i0);
+          // software pipeline: the next link's first 32 elements load while
+          // this link reduces
+          int jn = j0w + i0 * nw;
+          int bsn = offT[jn], nsn = offT[jn + 1] - bsn;
+          double pcu = lane < nsn ? V.cu[bn + bsn + lane] : 0.0;
+          double pcg = lane < nsn ? V.cg[bn + bsn + lane] : 0.0;
+          for (int u = 0; u < cnt; ++u) {
+            const int j = jn, base = bsn, n = nsn;
+            const double cu0 = pcu, cg0 = pcg;
+            if (u + 1 < cnt) {
+              jn = j + nw;
+              bsn = offT[jn];
+              nsn = offT[jn + 1] - bsn;
+              pcu = lane < nsn ? V.cu[bn + bsn + lane] : 0.0;
+              pcg = lane < nsn ? V.cg[bn + bsn + lane] : 0.0;
+            }
+            double ub = 0.0, jb = 0.0;
+            if (lane < n) {
+              ub += cu0;
+              jb += -1.0 * cg0;
+            }
+            for (int k = base + 32 + lane; k < base + n; k += 32) {
+              ub += V.cu[bn + k];
+              jb += -1.0 * V.cg[bn + k];
+            }
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            ub += __shfl_xor_sync(0xffffffffu, ub, o);
-            jb += __shfl_xor_sync(0xffffffffu, jb, o);
+            for (int o = 16; o > 0; o >>= 1) {
+              ub += __shfl_xor_sync(0xffffffffu, ub, o);
+              jb += __shfl_xor_sync(0xffffffffu, jb, o);
+            }
+            if (lane == u) {
+              my_j = j;
+              my_ub = ub;
+              my_jb = jb;
+            }
           }
-          if (lane == 0) {
+          if (my_j >= 0) {
+            const int j = my_j;
+            const int base = offT[j], n = offT[j + 1] - base;
             const double kap = d.kappa[bl + j];
             if (n) {
-              g5[j] += 0.0 + ub;
-              g5[L + j] += 0.0 - jb * static_cast<double>(d.delta_n) / (kap * kap);
+              g5[j] += 0.0 + my_ub;
+              g5[L + j] += 0.0 - my_jb * static_cast<double>(d.delta_n) / (kap * kap);
             }
             double ab = 0.0;
             if (n) {
@@ -657,7 +875,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
 }
 
 int backward_smem_bytes(int L, int maxdeg) {
-  return (2 * (L + 1) + 2) * 4 + (kBT / 32) * maxdeg * static_cast<int>(sizeof(T2)) + 16;
+  return (2 * (L + 1) + 2) * 4 + (kBT / 32) * maxdeg * static_cast<int>(sizeof(T2)) + 16 + (4 + 3 * kHeadCap) * 4;
 }
 
 int backward_max_grid(int L, int maxdeg) {

@@ -48,6 +48,7 @@ struct BView {
   const double* x_seed;     // [B][N]
   unsigned long long* sort_scratch;  // [B][maxdeg][N]
   int K, spi, T, bps, force_slow;
+  int dbg;  // timing experiments only (dtg_set_flag 2): bits skip parts of R1
   unsigned long long* tstamp;  // optional [T][grid][8] phase timestamps
 };
 

@@ -126,7 +126,8 @@ struct dtg_ctx {
   DevBuf<double> srec;
   DevBuf<unsigned int> gbar;
   bool custom_barrier = true;
-  int contig_mode = -1;  // -1 auto, 0 interleaved, 1 contiguous (fused forward slot mapping)
+  int contig_mode = -1;
+  int bwd_dbg = 0;  // timing experiments only  // -1 auto, 0 interleaved, 1 contiguous (fused forward slot mapping)
   bool want_wstamp = false;
   DevBuf<unsigned long long> wst;
   DevBuf<dtg::Cand> cands;
@@ -539,6 +540,9 @@ int dtg_set_flag(dtg_ctx* c, int flag, int value) {
   switch (flag) {
     case 0:  // grid barrier: 1 release/acquire counter (default), 0 cooperative_groups grid.sync
       c->custom_barrier = value != 0;
+      return DTG_OK;
+    case 2:  // reverse-sweep timing experiments (results invalid when nonzero)
+      c->bwd_dbg = value;
       return DTG_OK;
     case 1:  // fused forward slot mapping: -1 auto, 0 interleaved, 1 contiguous
       c->contig_mode = value < 0 ? -1 : (value ? 1 : 0);
@@ -957,6 +961,7 @@ static void run_backward_persistent(dtg_ctx* c, cudaStream_t st) {
   V.T = T;
   V.bps = bps;
   V.force_slow = c->force_slow;
+  V.dbg = c->bwd_dbg;
   V.tstamp = nullptr;
   if (c->want_stamps) {
     c->stamps.ensure(static_cast<std::size_t>(T) * grid * 8);

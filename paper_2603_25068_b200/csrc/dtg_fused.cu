@@ -35,6 +35,7 @@ namespace dtg {
 namespace {
 
 constexpr int kBatch = 4;   // slots per thread in flight together
+constexpr int kHeadCap = 1024;  // deferred arrived heads per CTA (overflow runs inline)
 
 constexpr int kFastDeg = 5;  // successor counts up to this take the unrolled head path
 
@@ -243,6 +244,8 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
   int* soff_s = win_s + L;  // succ_off, L + 1
   int* poff_s = soff_s + (L + 1);  // pred_off, L + 1
   int* tmp = poff_s + (L + 1);
+  int* hcnt = tmp + 34;              // deferred-head count
+  int* hq = tmp + 36;                // [3][kHeadCap] deferred heads: slot, link, agent
   const int bb = active ? b : 0;
   const std::size_t bl = static_cast<std::size_t>(bb) * L;
   const std::size_t bn = static_cast<std::size_t>(bb) * N;
@@ -334,6 +337,14 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
         limit = N;
         stride = nthr;
       }
+      // When a thread owns several slot batches, arrived heads are queued in
+      // shared memory and their link choices run after the loop, one per
+      // thread, instead of serialising a draw chain into every batch.
+      const bool defer = limit - off0 > stride;
+      if (defer) {
+        if (threadIdx.x == 0) *hcnt = 0;
+        __syncthreads();
+      }
       if (V.wstamp) wt1 = gnow();
       const int lane = threadIdx.x & 31;
       for (int k0 = off0 + static_cast<int>(threadIdx.x); k0 - lane < limit; k0 += kBatch * stride) {
@@ -424,8 +435,23 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
           if (!fa) continue;
           ++n_arr;
           wonc[k] = 0;
-          if (soff_s[j + 1] > soff_s[j]) head_choice(V, bl, h1l, h1m, k, j, aa[q], soff_s, slz);
+          if (soff_s[j + 1] > soff_s[j]) {
+            const int hi = defer ? atomicAdd(hcnt, 1) : kHeadCap;
+            if (hi < kHeadCap) {
+              hq[hi] = k;
+              hq[kHeadCap + hi] = j;
+              hq[2 * kHeadCap + hi] = aa[q];
+            } else {
+              head_choice(V, bl, h1l, h1m, k, j, aa[q], soff_s, slz);
+            }
+          }
         }
+      }
+      if (defer && !last) {
+        __syncthreads();
+        const int nh = min(*hcnt, kHeadCap);
+        for (int i = threadIdx.x; i < nh; i += blockDim.x)
+          head_choice(V, bl, h1l, h1m, hq[i], hq[kHeadCap + i], hq[2 * kHeadCap + i], soff_s, slz);
       }
     }
     if (V.wstamp && active && !last) {
@@ -505,7 +531,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
 }
 
 int fused_smem_bytes(int L, bool stage_params) {
-  return (stage_params ? 3 * L * 8 : 0) + (2 * (L + 1) + 3 * L + 2 * (L + 1) + 36) * 4;
+  return (stage_params ? 3 * L * 8 : 0) + (2 * (L + 1) + 3 * L + 2 * (L + 1) + 36 + 3 * kHeadCap) * 4;
 }
 
 cudaError_t launch_forward_fused(const CView& V, bool cluster, cudaStream_t st) {
