@@ -284,7 +284,7 @@ def run_ours(args):
     single_rtf = SIM_SECONDS / (dev_s / args.steps)
 
     # roofline of the production kernel: one persistent cooperative launch per
-    # nowcast (k_forward_persistent); its duration is the event-timed device
+    # nowcast (k_forward_fused); its duration is the event-timed device
     # time above.  Algorithmic bytes: SURVEY §8d forward figure, 16 B per
     # agent-step + 64 B per link-step, x T steps x B scenarios.
     per_launch_s = dev_s / args.steps
@@ -293,8 +293,8 @@ def run_ours(args):
     achieved = alg_bytes / per_launch_s / 1e9
     phases, grid = eng.profile_persistent(T_STEPS, SPI)
     ker_ms, _ = eng.profile_kernels(T_STEPS, SPI)  # the 4-kernel schedule, for reference
-    roofline = {"bound": "hbm", "kernel": "k_forward_persistent", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic("k_forward_persistent"),
+    roofline = {"bound": "hbm", "kernel": "k_forward_fused", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic("k_forward_fused"),
                 "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes,
                 "avg_launch_us": per_launch_s * 1e6, "share_of_step": 1.0, "grid_ctas": grid,
                 "phase_us_per_engine_step": {k: round(v, 2) for k, v in phases.items()},
@@ -360,12 +360,31 @@ def run_ours(args):
     return out
 
 
-def run_throughput(P, torch, sc, p, lk0, ps0, args, B=64):
-    """Batched nowcasts on one GPU (independent draws): where HBM bandwidth
-    starts to matter (roofline meaningful for B >= 256 / dn = 1)."""
+def run_throughput(P, torch, sc, p, lk0, ps0, args):
+    """Where HBM bandwidth starts to matter (SURVEY §8d asks for the roofline
+    fraction of (i) C3 at dn=1 and (ii) batched C3 with B >= 256): batched
+    independent draws of the C3 nowcast on one GPU, and the 1,000,020-agent
+    dn=1 variant of the same network (3,600 steps = 1 h).  Device time by CUDA
+    events; no L2 flush (B=256 state ~140 MB exceeds L2; dn=1 state ~50 MB
+    stays L2-resident, which the note records)."""
     N, L = sc.n_agents, sc.n_links
+    peak = measured_peak_hbm()[0]
     out = {}
-    for mode, name in ((0, "persistent grid"), (3, "4-kernel step graph")):
+
+    def timed(eng, T, spi, reps=3):
+        st = torch.cuda.current_stream()
+        for _ in range(2):
+            eng.forward(T, spi)
+        eng.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            eng.forward(T, spi)
+        e1.record(st)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps / 1e3
+
+    for B, mode in ((64, 0), (64, 3), (256, 0)):
         eng = P.Engine(sc, n_scenarios=B, max_steps=T_STEPS)
         eng.set_stream(torch.cuda.current_stream().cuda_stream)
         eng.set_mode(mode)
@@ -373,21 +392,32 @@ def run_throughput(P, torch, sc, p, lk0, ps0, args, B=64):
         eng.set_state(lk0, ps0)
         for b in range(B):
             eng.set_noise(SIM_SEED, 1000 + b, b)
-        for _ in range(2):
-            eng.forward(T_STEPS, SPI)
-        eng.sync()
-        st = torch.cuda.current_stream()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        for _ in range(3):
-            eng.forward(T_STEPS, SPI)
-        e1.record(st)
-        torch.cuda.synchronize()
-        s = e0.elapsed_time(e1) / 3 / 1e3
+        s = timed(eng, T_STEPS, SPI)
         alg = B * T_STEPS * (16 * N + 64 * L)
-        out[name] = {"scenarios": B, "ms_per_batch": s * 1e3, "rtf_aggregate": B * SIM_SECONDS / s,
-                     "alg_GBps": alg / s / 1e9}
+        out[f"c3_dn30_B{B}_mode{mode}"] = {
+            "scenarios": B, "schedule": {2: "fused persistent grid", 3: "4-kernel step graph"}.get(
+                eng.last_mode // 100, str(eng.last_mode)),
+            "ms_per_batch": s * 1e3, "rtf_aggregate": B * SIM_SECONDS / s,
+            "alg_GBps": alg / s / 1e9, "hbm_frac": alg / s / 1e9 / peak}
         del eng
+    # C3 at dn = 1: 1,000,020 agents, 3,600 steps
+    sc1 = P.Scenario.grid(GRID_N, LINK_LEN, NET_SEED, VIRT_LEN).configure(VEHICLES, 1, 3600, OBS_S)
+    p1 = sc1.sample_parameters(PARAM_SEED)
+    l1, q1 = sc1.seed_agents()
+    eng = P.Engine(sc1, n_scenarios=1, max_steps=3600)
+    eng.set_stream(torch.cuda.current_stream().cuda_stream)
+    eng.set_params(p1)
+    eng.set_state(l1, q1)
+    eng.set_noise(SIM_SEED, 0, 0)
+    s = timed(eng, 3600, sc1.steps_per_interval, reps=2)
+    N1 = sc1.n_agents
+    alg = 3600 * (16 * N1 + 64 * L)
+    out["c3_dn1_B1"] = {"agents": N1, "steps": 3600, "ms_per_nowcast": s * 1e3, "rtf": SIM_SECONDS / s,
+                        "us_per_step": s / 3600 * 1e6, "alg_GBps": alg / s / 1e9, "hbm_frac": alg / s / 1e9 / peak,
+                        "schedule": eng.last_mode,
+                        "note": "16 MB/step of algorithmic traffic against a ~50 MB working set that stays "
+                                "L2-resident; latency/issue-bound (profiles/r01/ncu_fused_dn1_summary.md)"}
+    del eng
     return out
 
 
@@ -419,12 +449,16 @@ def run_gradient(P, torch, world, rank, args):
 
     run(2)  # warm-up: context, graphs, loss buffers
     n_it = max(5, args.steps)
-    barrier(world)
-    torch.cuda.synchronize()
-    t = time.perf_counter()
-    res = run(n_it)
-    torch.cuda.synchronize()
-    s_iter = max_over_ranks((time.perf_counter() - t) / n_it, world)
+    walls = []
+    for n in (n_it, 2 * n_it):  # per-call setup (seeding, state upload) cancels in the difference
+        barrier(world)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        res = run(n)
+        torch.cuda.synchronize()
+        walls.append(max_over_ranks(time.perf_counter() - t, world))
+    s_iter = (walls[1] - walls[0]) / n_it
+    setup_s = walls[0] - n_it * s_iter
     # device time of the two passes (CUDA events on the engine's stream)
     local = CAL_DRAWS // world
     eng = P.Engine(sc, n_scenarios=local, max_steps=T)
@@ -450,16 +484,19 @@ def run_gradient(P, torch, world, rank, args):
     phases_f, _ = eng.profile_persistent(T, SPI)
     eng.forward(T, SPI, checkpoint=True)
     phases_b, grid_b = eng.profile_backward()
-    return {"s_per_iter": s_iter, "draws": CAL_DRAWS, "draws_per_gpu": local, "steps": T,
+    return {"s_per_iter": s_iter, "setup_s_per_calibrate_call": setup_s,
+            "wall_s": {f"{n_it}_it": walls[0], f"{2 * n_it}_it": walls[1]},
+            "draws": CAL_DRAWS, "draws_per_gpu": local, "steps": T,
             "iterations_timed": n_it, "params": 4 * L, "loss_first": float(res.loss_curve[0]),
             "loss_last": float(res.loss_curve[-1]),
-            "projected_200_iter_s": 200 * s_iter,
+            "projected_200_iter_s": 200 * s_iter + setup_s,
             "paper_calibration_s": 455.3,
             "fwd_ckpt_ms_per_pass": statistics.median(fwd_ms), "adj_ms_per_pass": statistics.median(adj_ms),
             "fwd_phase_us_per_step": {k: round(x, 2) for k, x in phases_f.items()},
             "adj_phase_us_per_step": {k: round(x, 2) for k, x in phases_b.items()},
             "timing": "wall clock per calibrate() iteration through the public API (device loss/seeds/draw sum, "
-                      "NCCL row gather for N>1, host transform + AdamW, 1 sync per iteration)"}
+                      "NCCL row gather for N>1, host transform + AdamW, 1 sync per iteration): difference of "
+                      "a 2n- and an n-iteration calibrate call / n; the per-call setup is reported separately"}
 
 
 # ---- reference arm -----------------------------------------------------------------------

@@ -39,6 +39,7 @@ struct CView {
   unsigned int* gbar;  // grid-barrier counter (null: cooperative_groups grid.sync)
   unsigned long long* wstamp;  // optional per-warp slot-phase record [T][warps][4]
   int contig;          // 1: contiguous slot range per CTA, 0: interleaved 512-slot blocks
+  int ckpt;            // keep every layout (else positions/links of the final one only)
 };
 
 void launch_pack_succ(const DevView& d, double* srec, cudaStream_t st);

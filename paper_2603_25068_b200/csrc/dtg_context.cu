@@ -752,6 +752,7 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       V.cands = c->cands.p;
       V.srec = c->srec.p;
       V.T = T;
+      V.ckpt = checkpoint ? 1 : 0;
       V.stage_params = c->stage_params ? 1 : 0;
       V.tstamp = nullptr;
       V.gbar = c->custom_barrier ? c->gbar.p : nullptr;
@@ -858,7 +859,7 @@ int dtg_read_state(dtg_ctx* c, int scenario, int step, int* link, double* pos) {
     const int T = c->last_T;
     if (T < 0) throw std::runtime_error("no forward run");
     if (step < 0) step = T;
-    if (step > T || (!c->last_ckpt && step < T - 1))
+    if (step > T || (!c->last_ckpt && step < T))
       throw std::invalid_argument("step not kept (run dtg_forward with checkpoint=1)");
     const dtg::DevView d = c->view();
     dtg::launch_gather_state(d, step % c->S, c->tmp_link.p, c->tmp_pos.p, c->stream);

@@ -400,11 +400,13 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
         }
         if (t > 0) {
 #pragma unroll
-          for (int q = 0; q < kBatch; ++q)  // checkpoint of layout t
+          for (int q = 0; q < kBatch; ++q)  // layout t (ids feed the next pull)
             if (kk[q] < N) {
-              d.pos[so + kk[q]] = xx[q];
               d.aid[so + kk[q]] = aa[q];
-              d.lnk[so + kk[q]] = jj[q];
+              if (V.ckpt || last) {  // positions / links: checkpoints and the final state only
+                d.pos[so + kk[q]] = xx[q];
+                d.lnk[so + kk[q]] = jj[q];
+              }
             }
         }
         if (last) continue;
