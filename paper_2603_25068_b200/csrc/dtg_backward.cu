@@ -51,6 +51,14 @@ __device__ __forceinline__ int findl(const int* off_s, int L, int k) {
   return lo;
 }
 
+// Item index of thread `tid` of the scenario's CTA `lg` (of nblk): 32-item
+// groups are dealt round-robin over the CTAs first, so a short item list
+// (links, arrived agents) spreads over all SMs instead of filling the first
+// CTAs' schedulers.  Stride: nblk * (threads per CTA taking part).
+__device__ __forceinline__ int spread(int tid, int lg, int nblk) {
+  return ((tid >> 5) * nblk + lg) * 32 + (tid & 31);
+}
+
 __device__ __forceinline__ double adm_bar(double xb, double x1, double M) {
   double r = 0.0;
   r += xb * (-M);
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         // warps [8, 16) the A[0] row partials over the arrived list
         constexpr int kHalf = kBT / 2;
         if (tid < kHalf) {
-        for (int i = lg * kHalf + tid; i < L; i += nblk * kHalf) {
+        for (int i = spread(tid, lg, nblk); i < L; i += nblk * kHalf) {
           if (snap_k >= 0 && V.snap_seed)
             V.cbar[bl + i] += V.snap_seed[(static_cast<std::size_t>(b) * V.K + snap_k) * L + i];
           const double cb = V.cbar[bl + i];
@@ -464,7 +472,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               tf[e] = T2{-INFINITY, -INFINITY, INT_MAX, -1};
               hf[e] = h2r[e < deg0 ? e : 0];
             }
-            for (int q = lg * kHalf + ta; q < nA; q += nblk * kHalf) {
+            for (int q = spread(ta, lg, nblk); q < nA; q += nblk * kHalf) {
               const int s = V.alist[bn + q];
               const int id = d.aid[so + s];
 #pragma unroll
@@ -478,7 +486,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
             for (int e = 0; e < kFastDeg; ++e)
               if (e < deg0) tp[e] = tf[e];
           } else {
-            for (int q = lg * kHalf + ta; q < nA; q += nblk * kHalf) {
+            for (int q = spread(ta, lg, nblk); q < nA; q += nblk * kHalf) {
               const int s = V.alist[bn + q];
               const int id = d.aid[so + s];
               for (int e = 0; e < deg0; ++e) {
@@ -531,7 +539,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         const double* xbn = V.xbar + static_cast<std::size_t>(par ^ 1) * d.B * N + bn;
         double* xbc = V.xbar + static_cast<std::size_t>(par) * d.B * N + bn;
         // merge rows
-        for (int i = lg * kBT + tid; i < L; i += nblk * kBT) {
+        for (int i = spread(tid, lg, nblk); i < L; i += nblk * kBT) {
           const int w = V.win[bl + i];
           if (w < 0) continue;
           const int cnt = V.ccnt[bl + i];
@@ -715,7 +723,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         const unsigned long long key = V.a0key[par * d.B + b];
         const int a0s = key == ULLONG_MAX ? -1 : static_cast<int>(key & 0xffffffffull);
         const int nA = V.acount[par * d.B + b];
-        for (int q = lg * kBT + tid; q < nA; q += nblk * kBT) {
+        for (int q = spread(tid, lg, nblk); q < nA; q += nblk * kBT) {
           const int s = V.alist[bn + q];
           const int c = V.choice[bn + s];
           if (c < 0) continue;

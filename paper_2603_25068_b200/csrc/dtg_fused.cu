@@ -483,7 +483,10 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
       const double* chp = d.cumh + hidx(d, t, bb);
       double* qhn = d.qh + hidx(d, t + 1, bb);
       double* chn = d.cumh + hidx(d, t + 1, bb);
-      for (int i = gt0; i < L; i += nthr) {
+      // links in 32-lane groups dealt round-robin over the CTAs first, so the
+      // ~L/32 busy warps land on different SMs instead of filling the first few
+      const int gw0 = (static_cast<int>(threadIdx.x) >> 5) * V.cs + rank;
+      for (int i = gw0 * 32 + (threadIdx.x & 31); i < L; i += nthr) {
         const int n_i = offB[i + 1] - offB[i];
         const int cnt = V.ccnt[bl + i];
         const int qc = n_i ? qnc[i] : 0;
