@@ -27,6 +27,7 @@
 
 #include "dtg_backward.h"
 #include "dtg_device.cuh"
+#include "dtg_merge.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -390,11 +391,26 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           const double tx = n_i ? V.tail[bl + i] : d.M;
           const bool vacant = tx > d.jam[bl + i];
           V.vac[bl + i] = vacant;
-          const int cnt = V.ccnt[bl + i];
+          const int cnt = (V.dbg & 8) ? 0 : V.ccnt[bl + i];
           int w = -1;
           if (vacant && cnt > 0) {
             if (cnt > kBwdCandCap) {
               atomicOr(&d.err[b], kErrCandOverflow);
+            } else if (cnt <= kFastDeg) {  // registers (dtg_merge.cuh)
+              Cand c[kFastDeg];
+              double lz[kFastDeg], pi[kFastDeg];
+              const int best = merge_softmax_fast<kFastDeg>(cnt, V.cands + (bl + i) * kBwdCandCap, d.kinv, c, lz, pi);
+#pragma unroll
+              for (int e = 0; e < kFastDeg; ++e)
+                if (e < cnt) {
+                  V.cands[(bl + i) * kBwdCandCap + e] = c[e];
+                  V.mpi[(bl + i) * kBwdCandCap + e] = pi[e];
+                  V.mlz[(bl + i) * kBwdCandCap + e] = lz[e];
+                }
+              const Cand cb = pick_cand(c, best);
+              w = cb.slot;
+              V.won[bn + w] = 1;
+              atomicAdd(&V.dep[bl + cb.link], 1);
             } else {
               Cand c[kBwdCandCap];
               for (int e = 0; e < cnt; ++e) c[e] = V.cands[(bl + i) * kBwdCandCap + e];
@@ -425,21 +441,45 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           }
           V.win[bl + i] = w;
           // deferred: preference gradient of step t+1 (its link-choice VJPs are ready)
-          if (t + 1 < T) {
+          if (t + 1 < T && !(V.dbg & 16)) {
             double pb = 0.0;
-            const int e0 = d.pred_off[i], ne = min(d.pred_off[i + 1] - e0, kMaxDeg);
-            int pp[kMaxDeg], pps[kMaxDeg];
-            for (int q = 0; q < ne; ++q) {  // independent loads first
-              pp[q] = d.pred[e0 + q];
-              pps[q] = d.pred_pos[e0 + q];
-            }
-            for (int q = 0; q < ne; ++q) {
-              const int p = pp[q];
-              const int pbse = offN[p];
-              if (offN[p + 1] == pbse) continue;
-              const int nap = nAn[p];
-              for (int r = 0; r < nap; ++r)
-                pb += vbn[static_cast<std::size_t>(pbse + r) * d.maxdeg + pps[q]] * 1.0;
+            const int e0 = d.pred_off[i], ne = d.pred_off[i + 1] - e0;
+            if (ne <= kFastDeg) {
+              // every predecessor's arrived count and first row load together;
+              // the sum then runs in (predecessor, row) order
+              int pbse[kFastDeg], nap[kFastDeg], pps[kFastDeg];
+              double v0[kFastDeg];
+#pragma unroll
+              for (int q = 0; q < kFastDeg; ++q) {
+                nap[q] = 0;
+                pbse[q] = 0;
+                pps[q] = 0;
+                if (q < ne) {
+                  const int p = d.pred[e0 + q];
+                  pps[q] = d.pred_pos[e0 + q];
+                  pbse[q] = offN[p];
+                  nap[q] = offN[p + 1] == pbse[q] ? 0 : nAn[p];
+                }
+              }
+#pragma unroll
+              for (int q = 0; q < kFastDeg; ++q)
+                v0[q] = nap[q] > 0 ? vbn[static_cast<std::size_t>(pbse[q]) * d.maxdeg + pps[q]] : 0.0;
+#pragma unroll
+              for (int q = 0; q < kFastDeg; ++q)
+                if (nap[q] > 0) {
+                  pb += v0[q] * 1.0;
+                  for (int r = 1; r < nap[q]; ++r)
+                    pb += vbn[static_cast<std::size_t>(pbse[q] + r) * d.maxdeg + pps[q]] * 1.0;
+                }
+            } else {
+              for (int q = 0; q < ne; ++q) {
+                const int p = d.pred[e0 + q];
+                const int pbse = offN[p];
+                if (offN[p + 1] == pbse) continue;
+                const int nap = nAn[p];
+                for (int r = 0; r < nap; ++r)
+                  pb += vbn[static_cast<std::size_t>(pbse + r) * d.maxdeg + d.pred_pos[e0 + q]] * 1.0;
+              }
             }
             const double cst = d.cost[bl + i], be = d.beta[bl + i];
             g5[2 * L + i] += 0.0 + pb / cst;
@@ -452,7 +492,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         // A[0]'s rows: per-row top-2 over the arrived list
         const unsigned long long key = V.a0key[par * d.B + b];
         const int nA = V.acount[par * d.B + b];
-        if (key != ULLONG_MAX) {
+        if (key != ULLONG_MAX && !(V.dbg & 32)) {
           const int a0s = static_cast<int>(key & 0xffffffffull);
           const int c0 = d.lnk[so + a0s];
           const int s0 = d.succ_off[c0], deg0 = d.succ_off[c0 + 1] - s0;
@@ -544,8 +584,58 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           if (w < 0) continue;
           const int cnt = V.ccnt[bl + i];
           const Cand* cc = V.cands + (bl + i) * kBwdCandCap;
-          double bar[kBwdCandCap], lz[kBwdCandCap], pi[kBwdCandCap];
           const double abar_w = xbn[offN[i + 1] - 1] * d.M + 0.0;
+          if (cnt <= kFastDeg) {  // registers; two_softmax_vjp's operation order
+            Cand cf[kFastDeg];
+            double bar[kFastDeg], lz[kFastDeg], pi[kFastDeg];
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e) {
+              bar[e] = 0.0;
+              lz[e] = 0.0;
+              pi[e] = 0.0;
+              if (e < cnt) {
+                cf[e] = cc[e];
+                lz[e] = V.mlz[(bl + i) * kBwdCandCap + e];
+                pi[e] = V.mpi[(bl + i) * kBwdCandCap + e];
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e)
+              if (e < cnt) {
+                const int s = cf[e].slot;
+                if (s == w) {
+                  bar[e] = abar_w * 1.0;
+                } else {
+                  const int p = cf[e].link;
+                  const int base = offT[p];
+                  int dd = 0;
+                  for (int q = base; q < s; ++q) dd += V.won[bn + q];
+                  const double xb = xbn[offN[p] + (s - base) - dd];
+                  bar[e] = adm_bar(xb, V.x1[bn + s], d.M) * 1.0;
+                }
+              }
+            double dot = 0.0;
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e)
+              if (e < cnt) dot += bar[e] * pi[e];
+            double gs = 0.0;
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e)
+              if (e < cnt) {
+                bar[e] = (pi[e] * (bar[e] - dot)) * d.kinv;
+                gs += bar[e];
+              }
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e)
+              if (e < cnt) {
+                const double bv = bar[e] - exp(lz[e]) * gs;
+                const int s = cf[e].slot;
+                V.lbar_row[bn + s] = (e == 0 ? 0.0 + abar_w : 0.0) + bv * cf[e].alpha;
+                V.prio_bar[bn + s] = 0.0 + bv * 1.0;
+              }
+            continue;
+          }
+          double bar[kBwdCandCap], lz[kBwdCandCap], pi[kBwdCandCap];
           for (int e = 0; e < cnt; ++e) {
             lz[e] = V.mlz[(bl + i) * kBwdCandCap + e];
             pi[e] = V.mpi[(bl + i) * kBwdCandCap + e];

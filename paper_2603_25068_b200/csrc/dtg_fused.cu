@@ -27,6 +27,7 @@
 
 #include "dtg_cluster.h"
 #include "dtg_device.cuh"
+#include "dtg_merge.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -503,6 +504,18 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
         if (vacant && cnt > 0) {
           if (cnt > kClusterCandCap) {
             atomicOr(&d.err[bb], kErrCandOverflow);
+          } else if (cnt <= kFastDeg) {  // registers (dtg_merge.cuh)
+            Cand c[kFastDeg];
+            double lz[kFastDeg], pi[kFastDeg];
+            const int best = merge_softmax_fast<kFastDeg>(cnt, V.cands + (bl + i) * kClusterCandCap, d.kinv, c,
+                                                          lz, pi);
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e)
+              if (e < cnt && c[e].alpha == 0.0) atomicOr(&d.err[bb], kErrZeroAlpha);
+            const Cand cb = pick_cand(c, best);
+            w = cb.slot;
+            wonc[w] = 1;
+            atomicAdd(&depc[cb.link], 1);
           } else {
             Cand c[kClusterCandCap];
             for (int e = 0; e < cnt; ++e) c[e] = V.cands[(bl + i) * kClusterCandCap + e];

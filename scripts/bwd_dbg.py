@@ -8,7 +8,7 @@ sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 30, T, 300)
 p = sc.sample_parameters(3); lk, ps = sc.seed_agents()
 e = P.Engine(sc, B, T); e.set_params(p); e.set_state(lk, ps)
 for b in range(B): e.set_noise(7, b + 1, b)
-for dbg in (0, 1, 2, 4, 7):
+for dbg in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else "0,1,2,4,7".split(","))]:
     e.set_flag(2, dbg)
     e.forward(T, sc.steps_per_interval, checkpoint=True)
     ph, g = e.profile_backward()
