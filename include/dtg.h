@@ -383,6 +383,31 @@ int dtg_mse_loss(int k_snap, int n_links, const double* snapshots, int n_obs,
                  int delta_n, double* loss, double* seeds);
 const char* dtg_scenario_last_error(const dtg_scenario* sc);
 
+/* ---- Observation / output side -------------------------
+ * Host-only helpers on count series (values [k][n] row-major, one row per
+ * observation interval).  Errors: dtg_observe_last_error(). */
+const char* dtg_observe_last_error(void);
+/* synthesize_observations (observation.cpp:46-83): m_out = floor(coverage*n)
+ * observed links (ascending position) into obs_ids[n] / obs_values[k][m]. */
+int dtg_synthesize_observations(int k, int n, const int* link_ids,
+                                const double* values, int interval_s,
+                                double noise_frac, double coverage,
+                                uint64_t root_seed, int* m_out, int* obs_ids,
+                                double* obs_values);
+/* count_metrics (optimization.cpp:297-336). */
+int dtg_count_metrics(int k_sim, int n_sim, const int* sim_ids,
+                      const double* sim_values, int k_truth, int n_truth,
+                      const int* truth_ids, const double* truth_values,
+                      double* mae, double* pearson_r, int* r_defined,
+                      int* n_pairs);
+/* series_to_csv (pipeline.cpp:113-127), byte-identical; buf NULL: *len only. */
+int dtg_series_to_csv(int k, int n, const int* ids, const double* values,
+                      int interval_s, char* buf, size_t cap, size_t* len);
+/* series_from_csv (pipeline.cpp:129-160); ids/values NULL: sizes only. */
+int dtg_series_from_csv(const char* text, int* k, int* n, int* interval_s,
+                        int* ids, double* values, size_t cap_ids,
+                        size_t cap_values);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,6 +12,7 @@
 #include <functional>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../paper_2603_25068_b200/csrc/dtg_rng.h"
@@ -299,6 +300,27 @@ struct ControlResult {
 ControlResult optimize_control(const Scenario& s, const LinkParams& calibrated, int target_link,
                                double desired_count, const ControlConfig& cfg,
                                const RngStream& rng, const DrawExchange* ex = nullptr);
+
+// ---- observation / output side --------------------------------
+struct Metrics {
+  double mae = 0.0;
+  double pearson_r = 0.0;
+  bool r_defined = false;
+  int n_pairs = 0;
+};
+/// Noisy partial-coverage observations of a truth series (observation.cpp:46-83):
+/// seeded Fisher-Yates link sample (lane 6), multiplicative uniform noise (lane 5).
+std::pair<CountSeries, std::vector<int>> synthesize_observations(const CountSeries& truth,
+                                                                 double noise_frac, double coverage,
+                                                                 const RngStream& rng);
+/// MAE and Pearson r over per-interval increments on common links (optimization.cpp:297-336).
+Metrics count_metrics(const CountSeries& sim, const CountSeries& truth);
+/// Intervals [k0, k1) of a series (pipeline.cpp:50-57).
+CountSeries slice_intervals(const CountSeries& s, int k0, int k1);
+/// "link_id,t_seconds,cumulative_count" CSV, byte-identical to pipeline.cpp:113-127.
+std::string series_to_csv(const CountSeries& s);
+/// Parser of that CSV with the reference's validation (pipeline.cpp:129-160).
+CountSeries series_from_csv(const std::string& text);
 
 /// series_from_levels (observation.cpp:27-44).
 CountSeries series_from_levels(const std::vector<std::vector<double>>& cum_per_step,

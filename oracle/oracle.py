@@ -114,6 +114,12 @@ class RefLib:
         L.ref_gradient.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, u64, u64, C.c_int,
                                    vp, vp, vp, vp, vp, vp, _dp, vp, vp, vp, vp, vp, vp]
         L.ref_gradient_mse.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, u64, u64, C.c_int, _ip, C.c_int, _dp, vp, _dp]
+        L.ref_synthesize_observations.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_int, C.c_double, C.c_double, u64,
+                                                  C.POINTER(C.c_int), _ip, _dp]
+        L.ref_count_metrics.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_int, C.c_int, _ip, _dp, _dp,
+                                        C.POINTER(C.c_int)]
+        L.ref_series_to_csv.restype = C.c_long
+        L.ref_series_to_csv.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_int, C.c_char_p, C.c_long]
         L.ref_calibrate.argtypes = [vp, C.c_int, _ip, C.c_int, _dp, _dp, _dp, _ip, u64, vp, vp, vp, vp, vp,
                                     _dp, _dp, _ip, _ip, _dp]
         L.ref_optimize_control.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_double, _dp, _ip,
@@ -121,6 +127,37 @@ class RefLib:
 
     def err(self) -> str:
         return self.lib.ref_last_error().decode()
+
+    # ---- observation / output side (observation.cpp:46-83, optimization.cpp:297-336,
+    # pipeline.cpp:113-127) ------------------------------------------------------------
+    def synthesize_observations(self, ids, vals, interval_s, noise_frac, coverage, seed):
+        ids = np.ascontiguousarray(ids, np.int32)
+        vals = np.ascontiguousarray(vals, np.float64)
+        k, n = vals.shape
+        m = C.c_int()
+        oi = np.zeros(max(n, 1), np.int32)
+        ov = np.zeros(max(k * n, 1))
+        self.check(self.lib.ref_synthesize_observations(k, n, ids, vals.ravel(), interval_s, noise_frac, coverage,
+                                                        seed, C.byref(m), oi, ov))
+        mm = m.value
+        return oi[:mm].copy(), ov[:k * mm].reshape(k, mm).copy()
+
+    def count_metrics(self, sim_ids, sim_vals, truth_ids, truth_vals):
+        a = [np.ascontiguousarray(x, t) for x, t in ((sim_ids, np.int32), (sim_vals, np.float64),
+                                                     (truth_ids, np.int32), (truth_vals, np.float64))]
+        out3 = np.zeros(3)
+        npairs = C.c_int()
+        self.check(self.lib.ref_count_metrics(a[1].shape[0], len(a[0]), a[0], a[1].ravel(), a[3].shape[0], len(a[2]),
+                                              a[2], a[3].ravel(), out3, C.byref(npairs)))
+        return dict(mae=float(out3[0]), pearson_r=float(out3[1]), r_defined=bool(out3[2]), n_pairs=npairs.value)
+
+    def series_to_csv(self, ids, vals, interval_s) -> str:
+        ids = np.ascontiguousarray(ids, np.int32)
+        vals = np.ascontiguousarray(vals, np.float64)
+        n = self.lib.ref_series_to_csv(vals.shape[0], len(ids), ids, vals.ravel(), interval_s, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        self.lib.ref_series_to_csv(vals.shape[0], len(ids), ids, vals.ravel(), interval_s, buf, n + 1)
+        return buf.value.decode()
 
     def check(self, rc: int):
         if rc != 0:

@@ -19,7 +19,9 @@
 
 #include "dtsim/engine.hpp"
 #include "dtsim/network.hpp"
+#include "dtsim/observation.hpp"
 #include "dtsim/optimization.hpp"
+#include "dtsim/pipeline.hpp"
 
 using namespace dtsim;
 
@@ -486,6 +488,49 @@ int ref_optimize_control(void* h, const double* u, const double* k,
     g_err = e.what();
     return 1;
   }
+}
+
+// ---- observation / output side (observation.cpp:46-83, optimization.cpp:297-336,
+// pipeline.cpp:113-160) ---------------------------------------------------------
+static CountSeries ref_series(int k, int n, const int* ids, const double* vals, int interval_s) {
+  CountSeries s;
+  s.link_ids.assign(ids, ids + n);
+  s.interval_s = interval_s;
+  for (int q = 0; q < k; ++q) s.values.emplace_back(vals + q * n, vals + (q + 1) * n);
+  return s;
+}
+
+int ref_synthesize_observations(int k, int n, const int* ids, const double* vals, int interval_s,
+                                double noise_frac, double coverage, uint64_t seed, int* m_out,
+                                int* obs_ids, double* obs_vals) {
+  return guarded([&] {
+    const auto r = synthesize_observations(ref_series(k, n, ids, vals, interval_s), noise_frac, coverage,
+                                           RngStream(seed));
+    const int m = static_cast<int>(r.second.size());
+    *m_out = m;
+    std::copy(r.second.begin(), r.second.end(), obs_ids);
+    for (int q = 0; q < k; ++q) std::copy(r.first.values[q].begin(), r.first.values[q].end(), obs_vals + q * m);
+  });
+}
+
+int ref_count_metrics(int ks, int ns, const int* sid, const double* sv, int kt, int nt, const int* tid,
+                      const double* tv, double* out3, int* n_pairs) {
+  return guarded([&] {
+    const Metrics m = count_metrics(ref_series(ks, ns, sid, sv, 1), ref_series(kt, nt, tid, tv, 1));
+    out3[0] = m.mae;
+    out3[1] = m.pearson_r;
+    out3[2] = m.r_defined ? 1.0 : 0.0;
+    *n_pairs = m.n_pairs;
+  });
+}
+
+// CSV text of a series into buf (cap bytes incl. NUL); returns the length.
+long ref_series_to_csv(int k, int n, const int* ids, const double* vals, int interval_s, char* buf,
+                       long cap) {
+  std::string s;
+  if (guarded([&] { s = series_to_csv(ref_series(k, n, ids, vals, interval_s)); })) return -1;
+  if (buf && cap > static_cast<long>(s.size())) std::memcpy(buf, s.c_str(), s.size() + 1);
+  return static_cast<long>(s.size());
 }
 
 }  // extern "C"

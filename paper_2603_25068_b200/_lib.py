@@ -139,6 +139,14 @@ SIGNATURES = [
                             _dp, _dp, _dp, _dp, _dp, vp, vp, vp, _dp, vp, vp]),
     ("dtg_optimize_control", i32, [vp, _dp, _dp, _dp, _dp, _dp, i32, C.c_double, vp,
                                    C.c_double, u64, _dp, vp, vp, vp, vp, _dp, vp, vp, vp]),
+    ("dtg_observe_last_error", C.c_char_p, []),
+    ("dtg_synthesize_observations", i32, [i32, i32, _ip, _dp, i32, C.c_double, C.c_double, u64,
+                                          C.POINTER(C.c_int), _ip, _dp]),
+    ("dtg_count_metrics", i32, [i32, i32, _ip, _dp, i32, i32, _ip, _dp, C.POINTER(C.c_double),
+                                C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("dtg_series_to_csv", i32, [i32, i32, _ip, _dp, i32, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("dtg_series_from_csv", i32, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                  vp, vp, C.c_size_t, C.c_size_t]),
     ("dtg_scenario_ctx", vp, [vp]),
     ("dtg_mse_loss", i32, [i32, i32, _dp, i32, _ip, i32, _dp, i32, _dp, _dp]),
     ("dtg_debug_gumbel", i32, [u64, u64, i32, _u64p, _u64p, _dp]),

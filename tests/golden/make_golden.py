@@ -173,6 +173,53 @@ def optim_cases():
          zero_gradient_stall=np.int32(ctl["zero_gradient_stall"]), loss_curve=ctl["loss_curve"])
 
 
+def observe_cases():
+    """synthesize_observations / count_metrics / series_to_csv on the C1 truth run."""
+    rs = RefScenario.grid(R, 4, 400.0, 42, 1000.0).configure(1000, 1, 1800, 300)
+    truth = rs.sample_parameters(42)
+    tr = rs.forward(truth, 42, 0)
+    f, t, ln, k = rs.links()
+    phys = np.array([j for j in range(rs.n_links) if k[j] == 0], np.int32)
+    vals = tr["cum_per_step"][299::300][:, phys] * 1.0  # series_from_levels, dn = 1
+    window = vals[:2]  # observe_window_min = 10 of 5-min intervals
+    oid, ov = R.synthesize_observations(phys, window, 300, 0.1, 0.8, 42)
+    # a calibrated-like series: the truth rows perturbed deterministically
+    rng = np.random.default_rng(3)
+    sim = vals * (1.0 + 0.05 * rng.standard_normal(vals.shape))
+    met = R.count_metrics(phys, sim, oid, ov)
+    met_self = R.count_metrics(phys, vals, phys, vals)
+    csv_truth = R.series_to_csv(phys, vals, 300)
+    csv_obs = R.series_to_csv(oid, ov, 300)
+    save("observe_c1", phys=phys, truth_vals=vals, obs_ids=oid, obs_vals=ov, sim_vals=sim,
+         metrics=np.array([met["mae"], met["pearson_r"], met["r_defined"], met["n_pairs"]], np.float64),
+         metrics_self=np.array([met_self["mae"], met_self["pearson_r"], met_self["r_defined"],
+                                met_self["n_pairs"]], np.float64),
+         csv_truth=np.frombuffer(csv_truth.encode(), np.uint8), csv_obs=np.frombuffer(csv_obs.encode(), np.uint8))
+
+
+def pipeline_case():
+    """synthesize -> calibrate -> nowcast -> metrics on a 3x3 grid, the data flow
+    of cmd_synthesize / cmd_calibrate / cmd_nowcast (pipeline.cpp:192-331)."""
+    rs = RefScenario.grid(R, 3, 300.0, 42, 600.0).configure(300, 1, 240, 60)
+    f, t, ln, k = rs.links()
+    phys = np.array([j for j in range(rs.n_links) if k[j] == 0], np.int32)
+    truth = rs.sample_parameters(42)
+    tr = rs.forward(truth, 42, 0)
+    truth_vals = tr["cum_per_step"][59::60][:, phys] * 1.0
+    oid, ov = R.synthesize_observations(phys, truth_vals[:2], 60, 0.1, 0.8, 42)
+    rw = RefScenario.grid(R, 3, 300.0, 42, 600.0).configure(300, 1, 120, 60)
+    cal = rw.calibrate(oid, ov, 42, cfg=dict(max_iterations=5, patience=3, noise_draws=2, lr=0.1))
+    from oracle.oracle import Params
+    best = Params(*cal["best"])
+    now = rs.forward(best, 42, 1000000007)
+    now_vals = now["cum_per_step"][59::60][:, phys] * 1.0
+    met = R.count_metrics(phys, now_vals, phys, truth_vals)
+    save("pipeline_grid3", phys=phys, truth_vals=truth_vals, obs_ids=oid, obs_vals=ov,
+         loss_curve=cal["loss_curve"], best=cal["best"], now_vals=now_vals,
+         metrics=np.array([met["mae"], met["pearson_r"], met["r_defined"], met["n_pairs"]], np.float64),
+         csv_now=np.frombuffer(R.series_to_csv(phys, now_vals, 60).encode(), np.uint8))
+
+
 def main():
     # RNG known-answer values (include/dtsim/rng.hpp, tensor.cpp:682-699)
     seeds = np.array([0, 1, 7, 42, 2**63 + 5, 0xDEADBEEF], np.uint64)
@@ -236,6 +283,11 @@ def main():
 if __name__ == "__main__":
     if sys.argv[1:] == ["optim"]:
         optim_cases()
+    elif sys.argv[1:] == ["observe"]:
+        observe_cases()
+        pipeline_case()
     else:
         main()
         optim_cases()
+        observe_cases()
+        pipeline_case()

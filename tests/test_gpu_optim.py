@@ -156,3 +156,33 @@ def test_sharded_exchange_world1_is_bit_identical():
     b = calibrate_sharded(sc, d["obs_ids"], d["obs"], 5, cfg=cfg)
     np.testing.assert_array_equal(a.loss_curve, b.loss_curve)
     np.testing.assert_array_equal(np.stack(a.best_params.arrays()), np.stack(b.best_params.arrays()))
+
+
+def test_pipeline_synthesize_calibrate_nowcast():
+    """The cmd_synthesize -> cmd_calibrate -> cmd_nowcast data flow
+    (pipeline.cpp:192-331) on the device path against the reference's run
+    (tests/golden/pipeline_grid3): observations and the nowcast CSV byte-for-byte,
+    the calibration curve to 1e-12, metrics exactly."""
+    from paper_2603_25068_b200 import observe as O
+
+    d = load("pipeline_grid3")
+    sc = P.Scenario.grid(3, 300.0, 42, 600.0).configure(300, 1, 240, 60)
+    phys = d["phys"]
+    truth = sc.sample_parameters(42)
+    tr = P.simulate_forward(sc, truth, seed=42)
+    truth_s = O.series_from_levels(tr.cum_per_step, phys, 60, 1.0, 1)
+    assert np.array_equal(truth_s.values, d["truth_vals"])
+    window = O.CountSeries(phys, 60, truth_s.values[:2])
+    obs, ids = O.synthesize_observations(window, 0.1, 0.8, 42)
+    assert np.array_equal(ids, d["obs_ids"]) and np.array_equal(obs.values, d["obs_vals"])
+    sw = P.Scenario.grid(3, 300.0, 42, 600.0).configure(300, 1, 120, 60)
+    cal = P.calibrate(sw, ids, obs.values, 42, cfg=P.OptimizeConfig(max_iterations=5, patience=3, noise_draws=2))
+    np.testing.assert_allclose(cal.loss_curve, d["loss_curve"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(np.stack(cal.best_params.arrays()), d["best"], rtol=1e-9, atol=0)
+    now = P.simulate_forward(sc, cal.best_params, seed=42, noise_iteration=1000000007)
+    now_s = O.series_from_levels(now.cum_per_step, phys, 60, 1.0, 1)
+    assert np.array_equal(now_s.values, d["now_vals"])
+    assert O.series_to_csv(now_s).encode() == bytes(d["csv_now"])
+    m = O.count_metrics(now_s, truth_s)
+    assert (m.mae, m.pearson_r, m.r_defined, m.n_pairs) == (
+        d["metrics"][0], d["metrics"][1], bool(d["metrics"][2]), int(d["metrics"][3]))
