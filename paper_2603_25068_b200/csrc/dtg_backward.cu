@@ -195,6 +195,7 @@ __device__ __forceinline__ void replay_head(const BView& V, int b, int t, int k,
       c = d.succ[s0 + ed];
       for (int e = 0; e < deg; ++e) lp[e] = pi[e];
     }
+    const int qq = atomicAdd(&V.ccnt[bl + c], 1);  // round trip overlaps the merge draw
     const double gmc =
         gumbel_bits(rng_final(rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
                                           static_cast<std::uint64_t>(c)),
@@ -207,7 +208,6 @@ __device__ __forceinline__ void replay_head(const BView& V, int b, int t, int k,
     cd.aid = a;
     cd.link = j;
     cd.pad = 0;
-    const int qq = atomicAdd(&V.ccnt[bl + c], 1);
     if (qq < kBwdCandCap) V.cands[(bl + c) * kBwdCandCap + qq] = cd;
   }
   V.choice[bn + k] = c;

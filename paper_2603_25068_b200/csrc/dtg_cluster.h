@@ -40,6 +40,7 @@ struct CView {
   unsigned long long* wstamp;  // optional per-warp slot-phase record [T][warps][4]
   int contig;          // 1: contiguous slot range per CTA, 0: interleaved 512-slot blocks
   int ckpt;            // keep every layout (else positions/links of the final one only)
+  int dbg;             // timing experiments only (dtg_set_flag 3); results invalid when nonzero
 };
 
 void launch_pack_succ(const DevView& d, double* srec, cudaStream_t st);

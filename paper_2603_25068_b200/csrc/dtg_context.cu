@@ -127,7 +127,8 @@ struct dtg_ctx {
   DevBuf<unsigned int> gbar;
   bool custom_barrier = true;
   int contig_mode = -1;
-  int bwd_dbg = 0;  // timing experiments only  // -1 auto, 0 interleaved, 1 contiguous (fused forward slot mapping)
+  int bwd_dbg = 0;  // timing experiments only
+  int fwd_dbg = 0;  // timing experiments only  // -1 auto, 0 interleaved, 1 contiguous (fused forward slot mapping)
   bool want_wstamp = false;
   DevBuf<unsigned long long> wst;
   DevBuf<dtg::Cand> cands;
@@ -541,6 +542,9 @@ int dtg_set_flag(dtg_ctx* c, int flag, int value) {
     case 0:  // grid barrier: 1 release/acquire counter (default), 0 cooperative_groups grid.sync
       c->custom_barrier = value != 0;
       return DTG_OK;
+    case 3:  // fused-forward timing experiments (results invalid when nonzero)
+      c->fwd_dbg = value;
+      return DTG_OK;
     case 2:  // reverse-sweep timing experiments (results invalid when nonzero)
       c->bwd_dbg = value;
       return DTG_OK;
@@ -753,6 +757,7 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       V.srec = c->srec.p;
       V.T = T;
       V.ckpt = checkpoint ? 1 : 0;
+      V.dbg = c->fwd_dbg;
       V.stage_params = c->stage_params ? 1 : 0;
       V.tstamp = nullptr;
       V.gbar = c->custom_barrier ? c->gbar.p : nullptr;

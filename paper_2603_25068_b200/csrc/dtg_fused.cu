@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
           if (!fa) continue;
           ++n_arr;
           wonc[k] = 0;
-          if (soff_s[j + 1] > soff_s[j]) {
+          if (soff_s[j + 1] > soff_s[j] && !(V.dbg & 1)) {
             const int hi = defer ? atomicAdd(hcnt, 1) : kHeadCap;
             if (hi < kHeadCap) {
               hq[hi] = k;
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
       const int gw0 = (static_cast<int>(threadIdx.x) >> 5) * V.cs + rank;
       for (int i = gw0 * 32 + (threadIdx.x & 31); i < L; i += nthr) {
         const int n_i = offB[i + 1] - offB[i];
-        const int cnt = V.ccnt[bl + i];
+        const int cnt = (V.dbg & 2) ? 0 : V.ccnt[bl + i];
         const int qc = n_i ? qnc[i] : 0;
         const double tx = n_i ? tailc[i] : d.M;
         const double qpv = qhp[i], cpv = chp[i];
