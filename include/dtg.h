@@ -142,6 +142,11 @@ int dtg_debug_gumbel(uint64_t seed, uint64_t key, int n, const uint64_t* rows,
  * (which: 0 Gumbel draw, 1 log, 2 exp, 3 division, 4 L2 pointer chase,
  * 5 counter-RNG uniform; 100 = empty grid.sync with `grid` CTAs of 512). */
 int dtg_debug_microbench(int which, int n, int grid, double* result);
+/* Test hook: bitwise check of the straight-line log / Gumbel against
+ * libdevice on n inputs per kind; mismatches must be 0, flagged counts the
+ * arguments routed to the libdevice fallback. */
+int dtg_debug_log_check(uint64_t seed, long long n, unsigned long long* mismatches,
+                        unsigned long long* flagged);
 /* Test hook: one fused forward recording, per step and warp, the slot-phase
  * start, end of the offsets prologue, end of the slot loop (globaltimer ns)
  * and the number of arrived agents in the warp: out[T][n_warps][4]. */

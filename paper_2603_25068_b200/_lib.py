@@ -151,6 +151,7 @@ SIGNATURES = [
     ("dtg_mse_loss", i32, [i32, i32, _dp, i32, _ip, i32, _dp, i32, _dp, _dp]),
     ("dtg_debug_gumbel", i32, [u64, u64, i32, _u64p, _u64p, _dp]),
     ("dtg_debug_microbench", i32, [i32, i32, i32, _dp]),
+    ("dtg_debug_log_check", i32, [u64, C.c_longlong, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     ("dtg_debug_warp_records", i32, [vp, i32, i32, vp, C.POINTER(C.c_int)]),
     ("dtg_scenario_last_error", C.c_char_p, [vp]),
 ]

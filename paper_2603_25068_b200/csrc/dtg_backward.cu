@@ -161,9 +161,15 @@ __device__ __forceinline__ void replay_head(const BView& V, int b, int t, int k,
       double y[kFastDeg], ex[kFastDeg];
 #pragma unroll
       for (int e = 0; e < kFastDeg; ++e) sc[e] = d.succ[s0 + (e < deg ? e : 0)];
+      int bad = 0;  // straight-line logs: the five draw chains interleave
 #pragma unroll
       for (int e = 0; e < kFastDeg; ++e)
-        y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sc[e])))) * d.kinv;
+        y[e] = (lz[e < deg ? e : 0] + gumbel_sl(rng_final(h2l, static_cast<std::uint64_t>(sc[e])), bad)) * d.kinv;
+      if (bad) {
+#pragma unroll
+        for (int e = 0; e < kFastDeg; ++e)
+          y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sc[e])))) * d.kinv;
+      }
       double m2 = y[0];
 #pragma unroll
       for (int e = 1; e < kFastDeg; ++e)
@@ -515,12 +521,17 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
             for (int q = spread(ta, lg, nblk); q < nA; q += nblk * kHalf) {
               const int s = V.alist[bn + q];
               const int id = d.aid[so + s];
+              double gq[kFastDeg];
+              int bad = 0;
+#pragma unroll
+              for (int e = 0; e < kFastDeg; ++e) gq[e] = gumbel_sl(rng_final(hf[e], static_cast<std::uint64_t>(id)), bad);
+              if (bad) {
+#pragma unroll
+                for (int e = 0; e < kFastDeg; ++e) gq[e] = gumbel_bits(rng_final(hf[e], static_cast<std::uint64_t>(id)));
+              }
 #pragma unroll
               for (int e = 0; e < kFastDeg; ++e)
-                if (e < deg0) {
-                  const double g = gumbel_bits(rng_final(hf[e], static_cast<std::uint64_t>(id)));
-                  t2_push(tf[e], (logz + g) * d.kinv, id, s);
-                }
+                if (e < deg0) t2_push(tf[e], (logz + gq[e]) * d.kinv, id, s);
             }
 #pragma unroll
             for (int e = 0; e < kFastDeg; ++e)

@@ -22,6 +22,7 @@
 //   barrier
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 
@@ -35,7 +36,8 @@ namespace dtg {
 
 namespace {
 
-constexpr int kBatch = 4;   // slots per thread in flight together
+// kBatch: slots per thread in flight together (4; 1 when every thread owns at
+// most one slot, which leaves the arrived-head draw chains more registers)
 constexpr int kHeadCap = 1024;  // deferred arrived heads per CTA (overflow runs inline)
 
 constexpr int kFastDeg = 5;  // successor counts up to this take the unrolled head path
@@ -61,9 +63,16 @@ __device__ __forceinline__ void head_choice(const CView& V, std::size_t bl, std:
     double y[kFastDeg], ex[kFastDeg];
 #pragma unroll
     for (int e = 0; e < kFastDeg; ++e) sj[e] = d.succ[sb + (e < deg ? e : 0)];
+    // straight-line logs (dtg_device.cuh): the five draw chains interleave
+    int bad = 0;
 #pragma unroll
     for (int e = 0; e < kFastDeg; ++e)
-      y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sj[e])))) * d.kinv;
+      y[e] = (lz[e < deg ? e : 0] + gumbel_sl(rng_final(h2l, static_cast<std::uint64_t>(sj[e])), bad)) * d.kinv;
+    if (bad) {
+#pragma unroll
+      for (int e = 0; e < kFastDeg; ++e)
+        y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sj[e])))) * d.kinv;
+    }
     double m2 = y[0];
 #pragma unroll
     for (int e = 1; e < kFastDeg; ++e)
@@ -202,7 +211,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ep
 
 }  // namespace
 
-template <bool kCluster>
+template <bool kCluster, int kBatch>
 __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const DevView& d = V.d;
@@ -552,10 +561,19 @@ int fused_smem_bytes(int L, bool stage_params) {
   return (stage_params ? 3 * L * 8 : 0) + (2 * (L + 1) + 3 * L + 2 * (L + 1) + 36 + 3 * kHeadCap) * 4;
 }
 
+namespace {
+template <int KB>
+const void* fused_fn(bool cluster) {
+  return cluster ? reinterpret_cast<const void*>(k_forward_fused<true, KB>)
+                 : reinterpret_cast<const void*>(k_forward_fused<false, KB>);
+}
+}  // namespace
+
 cudaError_t launch_forward_fused(const CView& V, bool cluster, cudaStream_t st) {
   const int smem = fused_smem_bytes(V.d.L, V.stage_params != 0);
-  const void* fn = cluster ? reinterpret_cast<const void*>(k_forward_fused<true>)
-                           : reinterpret_cast<const void*>(k_forward_fused<false>);
+  // one slot per thread -> kBatch 1
+  const bool one = V.d.N <= V.cs * kClusterThreads;
+  const void* fn = one ? fused_fn<1>(cluster) : fused_fn<4>(cluster);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   if (cluster) {
@@ -575,34 +593,37 @@ cudaError_t launch_forward_fused(const CView& V, bool cluster, cudaStream_t st) 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_forward_fused<true>, V);
+    return one ? cudaLaunchKernelEx(&cfg, k_forward_fused<true, 1>, V) : cudaLaunchKernelEx(&cfg, k_forward_fused<true, 4>, V);
   }
   void* args[] = {const_cast<CView*>(&V)};
   return cudaLaunchCooperativeKernel(fn, dim3(V.d.B * V.cs), dim3(kClusterThreads), args, smem, st);
 }
 
 int fused_max_grid(int L, bool stage_params) {
-  int dev = 0, sms = 0, occ = 0;
+  int dev = 0, sms = 0, occ = 0, occ1 = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int smem = fused_smem_bytes(L, stage_params);
-  const void* fn = reinterpret_cast<const void*>(k_forward_fused<false>);
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kClusterThreads, smem);
-  return occ * sms;
+  for (const void* fn : {fused_fn<4>(false), fused_fn<1>(false)})
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_fn<4>(false), kClusterThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, fused_fn<1>(false), kClusterThreads, smem);
+  return std::min(occ, occ1) * sms;
 }
 
 int fused_max_cluster(int L, bool stage_params) {
   const int smem = fused_smem_bytes(L, stage_params);
-  const void* fn = reinterpret_cast<const void*>(k_forward_fused<true>);
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
+  for (const void* fn : {fused_fn<4>(true), fused_fn<1>(true)}) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
-  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  const void* fn = fused_fn<4>(true);
   for (int cs = 16; cs >= 1; cs >>= 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);

@@ -86,3 +86,47 @@ extern "C" int dtg_debug_microbench(int which, int n, int grid, double* result) 
   cudaFree(chain);
   return e == cudaSuccess ? 0 : 4;
 }
+
+namespace dtg {
+// Bitwise comparison of the straight-line log / Gumbel with libdevice on
+// inputs the path produces (rng_unit draws and their -log) and on random
+// positive normal doubles over the whole exponent range.
+__global__ void k_log_check(std::uint64_t seed, long long n, unsigned long long* counts) {
+  unsigned long long mism = 0, bads = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const std::uint64_t b = rng_bits(seed, static_cast<std::uint64_t>(i), 17, 3);
+    int bad = 0;
+    const double u = rng_unit(b);
+    if (__double_as_longlong(log_sl(u, bad)) != __double_as_longlong(log(u))) ++mism;
+    const double v = -log(u);
+    if (__double_as_longlong(log_sl(v, bad)) != __double_as_longlong(log(v))) ++mism;
+    if (__double_as_longlong(gumbel_sl(b, bad)) != __double_as_longlong(gumbel_bits(b))) ++mism;
+    // random positive normal double: exponent field in [1, 2046]
+    const std::uint64_t r = rng_bits(seed ^ 0x5bd1e995ULL, static_cast<std::uint64_t>(i), 5, 9);
+    const std::uint64_t ex = 1 + (r >> 52) % 2046;
+    const double w = __longlong_as_double(static_cast<long long>((ex << 52) | (r & 0xFFFFFFFFFFFFFULL)));
+    int bw = 0;
+    const double lw = log_sl(w, bw);
+    if (bw) ++bads;
+    else if (__double_as_longlong(lw) != __double_as_longlong(log(w))) ++mism;
+    if (bad) ++bads;
+  }
+  atomicAdd(&counts[0], mism);
+  atomicAdd(&counts[1], bads);
+}
+}  // namespace dtg
+
+extern "C" int dtg_debug_log_check(uint64_t seed, long long n, unsigned long long* mismatches,
+                                   unsigned long long* flagged) {
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 16) != cudaSuccess) return 4;
+  cudaMemset(d, 0, 16);
+  dtg::k_log_check<<<148 * 8, 256>>>(seed, n, d);
+  unsigned long long h[2] = {0, 0};
+  const cudaError_t e = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  *mismatches = h[0];
+  *flagged = h[1];
+  return e == cudaSuccess ? 0 : 4;
+}

@@ -197,3 +197,15 @@ def test_sharded_gradient_world1_equals_per_draw_sum():
         seq += g.grads
     assert np.array_equal(gsum, seq)
     assert loss == pytest.approx(sum(g.loss for g in per) / 4, rel=1e-12)
+
+
+def test_straight_line_log():
+    """The branch-free log/Gumbel used on the head critical path is bitwise
+    libdevice's log on every input the path can produce (64M draws + 16M random
+    positive normal doubles)."""
+    import ctypes as C
+    lib = P.load()
+    mism, flagged = C.c_ulonglong(), C.c_ulonglong()
+    assert lib.dtg_debug_log_check(12345, 1 << 24, C.byref(mism), C.byref(flagged)) == 0
+    assert mism.value == 0
+    assert flagged.value == 0
