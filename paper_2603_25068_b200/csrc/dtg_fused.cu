@@ -73,27 +73,7 @@ __device__ __forceinline__ void head_choice(const CView& V, std::size_t bl, std:
       for (int e = 0; e < kFastDeg; ++e)
         y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sj[e])))) * d.kinv;
     }
-    double m2 = y[0];
-#pragma unroll
-    for (int e = 1; e < kFastDeg; ++e)
-      if (e < deg && m2 < y[e]) m2 = y[e];
-    double z2 = 0.0;
-#pragma unroll
-    for (int e = 0; e < kFastDeg; ++e) {
-      ex[e] = exp(y[e] - m2);
-      if (e < deg) z2 += ex[e];
-    }
-    int best = 0;
-    double pb = ex[0] / z2;
-#pragma unroll
-    for (int e = 1; e < kFastDeg; ++e)
-      if (e < deg) {
-        const double pv = ex[e] / z2;
-        if (pv > pb) {
-          pb = pv;
-          best = e;
-        }
-      }
+    const int best = softmax_first_argmax<kFastDeg>(deg, y, ex);
     c = sj[best];
   } else {
     double g[kMaxDeg], pi[kMaxDeg];
@@ -226,7 +206,6 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
   }
   const bool active = b < d.B;
   const int nthr = V.cs * blockDim.x;
-  const int gt0 = rank * blockDim.x + threadIdx.x;
   unsigned int epoch = 0;
   auto barrier = [&]() {
     if (kCluster)
@@ -516,8 +495,8 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
           } else if (cnt <= kFastDeg) {  // registers (dtg_merge.cuh)
             Cand c[kFastDeg];
             double lz[kFastDeg], pi[kFastDeg];
-            const int best = merge_softmax_fast<kFastDeg>(cnt, V.cands + (bl + i) * kClusterCandCap, d.kinv, c,
-                                                          lz, pi);
+            const int best = merge_softmax_fast<kFastDeg, false>(cnt, V.cands + (bl + i) * kClusterCandCap, d.kinv,
+                                                                 c, lz, pi);
 #pragma unroll
             for (int e = 0; e < kFastDeg; ++e)
               if (e < cnt && c[e].alpha == 0.0) atomicOr(&d.err[bb], kErrZeroAlpha);

@@ -19,7 +19,7 @@ namespace dtg {
 /// correct sort gives the reference's ascending order), runs two_softmax and
 /// returns the first argmax.  lz / pi receive the first-stage log-softmax and
 /// the probabilities of the sorted candidates.
-template <int F>
+template <int F, bool kNeedPi = true>
 __device__ __forceinline__ int merge_softmax_fast(int cnt, const Cand* src, double kinv, Cand (&c)[F],
                                                   double (&lz)[F], double (&pi)[F]) {
 #pragma unroll
@@ -61,6 +61,10 @@ __device__ __forceinline__ int merge_softmax_fast(int cnt, const Cand* src, doub
   for (int e = 0; e < F; ++e) {
     lz[e] = c[e].alpha - lzz;
     y[e] = (lz[e] + c[e].g) * kinv;
+  }
+  if (!kNeedPi) {  // the forward needs the winner only
+    double ex[F];
+    return softmax_first_argmax<F>(cnt, y, ex);
   }
   double m2 = y[0];
 #pragma unroll
