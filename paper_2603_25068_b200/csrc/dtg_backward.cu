@@ -202,10 +202,12 @@ __device__ __forceinline__ void replay_head(const BView& V, int b, int t, int k,
       for (int e = 0; e < deg; ++e) lp[e] = pi[e];
     }
     const int qq = atomicAdd(&V.ccnt[bl + c], 1);  // round trip overlaps the merge draw
-    const double gmc =
-        gumbel_bits(rng_final(rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
-                                          static_cast<std::uint64_t>(c)),
-                              static_cast<std::uint64_t>(a)));
+    const std::uint64_t mb = rng_final(rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
+                                                   static_cast<std::uint64_t>(c)),
+                                       static_cast<std::uint64_t>(a));
+    int mbad = 0;
+    double gmc = gumbel_sl(mb, mbad);
+    if (mbad) gmc = gumbel_bits(mb);
     V.ched[bn + k] = ed;
     Cand cd;
     cd.alpha = d.alpha[bl + j];

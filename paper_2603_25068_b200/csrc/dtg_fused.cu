@@ -82,7 +82,12 @@ __device__ __forceinline__ void head_choice(const CView& V, std::size_t bl, std:
   }
   Cand cd;
   cd.alpha = d.alpha[bl + j];
-  cd.g = gumbel_bits(rng_final(rng_prefix2(h1m, static_cast<std::uint64_t>(c)), static_cast<std::uint64_t>(a)));
+  {
+    int bad = 0;
+    const std::uint64_t mb = rng_final(rng_prefix2(h1m, static_cast<std::uint64_t>(c)), static_cast<std::uint64_t>(a));
+    cd.g = gumbel_sl(mb, bad);
+    if (bad) cd.g = gumbel_bits(mb);
+  }
   cd.slot = k;
   cd.aid = a;
   cd.link = j;
