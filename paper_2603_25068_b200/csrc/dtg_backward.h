@@ -50,6 +50,7 @@ struct BView {
   int K, spi, T, bps, force_slow;
   int dbg;  // timing experiments only (dtg_set_flag 2): bits skip parts of R1
   unsigned long long* tstamp;  // optional [T][grid][8] phase timestamps
+  unsigned int* gbar;          // grid-barrier counter (zeroed before launch; null: cooperative_groups)
 };
 
 int backward_smem_bytes(int L, int maxdeg);

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <functional>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
@@ -124,7 +125,7 @@ struct dtg_ctx {
   bool stage_params = false;
   int last_mode = 0, last_cs = 0;
   DevBuf<double> srec;
-  DevBuf<unsigned int> gbar;
+  DevBuf<unsigned int> gbar, bgbar;
   bool custom_barrier = true;
   int contig_mode = -1;
   int bwd_dbg = 0;  // timing experiments only
@@ -572,7 +573,8 @@ int dtg_profile_backward(dtg_ctx* c, double* phase_us, int* grid_out) {
     if (c->last_T < 1 || !c->last_ckpt) throw std::runtime_error("needs a checkpointed forward");
     c->want_stamps = true;
     try {
-      run_backward(c, nullptr, nullptr, nullptr, cudaMemcpyHostToDevice);
+      // the seeds of the last device-loss evaluation when there was one, else zeros
+      run_backward(c, nullptr, nullptr, nullptr, cudaMemcpyHostToDevice, c->loss_kind != dtg::kLossNone);
     } catch (...) {
       c->want_stamps = false;
       throw;
@@ -583,7 +585,8 @@ int dtg_profile_backward(dtg_ctx* c, double* phase_us, int* grid_out) {
     std::vector<unsigned long long> s(static_cast<std::size_t>(T) * G * 8);
     CK(cudaMemcpy(s.data(), c->stamps.p, s.size() * 8, cudaMemcpyDeviceToHost));
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int t = 0; t < T; ++t) {
+    unsigned long long prev_mx7 = 0;  // step t+1's R4 end (the sweep runs t = T-1 .. 0)
+    for (int t = T - 1; t >= 0; --t) {
       unsigned long long mn[8], mx[8];
       for (int w = 0; w < 8; ++w) {
         mn[w] = ~0ull;
@@ -603,8 +606,11 @@ int dtg_profile_backward(dtg_ctx* c, double* phase_us, int* grid_out) {
       acc[4] += double(mx[5] - mn[4]);
       acc[5] += double(mn[6] - mx[5]);
       acc[6] += double(mx[7] - mn[6]);
+      if (t < T - 1) acc[7] += double(mn[0] - prev_mx7);  // step barrier + next step's entry
+      prev_mx7 = mx[7];
     }
-    for (int w = 0; w < 8; ++w) phase_us[w] = acc[w] / T / 1e3;
+    for (int w = 0; w < 7; ++w) phase_us[w] = acc[w] / T / 1e3;
+    phase_us[7] = T > 1 ? acc[7] / (T - 1) / 1e3 : 0.0;
     if (grid_out) *grid_out = G;
   });
 }
@@ -974,6 +980,12 @@ static void run_backward_persistent(dtg_ctx* c, cudaStream_t st) {
     V.tstamp = c->stamps.p;
   }
   c->last_bgrid = grid;
+  V.gbar = nullptr;
+  if (c->custom_barrier) {
+    c->bgbar.ensure(1);
+    CK(cudaMemsetAsync(c->bgbar.p, 0, sizeof(unsigned int), st));
+    V.gbar = c->bgbar.p;
+  }
   CK(dtg::launch_backward_persistent(V, grid, st));
   c->launches = 1;
   c->pending = true;

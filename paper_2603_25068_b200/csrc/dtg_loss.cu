@@ -18,8 +18,8 @@ namespace {
 // order exactly like the host tape's `d_snapshots[k][id] += ...`.  Loss: one
 // thread per interval sums its squared residuals in q order, then thread 0 adds
 // the interval sums in k order and scales (acc = acc + r_k; loss = acc * sc).
-__global__ void k_loss_mse(LossView v) {
-  extern __shared__ double rk[];
+__global__ void k_loss_mse(LossView v, int kchunk) {
+  extern __shared__ double sq[];  // [kchunk][nobs] squared residuals, then [kobs] interval sums
   const int b = blockIdx.x;
   const double dn = v.dn, sc = v.sc;
   const int n = v.nobs;
@@ -36,18 +36,27 @@ __global__ void k_loss_mse(LossView v) {
     }
     v.snap_seed[(static_cast<std::size_t>(b) * v.K + k) * v.L + v.ids[q]] = acc;
   }
-  for (int k = threadIdx.x; k < v.kobs; k += blockDim.x) {
-    const double* snap =
-        v.cumh + (static_cast<std::size_t>(k + 1) * v.spi * v.B + b) * v.L;
-    const double* o = v.obs + static_cast<std::size_t>(k) * n;
-    double r = 0.0;
-    for (int q = 0; q < n; ++q) {
-      const double d = snap[v.ids[q]] * dn - o[q];
-      r += d * d;
+  // loss: the squared residuals are formed in parallel, then each interval's
+  // sum runs sequentially in q order (one warp lane per interval), as the tape
+  double* rk = sq + static_cast<std::size_t>(kchunk) * n;
+  for (int k0 = 0; k0 < v.kobs; k0 += kchunk) {
+    const int kc = min(kchunk, v.kobs - k0);
+    for (int e = threadIdx.x; e < kc * n; e += blockDim.x) {
+      const int k = k0 + e / n, q = e - (e / n) * n;
+      const double* snap = v.cumh + (static_cast<std::size_t>(k + 1) * v.spi * v.B + b) * v.L;
+      const double d = snap[v.ids[q]] * dn - v.obs[static_cast<std::size_t>(k) * n + q];
+      sq[e] = d * d;
     }
-    rk[k] = r;
+    __syncthreads();
+    for (int kk = threadIdx.x >> 5; kk < kc; kk += blockDim.x >> 5)
+      if ((threadIdx.x & 31) == 0) {
+        const double* row = sq + static_cast<std::size_t>(kk) * n;
+        double r = 0.0;
+        for (int q = 0; q < n; ++q) r += row[q];
+        rk[k0 + kk] = r;
+      }
+    __syncthreads();
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
     double acc = 0.0;
     for (int k = 0; k < v.kobs; ++k) acc = acc + rk[k];
@@ -109,7 +118,13 @@ __global__ void k_reduce_rows(int D, int L, const double* __restrict__ rows, int
 
 void launch_device_loss(const LossView& v, cudaStream_t st) {
   if (v.kind == kLossMse) {
-    k_loss_mse<<<v.B, 256, sizeof(double) * (v.kobs > 0 ? v.kobs : 1), st>>>(v);
+    // as many intervals' residuals in shared memory as fit in ~160 KB
+    const int n = v.nobs > 0 ? v.nobs : 1;
+    int kchunk = static_cast<int>((160 * 1024 / 8 - (v.kobs + 1)) / n);
+    kchunk = std::max(1, std::min(kchunk, v.kobs > 0 ? v.kobs : 1));
+    const std::size_t smem = sizeof(double) * (static_cast<std::size_t>(kchunk) * n + v.kobs + 1);
+    cudaFuncSetAttribute(k_loss_mse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_loss_mse<<<v.B, 512, smem, st>>>(v, kchunk);
   } else if (v.kind == kLossControl) {
     k_loss_control<<<(v.B + 127) / 128, 128, 0, st>>>(v);
   }

@@ -426,8 +426,8 @@ class Engine:
         ph = np.zeros(8)
         g = C.c_int()
         self._check(self._lib.dtg_profile_backward(self._h, ph, C.byref(g)))
-        names = ["R1", "bar1", "R2", "bar2", "R3", "bar3", "R4"]
-        return dict(zip(names, ph[:7].tolist())), g.value
+        names = ["R1", "bar1", "R2", "bar2", "R3", "bar3", "R4", "bar4"]
+        return dict(zip(names, ph.tolist())), g.value
 
     def force_slow_path(self, on: bool):
         self._check(self._lib.dtg_debug_force_slow_path(self._h, int(on)))

@@ -103,3 +103,16 @@ def test_c3_forward_chicago_scale(port):
     # SURVEY.md §8c C3 forward KAT (reference build, 574.9 s on one core)
     assert tr.cum_final.sum() == 38158
     assert fnv1a64(tr.link_final, tr.pos_final) == 0x5573A3F14223BBBA
+
+
+def test_c3_dn1_million_agents(port):
+    """C3 at dn=1: 1,000,020 agents (the stress variant of SURVEY.md §8d), 12
+    steps bit-exact against the C oracle; every layout conserves all agents
+    (the kernel's conservation check raises otherwise)."""
+    T = 12
+    sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 1, T, 300)
+    assert sc.n_agents == 1000020
+    p = sc.sample_parameters(3)
+    tr = P.simulate_forward(sc, p, seed=7)
+    ref = port_of(port, sc).forward(p, 7, 0)
+    assert_forward_equal(tr, ref)
