@@ -17,6 +17,8 @@
 
 #include "../paper_2603_25068_b200/csrc/dtg_rng.h"
 
+struct dtg_ctx;  // the C-ABI device context (include/dtg.h)
+
 namespace dtg {
 
 // ---- network (network.hpp:11-51) ------------------------------------------------
@@ -89,6 +91,11 @@ struct Scenario {
     double pos = 0.0;
   };
   std::vector<Placement> custom_init;
+  /// Nonzero: identifies the initial state seed_agents() produces (equal keys
+  /// promise equal states), so a device context that already holds it skips
+  /// the re-seeding and upload.  0 (default): always upload.  The level-2
+  /// C-ABI assigns a fresh key whenever a scenario is created or reconfigured.
+  std::uint64_t state_key = 0;
   int n_agents() const;
 };
 
@@ -130,6 +137,15 @@ Trajectory simulate_forward(const Scenario& s, const LinkParams& params,
 std::vector<Trajectory> simulate_forward_draws(
     const Scenario& s, const LinkParams& params, const RngStream& rng,
     const std::vector<std::uint64_t>& noise_iterations, bool record_states = false);
+
+/// The device run behind simulate_forward_draws without the host-side
+/// Trajectory: returns the context holding the results (read them with
+/// dtg_read_cum_all / dtg_read_state).  Used by the level-2 C-ABI so results
+/// land directly in the caller's buffers.
+::dtg_ctx* simulate_forward_device(const Scenario& s, const LinkParams& params,
+                                        const RngStream& rng,
+                                        const std::vector<std::uint64_t>& noise_iterations,
+                                        bool record_states = false);
 
 /// What a loss sees (engine.hpp:82-87) ...
 struct LossInputs {

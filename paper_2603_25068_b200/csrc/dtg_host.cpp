@@ -6,6 +6,7 @@
 // be contracted into an FMA or parameters differ from the reference in the
 // last bit.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <limits>
@@ -364,6 +365,9 @@ struct CacheEntry {
   std::vector<double> len;
   SimConfig cfg;
   int N = 0, B = 0;
+  // what the context holds, so unchanged inputs are not uploaded again
+  std::uint64_t state_key = 0;
+  std::vector<double> params;  // [5][L] of the last upload (all scenarios)
 };
 
 thread_local std::vector<CacheEntry> g_cache;
@@ -396,6 +400,20 @@ dtg_ctx* context_for(const Scenario& s, int N, int B, int T) {
   return g_last_ctx = c;
 }
 
+CacheEntry* entry_for(dtg_ctx* c) {
+  for (auto& e : g_cache)
+    if (e.ctx.get() == c) return &e;
+  return nullptr;
+}
+
+/// Forget what a context holds (its state / parameters were set directly).
+void invalidate(dtg_ctx* c) {
+  if (CacheEntry* e = entry_for(c)) {
+    e->state_key = 0;
+    e->params.clear();
+  }
+}
+
 }  // namespace detail
 
 namespace {
@@ -415,8 +433,7 @@ struct Prepared {
 Prepared prepare(const Scenario& s, const LinkParams& params, const RngStream& rng,
                  const std::vector<std::uint64_t>& its) {
   const int spi = steps_per_interval(s);
-  const InitialState init = seed_agents(s);
-  const int N = static_cast<int>(init.link.size());
+  const int N = s.n_agents();
   const int L = s.net.n_links();
   const int B = static_cast<int>(its.size());
   if (B < 1) throw std::runtime_error("no noise draws");
@@ -427,9 +444,29 @@ Prepared prepare(const Scenario& s, const LinkParams& params, const RngStream& r
   if (s.net.succ_off.size() != static_cast<std::size_t>(L + 1))
     throw std::runtime_error("network CSR is stale (call rebuild_csr)");
   dtg_ctx* c = detail::context_for(s, N, B, s.horizon_steps);
-  check(c, dtg_set_params(c, -1, params.u.data(), params.kappa.data(), params.beta.data(),
-                          params.alpha.data(), params.cost.data()));
-  check(c, dtg_set_state(c, -1, init.link.data(), init.pos.data()));
+  detail::CacheEntry* e = detail::entry_for(c);
+  const std::size_t Ls = static_cast<std::size_t>(L);
+  const bool same_params =
+      e && e->params.size() == 5 * Ls &&
+      std::equal(params.u.begin(), params.u.end(), e->params.begin()) &&
+      std::equal(params.kappa.begin(), params.kappa.end(), e->params.begin() + Ls) &&
+      std::equal(params.beta.begin(), params.beta.end(), e->params.begin() + 2 * Ls) &&
+      std::equal(params.alpha.begin(), params.alpha.end(), e->params.begin() + 3 * Ls) &&
+      std::equal(params.cost.begin(), params.cost.end(), e->params.begin() + 4 * Ls);
+  if (!same_params) {
+    check(c, dtg_set_params(c, -1, params.u.data(), params.kappa.data(), params.beta.data(),
+                            params.alpha.data(), params.cost.data()));
+    if (e) {
+      e->params.clear();
+      for (const auto* v : {&params.u, &params.kappa, &params.beta, &params.alpha, &params.cost})
+        e->params.insert(e->params.end(), v->begin(), v->end());
+    }
+  }
+  if (!e || s.state_key == 0 || e->state_key != s.state_key) {
+    const InitialState init = seed_agents(s);
+    check(c, dtg_set_state(c, -1, init.link.data(), init.pos.data()));
+    if (e) e->state_key = s.state_key;
+  }
   for (int b = 0; b < B; ++b) check(c, dtg_set_noise(c, b, rng.seed(), its[b]));
   return {c, N, L, B, s.horizon_steps, spi};
 }
@@ -478,6 +515,13 @@ std::vector<Trajectory> simulate_forward_draws(const Scenario& s, const LinkPara
   const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
   for (auto& tr : out) tr.wall_seconds = wall;
   return out;
+}
+
+dtg_ctx* simulate_forward_device(const Scenario& s, const LinkParams& params, const RngStream& rng,
+                                 const std::vector<std::uint64_t>& its, bool record_states) {
+  const Prepared p = prepare(s, params, rng, its);
+  check(p.ctx, dtg_forward(p.ctx, p.T, p.spi, record_states ? 1 : 0));
+  return p.ctx;
 }
 
 Trajectory simulate_forward(const Scenario& s, const LinkParams& params, const RngStream& rng,
@@ -719,6 +763,7 @@ class DeviceLoop {
     if (ex && world > 1 && (!ex->d_local || !ex->d_full || !ex->gather))
       throw std::invalid_argument("draw exchange needs d_local, d_full and gather");
     ctx_ = detail::context_for(s, N_, local_, s.horizon_steps);
+    detail::invalidate(ctx_);  // state and parameters are set directly below
     if (ex && ex->stream) check(ctx_, dtg_set_stream(ctx_, ex->stream));
     check(ctx_, dtg_set_state(ctx_, -1, init.link.data(), init.pos.data()));
     red_.resize(5 * static_cast<std::size_t>(L_) + 2);
@@ -935,6 +980,12 @@ struct dtg_scenario {
   dtg::Scenario s;
   std::string err;
   dtg_ctx* last_ctx = nullptr;
+  dtg_scenario() { touch(); }
+  /// New initial-state key after any change to the scenario.
+  void touch() {
+    static std::atomic<std::uint64_t> next{1};
+    s.state_key = next.fetch_add(1);
+  }
 };
 
 namespace {
@@ -1031,6 +1082,7 @@ int dtg_scenario_configure(dtg_scenario* sc, int n_vehicles, int delta_n, double
                            double gumbel_tau, int tg, int horizon_steps, int obs_interval_s,
                            int fit_queues) {
   return scn_guard(sc, [&] {
+    sc->touch();
     sc->s.n_vehicles = n_vehicles;
     sc->s.cfg.delta_n = delta_n;
     sc->s.cfg.tau = tau;
@@ -1044,6 +1096,7 @@ int dtg_scenario_configure(dtg_scenario* sc, int n_vehicles, int delta_n, double
 
 int dtg_scenario_custom_init(dtg_scenario* sc, int n, const int* link, const double* pos) {
   return scn_guard(sc, [&] {
+    sc->touch();
     sc->s.custom_init.clear();
     for (int i = 0; i < n; ++i) sc->s.custom_init.push_back({link[i], pos[i]});
   });
@@ -1116,31 +1169,34 @@ int dtg_simulate_forward(dtg_scenario* sc, const double* u, const double* k, con
                          double* pos_final, int* states_link, double* states_pos,
                          double* wall_seconds) {
   return scn_guard(sc, [&] {
+    const auto t0 = std::chrono::steady_clock::now();
     const int L = sc->s.net.n_links();
     const std::vector<std::uint64_t> iv(its, its + n_draws);
-    const auto trs = dtg::simulate_forward_draws(sc->s, make_params(L, u, k, b, a, c),
-                                                 dtg::RngStream(root_seed), iv,
-                                                 states_link != nullptr);
-    sc->last_ctx = dtg::detail::g_last_ctx;
+    // results go straight from the device into the caller's buffers
+    // ([D][T][L] counts are exactly dtg_read_cum_all's layout)
+    dtg_ctx* ctx = dtg::simulate_forward_device(sc->s, make_params(L, u, k, b, a, c),
+                                                dtg::RngStream(root_seed), iv, states_link != nullptr);
+    sc->last_ctx = ctx;
     const int T = sc->s.horizon_steps;
+    const std::size_t N = static_cast<std::size_t>(sc->s.n_agents());
+    auto ok = [&](int rc) {
+      if (rc != DTG_OK) throw std::runtime_error(dtg_last_error(ctx));
+    };
+    if (cum_per_step && T) ok(dtg_read_cum_all(ctx, cum_per_step));
     for (int d = 0; d < n_draws; ++d) {
-      const auto& tr = trs[d];
-      const std::size_t N = tr.final_state.link.size();
-      if (cum_per_step)
-        for (int t = 0; t < T; ++t)
-          std::copy(tr.cum_per_step[t].begin(), tr.cum_per_step[t].end(),
-                    cum_per_step + (static_cast<std::size_t>(d) * T + t) * L);
-      if (link_final) std::copy(tr.final_state.link.begin(), tr.final_state.link.end(), link_final + d * N);
-      if (pos_final) std::copy(tr.final_state.pos.begin(), tr.final_state.pos.end(), pos_final + d * N);
+      if (link_final || pos_final) {
+        std::vector<int> lk(link_final ? 0 : N);
+        std::vector<double> ps(pos_final ? 0 : N);
+        ok(dtg_read_state(ctx, d, T, link_final ? link_final + d * N : lk.data(),
+                          pos_final ? pos_final + d * N : ps.data()));
+      }
       if (states_link)
-        for (int t = 0; t < T; ++t) {
-          std::copy(tr.states[t].link.begin(), tr.states[t].link.end(),
-                    states_link + (static_cast<std::size_t>(d) * T + t) * N);
-          std::copy(tr.states[t].pos.begin(), tr.states[t].pos.end(),
-                    states_pos + (static_cast<std::size_t>(d) * T + t) * N);
-        }
-      if (wall_seconds) *wall_seconds = tr.wall_seconds;
+        for (int t = 1; t <= T; ++t)
+          ok(dtg_read_state(ctx, d, t, states_link + (static_cast<std::size_t>(d) * T + t - 1) * N,
+                            states_pos + (static_cast<std::size_t>(d) * T + t - 1) * N));
     }
+    if (wall_seconds)
+      *wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
 
@@ -1223,7 +1279,11 @@ int dtg_simulate_gradient_mse(dtg_scenario* sc, const double* u, const double* k
                          nullptr, nullptr, nullptr, nullptr, nullptr);
 }
 
-dtg_ctx* dtg_scenario_ctx(dtg_scenario* sc) { return sc->last_ctx; }
+dtg_ctx* dtg_scenario_ctx(dtg_scenario* sc) {
+  // the caller may change the context's state / parameters directly
+  if (sc->last_ctx) dtg::detail::invalidate(sc->last_ctx);
+  return sc->last_ctx;
+}
 
 int dtg_mse_loss(int k_snap, int n_links, const double* snapshots, int n_obs, const int* obs_ids,
                  int k_obs, const double* obs_values, int delta_n, double* loss, double* seeds) {
