@@ -116,3 +116,30 @@ def test_c3_dn1_million_agents(port):
     tr = P.simulate_forward(sc, p, seed=7)
     ref = port_of(port, sc).forward(p, 7, 0)
     assert_forward_equal(tr, ref)
+
+
+def test_context_reuse_state_and_param_caching(port):
+    """Scenarios sharing a cached device context (same network, agent count and
+    config) and alternating parameter sets: every call must see its own
+    initial state and parameters (the upload cache keys on both)."""
+    seeded = P.Scenario.grid(3, 300.0, 42, 600.0).configure(300, 1, 90, 30, fit_queues=False)
+    lk, ps = seeded.seed_agents()
+    rng = np.random.default_rng(0)
+    ps2 = np.minimum(ps, rng.uniform(0.0, 1.0, size=len(ps)) * 300.0)
+    a = P.Scenario.grid(3, 300.0, 42, 600.0).configure(0, 1, 90, 30, fit_queues=False, custom_init=(lk, ps))
+    b = P.Scenario.grid(3, 300.0, 42, 600.0).configure(0, 1, 90, 30, fit_queues=False, custom_init=(lk, ps2))
+    assert np.array_equal(a.links()[2], b.links()[2])  # same network -> one shared device context
+    p1 = a.sample_parameters(3)
+    p2 = a.sample_parameters(4)
+    ref = {}
+    for name, sc in (("a", a), ("b", b)):
+        for pn, p in (("1", p1), ("2", p2)):
+            ref[name + pn] = port_of(port, sc).forward(p, 7, 0)
+    for key in ("a1", "b1", "a2", "b2", "a1", "a2", "b2", "b1"):
+        sc = a if key[0] == "a" else b
+        p = p1 if key[1] == "1" else p2
+        assert_forward_equal(P.simulate_forward(sc, p, seed=7), ref[key])
+    assert a.device_context() == b.device_context()  # the cache really was shared
+    # reconfiguring a scenario (new initial state) invalidates what the context holds
+    a.configure(0, 1, 90, 30, fit_queues=False, custom_init=(lk, ps2))
+    assert_forward_equal(P.simulate_forward(a, p1, seed=7), ref["b1"])
