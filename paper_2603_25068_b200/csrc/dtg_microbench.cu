@@ -44,6 +44,55 @@ __global__ void k_micro(int which, int n, const int* chain, double* out) {
       for (int i = 0; i < n; ++i) acc += rng_uniform(static_cast<std::uint64_t>(acc > 1e300), 3, i, 7);
       break;
     }
+    case 6: {  // dependent straight-line Gumbel draws
+      int bad = 0;
+      for (int i = 0; i < n; ++i)
+        acc += gumbel_sl(rng_final(static_cast<std::uint64_t>(acc > 1e300), static_cast<std::uint64_t>(i)), bad);
+      acc += bad;
+      break;
+    }
+    case 7: {  // five independent straight-line Gumbel draws per iteration (cycles per 5)
+      int bad = 0;
+      for (int i = 0; i < n; ++i) {
+        const std::uint64_t h = static_cast<std::uint64_t>(acc > 1e300);
+        double g0 = gumbel_sl(rng_final(h, 5ull * i), bad), g1 = gumbel_sl(rng_final(h, 5ull * i + 1), bad),
+               g2 = gumbel_sl(rng_final(h, 5ull * i + 2), bad), g3 = gumbel_sl(rng_final(h, 5ull * i + 3), bad),
+               g4 = gumbel_sl(rng_final(h, 5ull * i + 4), bad);
+        acc += g0 + g1 + g2 + g3 + g4;
+      }
+      acc += bad;
+      break;
+    }
+    case 10: {  // five straight-line Gumbel draws per iteration, interleaved stage by stage
+      int bad = 0;
+      for (int i = 0; i < n; ++i) {
+        const std::uint64_t h = static_cast<std::uint64_t>(acc > 1e300);
+        std::uint64_t hh[5], cc[5], b[5];
+        double g[5];
+        for (int q = 0; q < 5; ++q) {
+          hh[q] = h;
+          cc[q] = 5ull * i + q;
+        }
+        rng_final_v<5>(hh, cc, b);
+        gumbel_sl_v<5>(b, g, bad);
+        acc += g[0] + g[1] + g[2] + g[3] + g[4];
+      }
+      acc += bad;
+      break;
+    }
+    case 8: {  // dependent straight-line log
+      int bad = 0;
+      double x = 1.5;
+      for (int i = 0; i < n; ++i) x = log_sl(x + 2.0, bad);
+      acc = x + bad;
+      break;
+    }
+    case 9: {  // dependent rng_final (integer mixes only)
+      std::uint64_t h = 1;
+      for (int i = 0; i < n; ++i) h = rng_final(h, static_cast<std::uint64_t>(i));
+      acc = static_cast<double>(h & 1023);
+      break;
+    }
   }
   long long t1 = clock64();
   out[0] = static_cast<double>(t1 - t0) / n;
@@ -102,6 +151,16 @@ __global__ void k_log_check(std::uint64_t seed, long long n, unsigned long long*
     const double v = -log(u);
     if (__double_as_longlong(log_sl(v, bad)) != __double_as_longlong(log(v))) ++mism;
     if (__double_as_longlong(gumbel_sl(b, bad)) != __double_as_longlong(gumbel_bits(b))) ++mism;
+    {
+      std::uint64_t hv[3] = {b, b ^ 0x1234567ULL, seed}, cv[3] = {1ull * i, 7ull, 11ull * i}, bv[3];
+      double gv[3];
+      rng_final_v<3>(hv, cv, bv);
+      gumbel_sl_v<3>(bv, gv, bad);
+      for (int q = 0; q < 3; ++q)
+        if (bv[q] != rng_final(hv[q], cv[q]) ||
+            __double_as_longlong(gv[q]) != __double_as_longlong(gumbel_bits(rng_final(hv[q], cv[q]))))
+          ++mism;
+    }
     // random positive normal double: exponent field in [1, 2046]
     const std::uint64_t r = rng_bits(seed ^ 0x5bd1e995ULL, static_cast<std::uint64_t>(i), 5, 9);
     const std::uint64_t ex = 1 + (r >> 52) % 2046;

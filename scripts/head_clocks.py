@@ -13,5 +13,5 @@ out = (C.c_ulonglong * 8)()
 fn(out)
 e.forward(120, 10); e.sync()
 fn(out)
-n = out[4]
-print("heads", n, "cycles/head: draws", out[0] / n, "softmax", out[1] / n, "merge draw", out[2] / n, "atomic+store", out[3] / n)
+
+n = out[5]; print("heads", n, "cyc/head: loads", out[0] / n, "draws", out[1] / n, "argmax", out[2] / n, "merge draw", out[3] / n, "atomic+store", out[4] / n)
