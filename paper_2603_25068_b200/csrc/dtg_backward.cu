@@ -339,6 +339,26 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               if (lane == 31 && r + 1 < n) fa_n = cf_step(xf[q], x - xf[q], jam, dxf, len).x1 >= thr;
             }
             const bool fdown = __shfl_down_sync(0xffffffffu, fa, 1);
+            // arrived list and A[0] key: one atomic per warp (warp-aggregated)
+            const bool arr = on && fa;
+            const int a = arr ? d.aid[so + k] : 0;
+            int qa = 0;
+            const unsigned am = __ballot_sync(0xffffffffu, arr);
+            if (am && !(V.dbg & 4)) {
+              const int leader = __ffs(am) - 1;
+              int base = 0;
+              if (lane == leader) base = atomicAdd(&V.acount[par * d.B + b], __popc(am));
+              base = __shfl_sync(0xffffffffu, base, leader);
+              qa = base + __popc(am & ((1u << lane) - 1u));
+              unsigned long long key =
+                  arr ? ((static_cast<unsigned long long>(a) << 32) | static_cast<unsigned>(k)) : ULLONG_MAX;
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+                key = other < key ? other : key;
+              }
+              if (lane == leader) atomicMin(&V.a0key[par * d.B + b], key);
+            }
             if (!on) continue;
             if (lane < 31) fa_n = r + 1 < n && fdown;
             V.x1[bn + k] = x1;
@@ -353,13 +373,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
             if (r == n - 1) V.tail[bl + j] = x1;
             if (fa) {
               V.won[bn + k] = 0;
-              const int a = d.aid[so + k];
-              if (!(V.dbg & 4)) {
-                const int qa = atomicAdd(&V.acount[par * d.B + b], 1);
-                V.alist[bn + qa] = k;
-                atomicMin(&V.a0key[par * d.B + b],
-                          (static_cast<unsigned long long>(a) << 32) | static_cast<unsigned>(k));
-              }
+              if (!(V.dbg & 4)) V.alist[bn + qa] = k;
               if (defer) {
                 const int hi = atomicAdd(hcnt, 1);
                 if (hi < kHeadCap) {
