@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         const double* xbn = V.xbar + static_cast<std::size_t>(par ^ 1) * d.B * N + bn;
         double* xbc = V.xbar + static_cast<std::size_t>(par) * d.B * N + bn;
         // merge rows
-        for (int i = spread(tid, lg, nblk); i < L; i += nblk * kBT) {
+        for (int i = spread(tid, lg, nblk); i < L && !(V.dbg & 64); i += nblk * kBT) {
           const int w = V.win[bl + i];
           if (w < 0) continue;
           const int cnt = V.ccnt[bl + i];
@@ -705,18 +705,20 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
             V.prio_bar[bn + s] = 0.0 + bar[e] * 1.0;
           }
         }
-        // A[0] rows: warp e of CTA 0 merges row e's per-CTA partials
-        if (lg == 0 && tid < d.maxdeg) V.lbar_a0[static_cast<std::size_t>(b) * d.maxdeg + tid] = 0.0;
-        __syncthreads();
-        const unsigned long long key = V.a0key[par * d.B + b];
-        if (lg == 0 && key != ULLONG_MAX) {
+        // A[0] rows: warp e of the scenario's last CTA (the one with the fewest
+        // slots in the interleaved mapping) merges row e's per-CTA partials and
+        // writes lbar_a0[e] (0 for rows that take no A[0] routing)
+        const unsigned long long key = lg == nblk - 1 ? V.a0key[par * d.B + b] : ULLONG_MAX;
+        if (lg == nblk - 1 && key != ULLONG_MAX && !(V.dbg & 128) && wid < d.maxdeg) {
           const int a0s = static_cast<int>(key & 0xffffffffull);
           const int c0 = d.lnk[so + a0s];
           const int s0 = d.succ_off[c0], deg0 = d.succ_off[c0 + 1] - s0;
           const int e = wid;
+          bool routed = false;
           if (e < deg0) {
             const int i = d.succ[s0 + e];
-            if (V.vac[bl + i] && V.win[bl + i] < 0) {
+            routed = V.vac[bl + i] && V.win[bl + i] < 0;
+            if (routed) {
               const T2* ap = static_cast<const T2*>(V.a0part);
               T2 x{-INFINITY, -INFINITY, INT_MAX, -1};
               for (int g2 = lane; g2 < nblk; g2 += 32)
@@ -784,13 +786,14 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               }
             }
           }
+          if (!routed && lane == 0) V.lbar_a0[static_cast<std::size_t>(b) * d.maxdeg + e] = 0.0;
         }
         // position adjoint of layout t: kB3 slots per thread in flight; the
         // follower's headway term is the follower lane's own gap adjoint
         // (lanes are consecutive slots), so only a warp's last lane evaluates
         // its follower's x1 adjoint itself.
         const int stride3 = nblk * kBT;
-        for (int k0 = lg * kBT + tid; k0 - lane < N; k0 += kB3 * stride3) {
+        for (int k0 = lg * kBT + tid; k0 - lane < N && !(V.dbg & 256); k0 += kB3 * stride3) {
           int kk[kB3], jj[kB3], rr[kB3], nn[kB3];
           double xx[kB3], xp[kB3], xf[kB3];
 #pragma unroll
