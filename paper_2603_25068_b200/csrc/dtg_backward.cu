@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         const unsigned long long key = V.a0key[par * d.B + b];
         const int a0s = key == ULLONG_MAX ? -1 : static_cast<int>(key & 0xffffffffull);
         const int nA = V.acount[par * d.B + b];
-        for (int q = spread(tid, lg, nblk); q < nA; q += nblk * kBT) {
+        for (int q = spread(tid, lg, nblk); q < nA && !(V.dbg & 512); q += nblk * kBT) {
           const int s = V.alist[bn + q];
           const int c = V.choice[bn + s];
           if (c < 0) continue;
@@ -916,71 +916,30 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         }
         // warp per link: u, kappa, alpha for step t
         double* g5 = V.grads + static_cast<std::size_t>(b) * 5 * L;
-        // warp per link for the segment sums (fixed xor tree); the per-link
-        // epilogues (parameter loads, gradient updates, alpha over the arrived
-        // prefix) of up to 32 links then run in parallel, one per lane.
-        const int nw = nblk * (kBT / 32);
-        const int j0w = lg * (kBT / 32) + wid;
-        const int nmine = j0w < L ? (L - 1 - j0w) / nw + 1 : 0;
-        for (int i0 = 0; i0 < nmine; i0 += 32) {
-          int my_j = -1;
-          double my_ub = 0.0, my_jb = 0.0;
-          const int cnt = min(32, nmine - i0);
-          // software pipeline: the next link's first 32 elements load while
-          // this link reduces
-          int jn = j0w + i0 * nw;
-          int bsn = offT[jn], nsn = offT[jn + 1] - bsn;
-          double pcu = lane < nsn ? V.cu[bn + bsn + lane] : 0.0;
-          double pcg = lane < nsn ? V.cg[bn + bsn + lane] : 0.0;
-          for (int u = 0; u < cnt; ++u) {
-            const int j = jn, base = bsn, n = nsn;
-            const double cu0 = pcu, cg0 = pcg;
-            if (u + 1 < cnt) {
-              jn = j + nw;
-              bsn = offT[jn];
-              nsn = offT[jn + 1] - bsn;
-              pcu = lane < nsn ? V.cu[bn + bsn + lane] : 0.0;
-              pcg = lane < nsn ? V.cg[bn + bsn + lane] : 0.0;
-            }
-            double ub = 0.0, jb = 0.0;
-            if (lane < n) {
-              ub += cu0;
-              jb += -1.0 * cg0;
-            }
-            for (int k = base + 32 + lane; k < base + n; k += 32) {
-              ub += V.cu[bn + k];
-              jb += -1.0 * V.cg[bn + k];
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              ub += __shfl_xor_sync(0xffffffffu, ub, o);
-              jb += __shfl_xor_sync(0xffffffffu, jb, o);
-            }
-            if (lane == u) {
-              my_j = j;
-              my_ub = ub;
-              my_jb = jb;
-            }
+        // thread per link (links dealt in 32-lane groups over the CTAs): the
+        // segment sums run in slot order; the parameter loads of the epilogue
+        // are issued together
+        for (int j = spread(tid, lg, nblk); j < L && !(V.dbg & 1024); j += nblk * kBT) {
+          const int base = offT[j], n = offT[j + 1] - base;
+          const double kap = d.kappa[bl + j];
+          const double g0 = g5[j], g1 = g5[L + j], g3 = g5[3 * L + j];
+          const int na = n ? V.nA_cur[bl + j] : 0;
+          double ub = 0.0, jb = 0.0;
+          for (int k = base; k < base + n; ++k) {
+            ub += V.cu[bn + k];
+            jb += -1.0 * V.cg[bn + k];
           }
-          if (my_j >= 0) {
-            const int j = my_j;
-            const int base = offT[j], n = offT[j + 1] - base;
-            const double kap = d.kappa[bl + j];
-            if (n) {
-              g5[j] += 0.0 + my_ub;
-              g5[L + j] += 0.0 - my_jb * static_cast<double>(d.delta_n) / (kap * kap);
-            }
-            double ab = 0.0;
-            if (n) {
-              const int na = V.nA_cur[bl + j];
-              for (int r = 0; r < na; ++r) {
-                const int s = base + r;
-                const int ch = V.choice[bn + s];
-                if (ch >= 0 && V.vac[bl + ch] && V.win[bl + ch] >= 0) ab += 1.0 * V.prio_bar[bn + s];
-              }
-            }
-            g5[3 * L + j] += ab;
+          if (n) {
+            g5[j] = g0 + (0.0 + ub);
+            g5[L + j] = g1 + (0.0 - jb * static_cast<double>(d.delta_n) / (kap * kap));
           }
+          double ab = 0.0;
+          for (int r = 0; r < na; ++r) {
+            const int s = base + r;
+            const int ch = V.choice[bn + s];
+            if (ch >= 0 && V.vac[bl + ch] && V.win[bl + ch] >= 0) ab += 1.0 * V.prio_bar[bn + s];
+          }
+          g5[3 * L + j] = g3 + ab;
         }
         for (int i = lg * kBT + tid; i < L; i += nblk * kBT) {
           V.ccnt[bl + i] = 0;

@@ -21,7 +21,7 @@
 //   k_adj_choice  per link: link-choice VJP of the arrived heads.
 //   k_adj_slot    per slot: transfer pass-through, counting sigmoid VJP,
 //                 car-following VJP with the follower's headway term.
-//   k_adj_link    warp per link: deterministic per-link reductions into the
+//   k_adj_link    thread per link: deterministic per-link reductions into the
 //                 u, kappa, beta, alpha, cost gradients.
 // All fp64 with -fmad=false: the forward is bit-identical to the reference.
 #include <climits>
@@ -668,24 +668,18 @@ __global__ void __launch_bounds__(256) k_adj_slot(DevView d, int s_cur, int s_ne
 
 __global__ void __launch_bounds__(256) k_adj_link(DevView d, int s_cur) {
   const int b = blockIdx.y;
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d.L) return;
   const std::size_t bl = static_cast<std::size_t>(b) * d.L;
   const std::size_t bn = static_cast<std::size_t>(b) * d.N;
   const int* off = d.off + oidx(d, s_cur, b);
   const int base = off[j], n = off[j + 1] - base;
+  // deterministic: each link's slots summed in slot order by one thread
   double ub = 0.0, jb = 0.0;
-  for (int k = base + lane; k < base + n; k += 32) {
+  for (int k = base; k < base + n; ++k) {
     ub += d.cu[bn + k];
     jb += -1.0 * d.cg[bn + k];
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {  // fixed xor tree: deterministic
-    ub += __shfl_xor_sync(0xffffffffu, ub, o);
-    jb += __shfl_xor_sync(0xffffffffu, jb, o);
-  }
-  if (lane) return;
   double* g = d.grads + static_cast<std::size_t>(b) * 5 * d.L;
   const double kap = d.kappa[bl + j];
   if (n) {
@@ -817,7 +811,7 @@ void launch_bwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
       k_adj_slot<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s_cur, s_next, xbar_next, xbar_cur);
       break;
     default:
-      k_adj_link<<<grid_n(d.L * 32, 256, d.B), 256, 0, st>>>(d, s_cur);
+      k_adj_link<<<grid_n(d.L, 256, d.B), 256, 0, st>>>(d, s_cur);
   }
 }
 
