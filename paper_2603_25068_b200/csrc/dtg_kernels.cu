@@ -32,6 +32,8 @@
 
 namespace dtg {
 
+constexpr int kFastSucc = 5;  // successor / candidate counts up to this use register fast paths
+
 // ---------------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------------
@@ -75,13 +77,36 @@ __global__ void __launch_bounds__(256) k_step_cf(DevView d, int t, int s_cur) {
     int c = -1;
     const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
     if (deg > 0) {  // link_choice (node_model.cpp:45-97)
-      double g[kMaxDeg], pi[kMaxDeg];
       const int agent = d.aid[so + k];
       const double* lz = d.slogz + (static_cast<std::size_t>(b) * d.L + j) * d.maxdeg;
-      for (int e = 0; e < deg; ++e)
-        g[e] = gumbel(d.seed_link[b], static_cast<std::uint64_t>(t),
-                      static_cast<std::uint64_t>(agent), static_cast<std::uint64_t>(d.succ[s0 + e]));
-      c = d.succ[s0 + softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi)];
+      if (deg <= kFastSucc) {  // registers, straight-line logs, argmax from the logits
+        const std::uint64_t h2 = rng_prefix2(rng_prefix1(d.seed_link[b], static_cast<std::uint64_t>(t)),
+                                             static_cast<std::uint64_t>(agent));
+        int sj[kFastSucc];
+        double y[kFastSucc], ex[kFastSucc];
+        int bad = 0;
+#pragma unroll
+        for (int e = 0; e < kFastSucc; ++e) {
+          sj[e] = d.succ[s0 + (e < deg ? e : 0)];
+          y[e] = (lz[e < deg ? e : 0] + gumbel_sl(rng_final(h2, static_cast<std::uint64_t>(sj[e])), bad)) * d.kinv;
+        }
+        if (bad) {
+#pragma unroll
+          for (int e = 0; e < kFastSucc; ++e)
+            y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2, static_cast<std::uint64_t>(sj[e])))) * d.kinv;
+        }
+        const int best = softmax_first_argmax<kFastSucc>(deg, y, ex);
+        c = sj[0];
+#pragma unroll
+        for (int e = 1; e < kFastSucc; ++e)
+          if (e == best) c = sj[e];
+      } else {
+        double g[kMaxDeg], pi[kMaxDeg];
+        for (int e = 0; e < deg; ++e)
+          g[e] = gumbel(d.seed_link[b], static_cast<std::uint64_t>(t),
+                        static_cast<std::uint64_t>(agent), static_cast<std::uint64_t>(d.succ[s0 + e]));
+        c = d.succ[s0 + softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi)];
+      }
     }
     d.choice[bn + k] = c;
   }
@@ -131,7 +156,37 @@ __device__ __forceinline__ int gather_candidates(const DevView& d, int b, int i,
 
 __device__ __forceinline__ int merge_softmax(const DevView& d, int b, int t, int i,
                                              int nc, const int* cid, const int* clink,
-                                             double* lz, double* pi) {
+                                             double* lz, double* pi, bool need_pi = true) {
+  if (!need_pi && nc <= kFastSucc) {  // registers; first stage exact, winner from the logits
+    const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+    const std::uint64_t h2 = rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
+                                         static_cast<std::uint64_t>(i));
+    double v[kFastSucc], y[kFastSucc], ex[kFastSucc];
+    int bad = 0;
+#pragma unroll
+    for (int e = 0; e < kFastSucc; ++e) {
+      v[e] = e < nc ? d.alpha[bl + clink[e]] : 0.0;
+      if (e < nc && v[e] == 0.0) atomicOr(&d.err[b], kErrZeroAlpha);
+      y[e] = e < nc ? gumbel_sl(rng_final(h2, static_cast<std::uint64_t>(cid[e])), bad) : 0.0;
+    }
+    if (bad) {
+#pragma unroll
+      for (int e = 0; e < kFastSucc; ++e)
+        y[e] = e < nc ? gumbel_bits(rng_final(h2, static_cast<std::uint64_t>(cid[e]))) : 0.0;
+    }
+    double m = v[0];
+#pragma unroll
+    for (int e = 1; e < kFastSucc; ++e)
+      if (e < nc && m < v[e]) m = v[e];
+    double z = 0.0;
+#pragma unroll
+    for (int e = 0; e < kFastSucc; ++e)
+      if (e < nc) z += exp(v[e] - m);
+    const double lzz = log(z) + m;
+#pragma unroll
+    for (int e = 0; e < kFastSucc; ++e) y[e] = ((v[e] - lzz) + y[e]) * d.kinv;
+    return softmax_first_argmax<kFastSucc>(nc, y, ex);
+  }
   double v[kMaxCand], g[kMaxCand];
   const std::size_t bl = static_cast<std::size_t>(b) * d.L;
   for (int e = 0; e < nc; ++e) {
@@ -167,7 +222,7 @@ __global__ void __launch_bounds__(128) k_step_merge(DevView d, int t, int s_cur,
     const int nc = gather_candidates(d, b, i, off, so, cid, cslot, clink);
     if (nc) {
       double lz[kMaxCand], pi[kMaxCand];
-      w = cslot[merge_softmax(d, b, t, i, nc, cid, clink, lz, pi)];
+      w = cslot[merge_softmax(d, b, t, i, nc, cid, clink, lz, pi, false)];
       d.won[static_cast<std::size_t>(b) * d.N + w] = 1;
     }
   }
