@@ -126,13 +126,15 @@ __device__ __forceinline__ int pull_f(int j, int rn, const int* offA, const int*
   return ob;
 }
 
+// Exclusive scan of v[0..n) in place, v[n] = total; two CTA barriers: every
+// warp scans the warp totals itself instead of waiting for warp 0 to do it.
 __device__ void scan_f(int* v, int n, int* tmp) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int per = (n + nt - 1) / nt;
   const int j0 = min(n, tid * per), j1 = min(n, j0 + per);
   int s = 0;
   for (int j = j0; j < j1; ++j) s += v[j];
-  const int lane = tid & 31, wid = tid >> 5;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
   int x = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -141,19 +143,15 @@ __device__ void scan_f(int* v, int n, int* tmp) {
   }
   if (lane == 31) tmp[wid] = x;
   __syncthreads();
-  if (wid == 0) {
-    int w = lane < (nt >> 5) ? tmp[lane] : 0;
+  int wt = lane < nw ? tmp[lane] : 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
-    }
-    tmp[lane] = w;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, wt, o);
+    if (lane >= o) wt += y;
   }
-  __syncthreads();
-  int run = (wid ? tmp[wid - 1] : 0) + x - s;
-  const int total = tmp[(nt >> 5) - 1];
-  __syncthreads();
+  const int before = __shfl_sync(0xffffffffu, wt, wid > 0 ? wid - 1 : 0);
+  const int total = __shfl_sync(0xffffffffu, wt, nw - 1);
+  int run = (wid ? before : 0) + x - s;
   for (int j = j0; j < j1; ++j) {
     const int c = v[j];
     v[j] = run;
@@ -283,14 +281,30 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
         offB = sw;
         const int* nAp = V.nAb + prv * BL + bl;
         const int* depp = V.depb + prv * BL + bl;
-#pragma unroll 8
-        for (int j = threadIdx.x; j < L; j += blockDim.x) {
-          const int nold = offA[j + 1] - offA[j];
-          const int na = nAp[j], dpv = depp[j], w = V.win[bl + j];
-          na_s[j] = nold ? na : 0;
-          dep_s[j] = dpv;
-          win_s[j] = w;
-          offB[j] = nold - dpv + (w >= 0 ? 1 : 0);
+        // all global loads of this thread's links first (one memory latency),
+        // then the shared-memory updates
+        constexpr int kPro = 8;
+        for (int j0 = threadIdx.x; j0 < L; j0 += kPro * blockDim.x) {
+          int na_r[kPro], dp_r[kPro], w_r[kPro];
+#pragma unroll
+          for (int u = 0; u < kPro; ++u) {
+            const int j = j0 + u * blockDim.x;
+            const bool on = j < L;
+            na_r[u] = on ? nAp[j] : 0;
+            dp_r[u] = on ? depp[j] : 0;
+            w_r[u] = on ? V.win[bl + j] : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < kPro; ++u) {
+            const int j = j0 + u * blockDim.x;
+            if (j < L) {
+              const int nold = offA[j + 1] - offA[j];
+              na_s[j] = nold ? na_r[u] : 0;
+              dep_s[j] = dp_r[u];
+              win_s[j] = w_r[u];
+              offB[j] = nold - dp_r[u] + (w_r[u] >= 0 ? 1 : 0);
+            }
+          }
         }
         __syncthreads();
         scan_f(offB, L, tmp);
