@@ -355,15 +355,36 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
       }
       if (V.wstamp) wt1 = gnow();
       const int lane = threadIdx.x & 31;
-      for (int k0 = off0 + static_cast<int>(threadIdx.x); k0 - lane < limit; k0 += kBatch * stride) {
+      // Interleaved mapping: warp gw takes 32 * kBatch consecutive slots per
+      // iteration (chunks dealt round-robin over all warps of the scenario),
+      // so after one binary search the next sub-chunks' links are reached by a
+      // short forward walk.  Contiguous mapping: the CTA's range as before.
+      // (Used for long links, N >= 32 L; with short links the walk costs more
+      // than the search and the 512-slot blocks spread heads better.)
+      const bool chunked = !V.contig && N >= 32 * L;
+      const int wpc = blockDim.x >> 5;
+      const int span = chunked ? 32 * kBatch : kBatch * stride;
+      const int cstep = chunked ? V.cs * wpc : 1;
+      const int c0 = chunked ? rank * wpc + (threadIdx.x >> 5) : 0;
+      for (int c = c0;; c += cstep) {
+        const int k0 = chunked ? c * span + lane : off0 + static_cast<int>(threadIdx.x) + c * span;
+        if (k0 - lane >= limit) break;
         int kk[kBatch], jj[kBatch], rr[kBatch], nn[kBatch], aa[kBatch];
         double xx[kBatch], xl[kBatch], xn[kBatch];
 #pragma unroll
         for (int q = 0; q < kBatch; ++q) {  // segment lookup (smem)
-          const int k = k0 + q * stride;
+          const int k = k0 + q * (chunked ? 32 : stride);
           const bool on = k < limit;
           kk[q] = on ? k : N;
-          const int j = on ? find_link_w(offB, jA, jB, k) : 0;
+          int j = 0;
+          if (on) {
+            if (q == 0 || !chunked) {
+              j = find_link_w(offB, jA, jB, k);
+            } else {
+              j = jj[q - 1];
+              while (offB[j + 1] <= k) ++j;
+            }
+          }
           jj[q] = j;
           rr[q] = k - offB[j];
           nn[q] = offB[j + 1] - offB[j];
