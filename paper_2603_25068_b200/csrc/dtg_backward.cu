@@ -170,36 +170,22 @@ __device__ __forceinline__ void replay_head(const BView& V, int b, int t, int k,
         for (int e = 0; e < kFastDeg; ++e)
           y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sc[e])))) * d.kinv;
       }
-      double m2 = y[0];
+      // the logits are kept (R4 forms pi from them with softmax_stage2's
+      // operations); the choice is the first argmax, read off the logits
+#pragma unroll
+      for (int e = 0; e < kFastDeg; ++e)
+        if (e < deg) lp[e] = y[e];
+      ed = softmax_first_argmax<kFastDeg>(deg, y, ex);
+      c = sc[0];
 #pragma unroll
       for (int e = 1; e < kFastDeg; ++e)
-        if (e < deg && m2 < y[e]) m2 = y[e];
-      double z2 = 0.0;
-#pragma unroll
-      for (int e = 0; e < kFastDeg; ++e) {
-        ex[e] = exp(y[e] - m2);
-        if (e < deg) z2 += ex[e];
-      }
-      ed = 0;
-      double pb = ex[0] / z2;
-      lp[0] = pb;
-#pragma unroll
-      for (int e = 1; e < kFastDeg; ++e)
-        if (e < deg) {
-          const double pv = ex[e] / z2;
-          lp[e] = pv;
-          if (pv > pb) {
-            pb = pv;
-            ed = e;
-          }
-        }
-      c = sc[ed];
+        if (e == ed) c = sc[e];
     } else {
       double g[kMaxDeg], pi[kMaxDeg];
       for (int e = 0; e < deg; ++e) g[e] = gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(d.succ[s0 + e])));
       ed = softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi);
       c = d.succ[s0 + ed];
-      for (int e = 0; e < deg; ++e) lp[e] = pi[e];
+      for (int e = 0; e < deg; ++e) lp[e] = (lz[e] + g[e]) * d.kinv;  // logits, as in softmax_stage2
     }
     const int qq = atomicAdd(&V.ccnt[bl + c], 1);  // round trip overlaps the merge draw
     const std::uint64_t mb = rng_final(rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
@@ -877,10 +863,26 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           const double* la0 = V.lbar_a0 + static_cast<std::size_t>(b) * d.maxdeg;
           if (deg <= kFastDeg) {  // registers, same operation order as two_softmax_vjp
             double bar[kFastDeg], pi[kFastDeg];
+            {  // pi from the replayed logits: softmax_stage2's operations
+              double yv[kFastDeg];
+#pragma unroll
+              for (int e = 0; e < kFastDeg; ++e) yv[e] = e < deg ? lp[e] : 0.0;
+              double m2 = yv[0];
+#pragma unroll
+              for (int e = 1; e < kFastDeg; ++e)
+                if (e < deg && m2 < yv[e]) m2 = yv[e];
+              double z2 = 0.0;
+#pragma unroll
+              for (int e = 0; e < kFastDeg; ++e) {
+                pi[e] = exp(yv[e] - m2);
+                if (e < deg) z2 += pi[e];
+              }
+#pragma unroll
+              for (int e = 0; e < kFastDeg; ++e) pi[e] = e < deg ? pi[e] / z2 : 0.0;
+            }
 #pragma unroll
             for (int e = 0; e < kFastDeg; ++e) {
               const bool on = e < deg;
-              pi[e] = on ? lp[e] : 0.0;
               double v = (hit && e == ed) ? lrow : 0.0;
               if (on && s == a0s) v += la0[e];
               bar[e] = on ? ((v * 1.0) * 1.0) * (V.vac[bl + d.succ[s0 + e]] ? 1.0 : 0.0) : 0.0;
@@ -901,10 +903,15 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               if (e < deg) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e] - exp(lz[e]) * gs;
           } else {
             double bar[kMaxDeg], pi[kMaxDeg];
-            for (int e = 0; e < deg; ++e) {
-              bar[e] = 0.0;
-              pi[e] = lp[e];
+            {  // pi from the replayed logits: softmax_stage2's operations
+              double m2 = lp[0];
+              for (int e = 1; e < deg; ++e)
+                if (m2 < lp[e]) m2 = lp[e];
+              double z2 = 0.0;
+              for (int e = 0; e < deg; ++e) z2 += exp(lp[e] - m2);
+              for (int e = 0; e < deg; ++e) pi[e] = exp(lp[e] - m2) / z2;
             }
+            for (int e = 0; e < deg; ++e) bar[e] = 0.0;
             if (hit) bar[ed] = lrow;
             if (s == a0s)
               for (int e = 0; e < deg; ++e) bar[e] += la0[e];
