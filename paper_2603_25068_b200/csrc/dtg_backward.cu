@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
     grid_sync();
     bstamp(V, t, 2);
     // ================= R2: count adjoint, merge replay, deferred pref, A0 partials =====
-    if (active)
+    if (active && !(V.dbg & 2048))
       for (int b = b0; b < d.B; b += bstep) {
         if (!grouped) {  // scenario loop: reload this scenario's offsets
           __syncthreads();
