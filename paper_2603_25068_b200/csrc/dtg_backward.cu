@@ -527,49 +527,29 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           const double vv = 0.0 - kMaskLarge;
           const double lzv = log(static_cast<double>(nA) * 1.0) + vv;
           const double logz = vv - lzv;
-          T2 tp[kMaxDeg];
-          for (int e = 0; e < deg0; ++e) tp[e] = T2{-INFINITY, -INFINITY, INT_MAX, -1};
-          std::uint64_t h2r[kMaxDeg];  // row prefixes of the merge stream
+          // one draw per thread: items (row e, arrived q) row-major with each row
+          // padded to whole warps, so a warp reduces a single row; every warp
+          // folds its groups into its own per-row slot
           const std::uint64_t h1m = rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t));
-          for (int e = 0; e < deg0; ++e) h2r[e] = rng_prefix2(h1m, static_cast<std::uint64_t>(d.succ[s0 + e]));
-          if (deg0 <= kFastDeg) {  // unrolled rows: independent draw chains interleave
-            T2 tf[kFastDeg];
-            std::uint64_t hf[kFastDeg];
-#pragma unroll
-            for (int e = 0; e < kFastDeg; ++e) {
-              tf[e] = T2{-INFINITY, -INFINITY, INT_MAX, -1};
-              hf[e] = h2r[e < deg0 ? e : 0];
-            }
-            for (int q = spread(ta, lg, nblk); q < nA; q += nblk * kHalf) {
+          const int nAp = (nA + 31) & ~31;
+          const int nitems = deg0 * nAp;
+          if (lane < d.maxdeg) red[wa * d.maxdeg + lane] = T2{-INFINITY, -INFINITY, INT_MAX, -1};
+          __syncwarp();
+          for (int i = spread(ta, lg, nblk); i - lane < nitems; i += nblk * kHalf) {
+            const int e = (i - lane) / nAp, q = i - e * nAp;
+            T2 x{-INFINITY, -INFINITY, INT_MAX, -1};
+            if (q < nA) {
               const int s = V.alist[bn + q];
               const int id = d.aid[so + s];
-              double gq[kFastDeg];
+              const std::uint64_t bits = rng_final(rng_prefix2(h1m, static_cast<std::uint64_t>(d.succ[s0 + e])),
+                                                   static_cast<std::uint64_t>(id));
               int bad = 0;
-#pragma unroll
-              for (int e = 0; e < kFastDeg; ++e) gq[e] = gumbel_sl(rng_final(hf[e], static_cast<std::uint64_t>(id)), bad);
-              if (bad) {
-#pragma unroll
-                for (int e = 0; e < kFastDeg; ++e) gq[e] = gumbel_bits(rng_final(hf[e], static_cast<std::uint64_t>(id)));
-              }
-#pragma unroll
-              for (int e = 0; e < kFastDeg; ++e)
-                if (e < deg0) t2_push(tf[e], (logz + gq[e]) * d.kinv, id, s);
+              double g = gumbel_sl(bits, bad);
+              if (bad) g = gumbel_bits(bits);
+              x.y1 = (logz + g) * d.kinv;
+              x.id1 = id;
+              x.s1 = s;
             }
-#pragma unroll
-            for (int e = 0; e < kFastDeg; ++e)
-              if (e < deg0) tp[e] = tf[e];
-          } else {
-            for (int q = spread(ta, lg, nblk); q < nA; q += nblk * kHalf) {
-              const int s = V.alist[bn + q];
-              const int id = d.aid[so + s];
-              for (int e = 0; e < deg0; ++e) {
-                const double g = gumbel_bits(rng_final(h2r[e], static_cast<std::uint64_t>(id)));
-                t2_push(tp[e], (logz + g) * d.kinv, id, s);
-              }
-            }
-          }
-          for (int e = 0; e < deg0; ++e) {
-            T2 x = tp[e];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
               T2 y;
@@ -579,7 +559,8 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               y.s1 = __shfl_xor_sync(0xffffffffu, x.s1, o);
               t2_merge(x, y);
             }
-            if (lane == 0) red[wa * d.maxdeg + e] = x;
+            if (lane == 0) t2_merge(red[wa * d.maxdeg + e], x);
+            __syncwarp();
           }
           asm volatile("bar.sync 1, %0;" ::"r"(kHalf) : "memory");  // the A[0] half only
           if (ta < deg0) {
