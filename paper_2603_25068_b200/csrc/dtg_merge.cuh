@@ -47,6 +47,32 @@ __device__ __forceinline__ int merge_softmax_fast(int cnt, const Cand* src, doub
       }
     }
   }
+  if (!kNeedPi) {
+    // Winner only: y_e = ((alpha_e - lz) + g_e) * k differs from the exact
+    // (alpha_e + g_e - lz) * k by three roundings, under 2^-52 k (|alpha_e - lz|
+    // + |g_e| + |alpha_e - lz + g_e|) < 3e-11 for |alpha|, |g| < 64 and k <=
+    // 100.  When the two largest alpha_e + g_e are more than kGap apart the
+    // rounded argmax is the exact one and the first stage is not needed;
+    // closer calls take the full computation below.
+    constexpr double kGap = 1e-9;
+    int best = 0;
+    double v1 = c[0].alpha + c[0].g, v2 = -INFINITY;
+    bool small = fabs(c[0].alpha) < 64.0 && fabs(c[0].g) < 64.0;
+#pragma unroll
+    for (int e = 1; e < F; ++e)
+      if (e < cnt) {
+        const double v = c[e].alpha + c[e].g;
+        small = small && fabs(c[e].alpha) < 64.0 && fabs(c[e].g) < 64.0;
+        if (v > v1) {
+          v2 = v1;
+          v1 = v;
+          best = e;
+        } else if (v > v2) {
+          v2 = v;
+        }
+      }
+    if (small && kinv <= 100.0 && (cnt == 1 || (v1 - v2) * kinv > kGap)) return best;
+  }
   double m = c[0].alpha;
 #pragma unroll
   for (int e = 1; e < F; ++e)
