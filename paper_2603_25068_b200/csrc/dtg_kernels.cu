@@ -174,6 +174,25 @@ __device__ __forceinline__ int merge_softmax(const DevView& d, int b, int t, int
       for (int e = 0; e < kFastSucc; ++e)
         y[e] = e < nc ? gumbel_bits(rng_final(h2, static_cast<std::uint64_t>(cid[e]))) : 0.0;
     }
+    {  // winner from alpha + g when the top two are clearly apart (bound in dtg_merge.cuh)
+      int best = 0;
+      double v1 = v[0] + y[0], v2 = -INFINITY;
+      bool small = fabs(v[0]) < 64.0 && fabs(y[0]) < 64.0;
+#pragma unroll
+      for (int e = 1; e < kFastSucc; ++e)
+        if (e < nc) {
+          const double a = v[e] + y[e];
+          small = small && fabs(v[e]) < 64.0 && fabs(y[e]) < 64.0;
+          if (a > v1) {
+            v2 = v1;
+            v1 = a;
+            best = e;
+          } else if (a > v2) {
+            v2 = a;
+          }
+        }
+      if (small && d.kinv <= 100.0 && (nc == 1 || (v1 - v2) * d.kinv > 1e-9)) return best;
+    }
     double m = v[0];
 #pragma unroll
     for (int e = 1; e < kFastSucc; ++e)
