@@ -143,3 +143,19 @@ def test_context_reuse_state_and_param_caching(port):
     # reconfiguring a scenario (new initial state) invalidates what the context holds
     a.configure(0, 1, 90, 30, fit_queues=False, custom_init=(lk, ps2))
     assert_forward_equal(P.simulate_forward(a, p1, seed=7), ref["b1"])
+
+
+def test_c3_dn1_gradient_short(port):
+    """Reverse sweep at 1,000,020 agents (dn=1) over 6 steps: the cum_final and
+    final-position loss gradients against the C oracle (normwise 1e-9)."""
+    T = 6
+    sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 1, T, 300)
+    p = sc.sample_parameters(3)
+    rng = np.random.default_rng(11)
+    wc = rng.normal(size=sc.n_links)
+    wx = rng.normal(size=sc.n_agents)
+    g = P.simulate_gradient(sc, p, seed=7, wc=wc, wx=wx)
+    r = port_of(port, sc).gradient(p, 7, 0, wc=wc, wx=wx)
+    assert abs(g.loss - r["loss"]) <= 1e-9 * max(1.0, abs(r["loss"]))
+    for blk in range(5):
+        assert normwise(g.grads[blk], r["grads"][blk]) <= GRAD_TOL
