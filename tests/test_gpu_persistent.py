@@ -81,3 +81,33 @@ def test_persistent_backward_equals_step_graph(n, length, veh, dn, T, B, tg):
         e.forward(T, spi, checkpoint=True)
         out.append(e.backward(snap_seeds=snap if K else None, cum_seeds=cum, x_seeds=xs))
     assert np.array_equal(out[0], out[1])
+
+
+def test_dn1_full_hour_invariants_and_schedules():
+    """C3 at dn=1 (1,000,020 agents) for the full hour (3,600 steps) — sizes the
+    oracle cannot run: cumulative counts never decrease, every agent ends on a
+    valid link inside it, reruns are bit-identical, and the fused grid kernel
+    equals the 4-kernel step graph over the first 300 steps."""
+    sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 1, 3600, 300)
+    p = sc.sample_parameters(3)
+    a = P.simulate_forward(sc, p, seed=7)
+    b = P.simulate_forward(sc, p, seed=7)
+    assert np.array_equal(a.cum_per_step, b.cum_per_step) and np.array_equal(a.pos_final, b.pos_final)
+    assert (np.diff(a.cum_per_step, axis=0) >= 0).all() and (a.cum_per_step >= 0).all()
+    _, _, length, _ = sc.links()
+    assert a.link_final.min() >= 0 and a.link_final.max() < sc.n_links
+    assert (a.pos_final >= -1e-2).all() and (a.pos_final <= length[a.link_final]).all()
+    assert len(a.link_final) == 1000020
+    T = 300
+    lk, ps = sc.seed_agents()
+    e = P.Engine(sc, 1, T)
+    e.set_params(p)
+    e.set_state(lk, ps)
+    e.set_noise(7, 0)
+    out = []
+    for mode in (2, 3):
+        e.set_mode(mode)
+        e.forward(T, 300)
+        out.append((e.read_cum_all(), e.read_state(0, -1)))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1][0], out[1][1][0]) and np.array_equal(out[0][1][1], out[1][1][1])
