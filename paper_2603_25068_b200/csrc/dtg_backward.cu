@@ -912,11 +912,8 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           const double kap = d.kappa[bl + j];
           const double g0 = g5[j], g1 = g5[L + j], g3 = g5[3 * L + j];
           const int na = n ? V.nA_cur[bl + j] : 0;
-          double ub = 0.0, jb = 0.0;
-          for (int k = base; k < base + n; ++k) {
-            ub += V.cu[bn + k];
-            jb += -1.0 * V.cg[bn + k];
-          }
+          double ub, jb;
+          link_sums8(V.cu + bn, V.cg + bn, base, n, ub, jb);
           if (n) {
             g5[j] = g0 + (0.0 + ub);
             g5[L + j] = g1 + (0.0 - jb * static_cast<double>(d.delta_n) / (kap * kap));

@@ -748,12 +748,9 @@ __global__ void __launch_bounds__(256) k_adj_link(DevView d, int s_cur) {
   const std::size_t bn = static_cast<std::size_t>(b) * d.N;
   const int* off = d.off + oidx(d, s_cur, b);
   const int base = off[j], n = off[j + 1] - base;
-  // deterministic: each link's slots summed in slot order by one thread
-  double ub = 0.0, jb = 0.0;
-  for (int k = base; k < base + n; ++k) {
-    ub += d.cu[bn + k];
-    jb += -1.0 * d.cg[bn + k];
-  }
+  // deterministic: each link's slots summed by one thread (link_sums8 order)
+  double ub, jb;
+  link_sums8(d.cu + bn, d.cg + bn, base, n, ub, jb);
   double* g = d.grads + static_cast<std::size_t>(b) * 5 * d.L;
   const double kap = d.kappa[bl + j];
   if (n) {
