@@ -388,6 +388,61 @@ int dtg_mse_loss(int k_snap, int n_links, const double* snapshots, int n_obs,
                  int delta_n, double* loss, double* seeds);
 const char* dtg_scenario_last_error(const dtg_scenario* sc);
 
+/* ---- FD-validation instrumentation ----------------------
+ * The reference's finite-difference validation modes (car_following.hpp:23-40,
+ * branch_trace.hpp, engine.hpp:55-59/70/98, pipeline.hpp:49-61), run by the
+ * device probe engine (csrc/dtg_probe.cu, one CTA per probe).  Soft choices
+ * and surrogate replay keep the compact per-agent state, so every choice value
+ * must stay 0 or 1 (one-hot rows, e.g. run_gradcheck's chain); a fractional
+ * value returns DTG_ERR_UNSUPPORTED.  Errors: dtg_scenario_last_error(sc)
+ * (dtg_scenario_last_error(NULL) for dtg_run_gradcheck). */
+typedef struct dtg_surrogate dtg_surrogate; /* SurrogateTrace */
+dtg_surrogate* dtg_surrogate_create(void);
+void dtg_surrogate_free(dtg_surrogate* tr);
+/* SurrogateTrace::replay (false: the next run records) and rewind(). */
+int dtg_surrogate_set_replay(dtg_surrogate* tr, int replay);
+int dtg_surrogate_rewind(dtg_surrogate* tr);
+/* SimConfig::soft_choices / SimConfig::surrogate (NULL detaches). */
+int dtg_scenario_set_soft_choices(dtg_scenario* sc, int soft);
+int dtg_scenario_set_surrogate(dtg_scenario* sc, dtg_surrogate* tr);
+/* simulate_forward with ForwardOptions{noise_iteration, trace_branches} and
+ * the scenario's soft / surrogate settings; branch_hash = Trajectory::
+ * branch_hash (the FNV offset basis when not tracing).  cum_per_step [T][L],
+ * link_final / pos_final [N] (link -1: the agent has no valid cell). */
+int dtg_simulate_forward_traced(dtg_scenario* sc, const double* u,
+                                const double* kappa, const double* beta,
+                                const double* alpha, const double* cost,
+                                uint64_t root_seed, uint64_t noise_iteration,
+                                int trace_branches, double* cum_per_step,
+                                int* link_final, double* pos_final,
+                                uint64_t* branch_hash, double* wall_seconds);
+/* simulate_gradient (grad_mode 0 FullTape, 1 Checkpointed) with the
+ * linear-quadratic loss of dtg_simulate_gradient; branch_hash =
+ * GradResult::branch_hash.  A recording surrogate is filled. */
+int dtg_simulate_gradient_traced(dtg_scenario* sc, const double* u,
+                                 const double* kappa, const double* beta,
+                                 const double* alpha, const double* cost,
+                                 uint64_t root_seed, uint64_t noise_iteration,
+                                 int grad_mode, int trace_branches,
+                                 const double* ws, const double* qs,
+                                 const double* wc, const double* qc,
+                                 const double* wx, double* loss, double* grads,
+                                 double* cum_final, uint64_t* branch_hash);
+/* n_probes instrumented forwards in ONE device launch (params [P][5][L]):
+ * cum_final [P][L], cum_sum [P] (sum of cum_final in link order),
+ * branch_hash [P], on_path [P] (0: a replay left the recorded control path).
+ * Any output may be NULL. */
+int dtg_probe_forward_batch(dtg_scenario* sc, int n_probes, const double* params,
+                            uint64_t root_seed, uint64_t noise_iteration,
+                            int trace_branches, double* cum_final,
+                            double* cum_sum, uint64_t* branch_hash,
+                            int* on_path);
+/* run_gradcheck (pipeline.cpp:499-585) -> GradcheckReport; per_draw_max has
+ * room for `draws`.  The report not passing is not an error (pass = 0). */
+int dtg_run_gradcheck(int draws, int steps, int agents, double tol,
+                      uint64_t seed, double* max_rel_err, int* redraws,
+                      int* pass, double* per_draw_max);
+
 /* ---- Observation / output side -------------------------
  * Host-only helpers on count series (values [k][n] row-major, one row per
  * observation interval).  Errors: dtg_observe_last_error(). */

@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -20,6 +21,25 @@
 struct dtg_ctx;  // the C-ABI device context (include/dtg.h)
 
 namespace dtg {
+
+struct ProbeTrace;  // device payload of a SurrogateTrace (csrc/dtg_probe.h)
+
+/// Input outside the device path's contract (C-ABI status DTG_ERR_UNSUPPORTED).
+struct UnsupportedError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+/// SurrogateTrace (car_following.hpp:23-29): a recording run stores the graft /
+/// carrier values and min / relu picks of every step on the device; a replay
+/// run re-evaluates the program with those discontinuities frozen.  The device
+/// keys the records by (step, agent) / (step, link) rather than by call order,
+/// so rewind() has nothing to reset; leaving the recorded control path is
+/// reported as "surrogate trace misaligned" like the reference's trace_fail.
+struct SurrogateTrace {
+  bool replay = false;
+  void rewind() {}
+  std::shared_ptr<ProbeTrace> rec;  // device records (null until recorded)
+};
 
 // ---- network (network.hpp:11-51) ------------------------------------------------
 enum class LinkKind { Physical = 0, VirtualInflow = 1, VirtualOutflow = 2 };
@@ -75,7 +95,11 @@ struct SimConfig {
   double sentinel = 99999.0;
   double gumbel_tau = 0.01;
   bool trajectory_grafting = true;
-  bool soft_choices = false;  // relaxed surrogate: not on the device path
+  /// Relaxed choice tensors (node_model.cpp:21).  On the device the state stays
+  /// compact, so every choice value must be 0 or 1 (one-hot rows, e.g. chains);
+  /// a fractional value raises UnsupportedError.
+  bool soft_choices = false;
+  SurrogateTrace* surrogate = nullptr;  // FD-validation record / replay
   double dt() const { return tau * delta_n; }
 };
 
@@ -112,7 +136,7 @@ void fit_inflow_queues(Scenario& s);
 struct ForwardOptions {
   bool record_states = false;
   std::uint64_t noise_iteration = 0;
-  bool trace_branches = false;  // FD-validation instrumentation: not on device
+  bool trace_branches = false;  // BranchTrace hash of every discrete decision
 };
 
 /// Compact per-agent state (the reference returns it dense N x L; see
@@ -129,6 +153,7 @@ struct Trajectory {
   CompactState final_state;
   std::vector<double> cum_final;
   double wall_seconds = 0.0;
+  std::uint64_t branch_hash = 0xcbf29ce484222325ULL;  // BranchTrace::h (engine.cpp:251)
 };
 
 Trajectory simulate_forward(const Scenario& s, const LinkParams& params,
@@ -173,17 +198,49 @@ struct GradResult {
   std::vector<double> cum_final_values;
   CompactState final_state;
   double wall_seconds = 0.0;
+  std::uint64_t branch_hash = 0xcbf29ce484222325ULL;  // engine.cpp:426
 };
 
 /// Both modes run the device checkpointed sweep (the reference asserts
-/// FullTape == Checkpointed to 1e-12, test_engine.cpp:147-192); soft_choices
-/// is rejected as in the reference's Checkpointed mode (engine.cpp:306-309).
+/// FullTape == Checkpointed to 1e-12, test_engine.cpp:147-192).  soft_choices
+/// is rejected in Checkpointed mode as in the reference (engine.cpp:306-309);
+/// in FullTape mode it is accepted where every choice is one-hot (then the
+/// relaxed and straight-through programs have the same values and VJP).
+/// trace_branches / a recording surrogate run the instrumented forward
+/// (dtg_probe) beside the gradient; a replaying surrogate is unsupported.
 GradResult simulate_gradient(const Scenario& s, const LinkParams& params,
                              const RngStream& rng, const LossBuilder& builder,
                              GradMode mode, const ForwardOptions& opt = {});
 std::vector<GradResult> simulate_gradient_draws(
     const Scenario& s, const LinkParams& params, const RngStream& rng,
     const LossBuilder& builder, const std::vector<std::uint64_t>& noise_iterations);
+
+// ---- FD-validation (pipeline.cpp:486-603) ----------------------
+/// Result of one probe of a batched instrumented forward.
+struct ProbeResult {
+  std::vector<double> cum_final;
+  double cum_sum = 0.0;  // sum of cum_final in link order (run_gradcheck's loss)
+  std::uint64_t branch_hash = 0;
+  bool on_path = true;   // false: replay left the recorded control path
+};
+/// Instrumented forwards of many parameter sets in ONE device launch (one CTA
+/// per probe), with the scenario's soft_choices / surrogate / trace settings.
+std::vector<ProbeResult> probe_forward_batch(const Scenario& s,
+                                             const std::vector<LinkParams>& params,
+                                             const RngStream& rng, std::uint64_t noise_iteration,
+                                             bool trace_branches);
+
+struct GradcheckReport {  // pipeline.hpp:49-55
+  double max_rel_err = 0.0;
+  int draws = 0;
+  int redraws = 0;
+  bool pass = false;
+  std::vector<double> per_draw_max;
+};
+/// run_gradcheck (pipeline.cpp:499-585): central differences of the frozen-
+/// discontinuity surrogate against the adjoint on a 3-link chain with relaxed
+/// choices; all 10·L stencil probes of a draw run as one batched launch.
+GradcheckReport run_gradcheck(int draws, int steps, int agents, double tol, std::uint64_t seed);
 
 // ---- losses used by the callers of the path -----------------------------------------
 struct CountSeries {

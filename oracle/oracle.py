@@ -125,6 +125,28 @@ class RefLib:
         L.ref_optimize_control.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_double, _dp, _ip,
                                            C.c_double, u64, _dp, _dp, _ip, _ip, _dp]
 
+        # FD-validation instrumentation (row f4)
+        L.ref_scenario_set_soft.argtypes = [vp, C.c_int]
+        L.ref_surrogate_new.restype = vp
+        L.ref_surrogate_free.argtypes = [vp]
+        L.ref_surrogate_set_replay.argtypes = [vp, C.c_int]
+        L.ref_surrogate_rewind.argtypes = [vp]
+        L.ref_surrogate_sizes.argtypes = [vp, C.POINTER(C.c_long)]
+        L.ref_forward_traced.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, u64, u64, vp, C.c_int, vp, vp, vp,
+                                         C.POINTER(u64)]
+        L.ref_gradient_traced.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, u64, u64, C.c_int, vp, C.c_int, vp, _dp,
+                                          vp, C.POINTER(u64)]
+        L.ref_run_gradcheck.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, u64, _dp, C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int), _dp]
+
+    def run_gradcheck(self, draws=20, steps=20, agents=5, tol=1e-4, seed=42):
+        """run_gradcheck (pipeline.cpp:499-585) of the reference."""
+        mx = np.zeros(1)
+        red, ps = C.c_int(0), C.c_int(0)
+        per = np.zeros(max(draws, 1))
+        self.check(self.lib.ref_run_gradcheck(draws, steps, agents, tol, seed, mx, C.byref(red), C.byref(ps), per))
+        return dict(max_rel_err=float(mx[0]), redraws=red.value, passed=bool(ps.value), per_draw_max=per[:draws])
+
     def err(self) -> str:
         return self.lib.ref_last_error().decode()
 
@@ -279,6 +301,32 @@ class RefScenario:
         k = int(nsn[0])
         return dict(loss=float(loss[0]), grads=grads.reshape(5, Ln), snapshots=snaps[: k * Ln].reshape(k, Ln),
                     cum_final=cumf, link=lk, pos=ps, wall=float(wall[0]))
+
+    # ---- FD-validation instrumentation (row f4) ------------------------------
+    def set_soft(self, soft: bool):
+        self.lib.lib.ref_scenario_set_soft(self.h, int(soft))
+        return self
+
+    def forward_traced(self, p: Params, seed: int, noise_iteration: int = 0, surrogate=None,
+                       trace_branches=True):
+        Ln, N, T = self.n_links, self.n_agents, self.horizon_steps
+        cum = np.zeros(T * Ln)
+        lk, ps = np.zeros(N, np.int32), np.zeros(N)
+        h = u64(0)
+        self.lib.check(self.lib.lib.ref_forward_traced(
+            self.h, *p.arrays(), seed, noise_iteration, surrogate.h if surrogate else None, int(trace_branches),
+            _ptr(cum), _ptr(lk), _ptr(ps), C.byref(h)))
+        return dict(cum_per_step=cum.reshape(T, Ln), link=lk, pos=ps, hash=int(h.value))
+
+    def gradient_traced(self, p: Params, seed: int, noise_iteration: int = 0, mode: int = 0, surrogate=None,
+                        trace_branches=True):
+        Ln = self.n_links
+        loss, grads, cumf = np.zeros(1), np.zeros(5 * Ln), np.zeros(Ln)
+        h = u64(0)
+        self.lib.check(self.lib.lib.ref_gradient_traced(
+            self.h, *p.arrays(), seed, noise_iteration, mode, surrogate.h if surrogate else None,
+            int(trace_branches), _ptr(loss), grads, _ptr(cumf), C.byref(h)))
+        return dict(loss=float(loss[0]), grads=grads.reshape(5, Ln), cum_final=cumf, hash=int(h.value))
 
     def gradient_mse(self, p: Params, seed: int, noise_iteration: int, obs_ids, obs_vals):
         Ln = self.n_links
@@ -476,3 +524,27 @@ class PortScenario:
         if rc:
             raise RuntimeError(self.lib.err())
         return grads.reshape(5, L)
+
+
+class RefSurrogate:
+    """The reference's SurrogateTrace (car_following.hpp:23-29)."""
+
+    def __init__(self, lib: RefLib):
+        self.lib, self.h = lib, lib.lib.ref_surrogate_new()
+
+    def __del__(self):
+        try:
+            self.lib.lib.ref_surrogate_free(self.h)
+        except Exception:
+            pass
+
+    def set_replay(self, on: bool):
+        self.lib.lib.ref_surrogate_set_replay(self.h, int(on))
+
+    def rewind(self):
+        self.lib.lib.ref_surrogate_rewind(self.h)
+
+    def sizes(self):
+        s = (C.c_long * 4)()
+        self.lib.lib.ref_surrogate_sizes(self.h, s)
+        return list(s)

@@ -533,4 +533,121 @@ long ref_series_to_csv(int k, int n, const int* ids, const double* vals, int int
   return static_cast<long>(s.size());
 }
 
+// ---- FD-validation instrumentation ---------------------
+// soft_choices (car_following.hpp:37), SurrogateTrace record/replay
+// (car_following.hpp:23-29, car_following.cpp:17-94), BranchTrace
+// (branch_trace.hpp) and run_gradcheck (pipeline.cpp:499-603), all through the
+// reference's own entry points.  States are compacted by the VALID rule
+// (x >= kValidThreshold; surrogate replay leaves -(M + d) in vacated cells,
+// so the != -M rule of compact() does not apply); link -1 = no valid cell.
+namespace {
+void compact_valid(const std::vector<double>& X, int N, int L, int* link, double* pos) {
+  for (int i = 0; i < N; ++i) {
+    link[i] = -1;
+    pos[i] = 0.0;
+    for (int j = 0; j < L; ++j) {
+      const double x = X[static_cast<std::size_t>(i) * L + j];
+      if (x >= kValidThreshold) {
+        link[i] = j;
+        pos[i] = x;
+        break;
+      }
+    }
+  }
+}
+}  // namespace
+
+void ref_scenario_set_soft(void* h, int soft) {
+  static_cast<RefScn*>(h)->s.cfg.soft_choices = soft != 0;
+}
+void* ref_surrogate_new() { return new SurrogateTrace; }
+void ref_surrogate_free(void* t) { delete static_cast<SurrogateTrace*>(t); }
+void ref_surrogate_set_replay(void* t, int replay) {
+  static_cast<SurrogateTrace*>(t)->replay = replay != 0;
+}
+void ref_surrogate_rewind(void* t) { static_cast<SurrogateTrace*>(t)->rewind(); }
+/// sizes[0..3] = #graft records, #carrier records, #pick records, total doubles.
+void ref_surrogate_sizes(void* t, long* sizes) {
+  const auto* tr = static_cast<SurrogateTrace*>(t);
+  long nd = 0;
+  for (const auto& v : tr->graft_new) nd += static_cast<long>(v.size());
+  for (const auto& v : tr->graft_old) nd += static_cast<long>(v.size());
+  for (const auto& v : tr->carriers) nd += static_cast<long>(v.size());
+  sizes[0] = static_cast<long>(tr->graft_new.size());
+  sizes[1] = static_cast<long>(tr->carriers.size());
+  sizes[2] = static_cast<long>(tr->picks.size());
+  sizes[3] = nd;
+}
+
+/// simulate_forward with the instrumentation options: surrogate (may be
+/// null), ForwardOptions.trace_branches; returns Trajectory.branch_hash.
+int ref_forward_traced(void* h, const double* u, const double* k, const double* b,
+                       const double* a, const double* c, uint64_t seed,
+                       uint64_t noise_iteration, void* surrogate, int trace_branches,
+                       double* cum_per_step, int* link_final, double* pos_final,
+                       uint64_t* hash) {
+  return guarded([&] {
+    Scenario s = static_cast<RefScn*>(h)->s;
+    s.cfg.surrogate = static_cast<SurrogateTrace*>(surrogate);
+    const int L = s.net.n_links();
+    const int N = s.n_agents();
+    ForwardOptions opt;
+    opt.noise_iteration = noise_iteration;
+    opt.trace_branches = trace_branches != 0;
+    const Trajectory tr =
+        simulate_forward(s, make_params(L, u, k, b, a, c), RngStream(seed), opt);
+    if (cum_per_step)
+      for (int t = 0; t < tr.steps; ++t)
+        std::memcpy(cum_per_step + static_cast<std::size_t>(t) * L,
+                    tr.cum_per_step[t].data(), L * 8);
+    if (link_final) compact_valid(tr.X_final, N, L, link_final, pos_final);
+    if (hash) *hash = tr.branch_hash;
+  });
+}
+
+/// simulate_gradient of sum(cum_final) (run_gradcheck's loss,
+/// pipeline.cpp:522-524) with the instrumentation options.
+int ref_gradient_traced(void* h, const double* u, const double* k, const double* b,
+                        const double* a, const double* c, uint64_t seed,
+                        uint64_t noise_iteration, int mode, void* surrogate,
+                        int trace_branches, double* loss, double* grads,
+                        double* cum_final, uint64_t* hash) {
+  return guarded([&] {
+    Scenario s = static_cast<RefScn*>(h)->s;
+    s.cfg.surrogate = static_cast<SurrogateTrace*>(surrogate);
+    const int L = s.net.n_links();
+    const LossBuilder builder = [](Tape&, const LossInputs& li) -> Tensor {
+      return reduce_sum(li.cum_final, kAxisAll);
+    };
+    ForwardOptions opt;
+    opt.noise_iteration = noise_iteration;
+    opt.trace_branches = trace_branches != 0;
+    const GradResult g = simulate_gradient(
+        s, make_params(L, u, k, b, a, c), RngStream(seed), builder,
+        mode == 0 ? GradMode::FullTape : GradMode::Checkpointed, opt);
+    if (loss) *loss = g.loss;
+    std::memcpy(grads + 0 * L, g.grads.u.data(), L * 8);
+    std::memcpy(grads + 1 * L, g.grads.kappa.data(), L * 8);
+    std::memcpy(grads + 2 * L, g.grads.beta.data(), L * 8);
+    std::memcpy(grads + 3 * L, g.grads.alpha.data(), L * 8);
+    std::memcpy(grads + 4 * L, g.grads.cost.data(), L * 8);
+    if (cum_final) std::memcpy(cum_final, g.cum_final_values.data(), L * 8);
+    if (hash) *hash = g.branch_hash;
+  });
+}
+
+/// run_gradcheck (pipeline.cpp:499-585).  per_draw_max has room for `draws`.
+/// Returns 0 also when the report does not pass (pass = 0); 1 on exceptions.
+int ref_run_gradcheck(int draws, int steps, int agents, double tol, uint64_t seed,
+                      double* max_rel_err, int* redraws, int* pass,
+                      double* per_draw_max) {
+  return guarded([&] {
+    const GradcheckReport r = run_gradcheck(draws, steps, agents, tol, seed);
+    *max_rel_err = r.max_rel_err;
+    *redraws = r.redraws;
+    *pass = r.pass ? 1 : 0;
+    for (std::size_t i = 0; i < r.per_draw_max.size(); ++i) per_draw_max[i] = r.per_draw_max[i];
+  });
+}
+
 }  // extern "C"

@@ -154,6 +154,19 @@ SIGNATURES = [
     ("dtg_debug_log_check", i32, [u64, C.c_longlong, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     ("dtg_debug_warp_records", i32, [vp, i32, i32, vp, C.POINTER(C.c_int)]),
     ("dtg_scenario_last_error", C.c_char_p, [vp]),
+    # FD-validation instrumentation
+    ("dtg_surrogate_create", vp, []),
+    ("dtg_surrogate_free", None, [vp]),
+    ("dtg_surrogate_set_replay", i32, [vp, i32]),
+    ("dtg_surrogate_rewind", i32, [vp]),
+    ("dtg_scenario_set_soft_choices", i32, [vp, i32]),
+    ("dtg_scenario_set_surrogate", i32, [vp, vp]),
+    ("dtg_simulate_forward_traced", i32, [vp, _dp, _dp, _dp, _dp, _dp, u64, u64, i32, vp, vp, vp, _u64p, vp]),
+    ("dtg_simulate_gradient_traced", i32, [vp, _dp, _dp, _dp, _dp, _dp, u64, u64, i32, i32,
+                                           vp, vp, vp, vp, vp, vp, _dp, vp, _u64p]),
+    ("dtg_probe_forward_batch", i32, [vp, i32, _dp, u64, u64, i32, vp, vp, vp, vp]),
+    ("dtg_run_gradcheck", i32, [i32, i32, i32, C.c_double, u64, _dp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                _dp]),
 ]
 
 _lib = None

@@ -21,6 +21,7 @@
 
 #include "../../include/dtg.h"
 #include "../../include/dtg_engine.hpp"
+#include "dtg_fdcheck.h"
 
 namespace dtg {
 
@@ -526,8 +527,7 @@ dtg_ctx* simulate_forward_device(const Scenario& s, const LinkParams& params, co
 
 Trajectory simulate_forward(const Scenario& s, const LinkParams& params, const RngStream& rng,
                             const ForwardOptions& opt) {
-  if (opt.trace_branches)
-    throw std::runtime_error("trace_branches is FD-validation instrumentation; not on the device path");
+  if (detail::instrumented(s, opt)) return detail::forward_instrumented(s, params, rng, opt);
   return std::move(simulate_forward_draws(s, params, rng, {opt.noise_iteration},
                                           opt.record_states)[0]);
 }
@@ -585,10 +585,24 @@ std::vector<GradResult> simulate_gradient_draws(const Scenario& s, const LinkPar
 }
 
 GradResult simulate_gradient(const Scenario& s, const LinkParams& params, const RngStream& rng,
-                             const LossBuilder& builder, GradMode, const ForwardOptions& opt) {
-  if (opt.trace_branches)
-    throw std::runtime_error("trace_branches is FD-validation instrumentation; not on the device path");
-  return std::move(simulate_gradient_draws(s, params, rng, builder, {opt.noise_iteration})[0]);
+                             const LossBuilder& builder, GradMode mode, const ForwardOptions& opt) {
+  if (!detail::instrumented(s, opt))
+    return std::move(simulate_gradient_draws(s, params, rng, builder, {opt.noise_iteration})[0]);
+  if (mode == GradMode::Checkpointed && s.cfg.soft_choices)  // engine.cpp:306-309
+    throw std::runtime_error(
+        "checkpointed backward requires discrete choices (compact state snapshots are exact "
+        "only for one-link-per-agent states)");
+  if (s.cfg.surrogate && s.cfg.surrogate->replay)
+    throw UnsupportedError("the gradient of a replaying surrogate is not on the device path");
+  // With one-hot choices (checked by the instrumented run) the relaxed and the
+  // straight-through programs have equal values and VJPs: the choice rows'
+  // softmax VJPs vanish identically, so the device adjoint applies unchanged.
+  Scenario hard = s;
+  hard.cfg.soft_choices = false;
+  hard.cfg.surrogate = nullptr;
+  GradResult g = std::move(simulate_gradient_draws(hard, params, rng, builder, {opt.noise_iteration})[0]);
+  g.branch_hash = detail::gradient_instrumentation(s, params, rng, opt, g.cum_final_values);
+  return g;
 }
 
 // ---- losses (host mini-tape restated: values and seeds in the reference's op order)
@@ -1003,6 +1017,9 @@ int scn_guard(dtg_scenario* sc, F&& f) {
   } catch (const dtg::DivergenceError& e) {
     if (sc) sc->err = e.what();
     return DTG_ERR_DIVERGENCE;
+  } catch (const dtg::UnsupportedError& e) {
+    if (sc) sc->err = e.what();
+    return DTG_ERR_UNSUPPORTED;
   } catch (const std::invalid_argument& e) {
     if (sc) sc->err = e.what();
     return DTG_ERR_CONFIG;
@@ -1169,6 +1186,9 @@ int dtg_simulate_forward(dtg_scenario* sc, const double* u, const double* k, con
                          double* pos_final, int* states_link, double* states_pos,
                          double* wall_seconds) {
   return scn_guard(sc, [&] {
+    if (sc->s.cfg.soft_choices || sc->s.cfg.surrogate)
+      throw dtg::UnsupportedError(
+          "soft choices / surrogate traces run through dtg_simulate_forward_traced");
     const auto t0 = std::chrono::steady_clock::now();
     const int L = sc->s.net.n_links();
     const std::vector<std::uint64_t> iv(its, its + n_draws);
@@ -1206,6 +1226,8 @@ static int gradient_common(dtg_scenario* sc, const double* u, const double* k, c
                            double* grads, double* snapshots, double* cum_final, int* link_final,
                            double* pos_final, double* wall_seconds) {
   return scn_guard(sc, [&] {
+    if (sc->s.cfg.surrogate)
+      throw dtg::UnsupportedError("surrogate traces run through dtg_simulate_gradient_traced");
     const int L = sc->s.net.n_links();
     const std::vector<std::uint64_t> iv(its, its + n_draws);
     const auto res = dtg::simulate_gradient_draws(sc->s, make_params(L, u, k, b, a, c),
@@ -1277,6 +1299,134 @@ int dtg_simulate_gradient_mse(dtg_scenario* sc, const double* u, const double* k
   if (rc) return rc;
   return gradient_common(sc, u, k, b, a, c, root_seed, n_draws, its, builder, loss, grads,
                          nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+// ---- FD-validation instrumentation ---------------------------
+}  // extern "C"
+
+struct dtg_surrogate {
+  dtg::SurrogateTrace tr;
+};
+
+extern "C" {
+
+dtg_surrogate* dtg_surrogate_create(void) { return new (std::nothrow) dtg_surrogate; }
+void dtg_surrogate_free(dtg_surrogate* tr) { delete tr; }
+int dtg_surrogate_set_replay(dtg_surrogate* tr, int replay) {
+  if (!tr) return DTG_ERR_CONFIG;
+  tr->tr.replay = replay != 0;
+  return DTG_OK;
+}
+int dtg_surrogate_rewind(dtg_surrogate* tr) {
+  if (!tr) return DTG_ERR_CONFIG;
+  tr->tr.rewind();
+  return DTG_OK;
+}
+int dtg_scenario_set_soft_choices(dtg_scenario* sc, int soft) {
+  sc->s.cfg.soft_choices = soft != 0;
+  return DTG_OK;
+}
+int dtg_scenario_set_surrogate(dtg_scenario* sc, dtg_surrogate* tr) {
+  sc->s.cfg.surrogate = tr ? &tr->tr : nullptr;
+  return DTG_OK;
+}
+
+int dtg_simulate_forward_traced(dtg_scenario* sc, const double* u, const double* k,
+                                const double* b, const double* a, const double* c,
+                                uint64_t root_seed, uint64_t noise_iteration, int trace_branches,
+                                double* cum_per_step, int* link_final, double* pos_final,
+                                uint64_t* branch_hash, double* wall_seconds) {
+  return scn_guard(sc, [&] {
+    const int L = sc->s.net.n_links();
+    dtg::ForwardOptions opt;
+    opt.noise_iteration = noise_iteration;
+    opt.trace_branches = trace_branches != 0;
+    const dtg::Trajectory tr = dtg::simulate_forward(sc->s, make_params(L, u, k, b, a, c),
+                                                     dtg::RngStream(root_seed), opt);
+    if (cum_per_step)
+      for (int t = 0; t < tr.steps; ++t)
+        std::copy(tr.cum_per_step[t].begin(), tr.cum_per_step[t].end(),
+                  cum_per_step + static_cast<std::size_t>(t) * L);
+    if (link_final) std::copy(tr.final_state.link.begin(), tr.final_state.link.end(), link_final);
+    if (pos_final) std::copy(tr.final_state.pos.begin(), tr.final_state.pos.end(), pos_final);
+    if (branch_hash) *branch_hash = tr.branch_hash;
+    if (wall_seconds) *wall_seconds = tr.wall_seconds;
+  });
+}
+
+int dtg_simulate_gradient_traced(dtg_scenario* sc, const double* u, const double* k,
+                                 const double* b, const double* a, const double* c,
+                                 uint64_t root_seed, uint64_t noise_iteration, int grad_mode,
+                                 int trace_branches, const double* ws, const double* qs,
+                                 const double* wc, const double* qc, const double* wx,
+                                 double* loss, double* grads, double* cum_final,
+                                 uint64_t* branch_hash) {
+  return scn_guard(sc, [&] {
+    const int L = sc->s.net.n_links();
+    const int T = sc->s.horizon_steps;
+    const double spi = sc->s.obs_interval_s / sc->s.cfg.dt();
+    const int K = spi >= 1.0 ? static_cast<int>(T / std::llround(spi)) : 0;
+    const int N = sc->s.n_agents();
+    std::vector<double> vws, vqs, vwc, vqc, vwx;
+    if (ws) vws.assign(ws, ws + static_cast<std::size_t>(K) * L);
+    if (qs) vqs.assign(qs, qs + static_cast<std::size_t>(K) * L);
+    if (wc) vwc.assign(wc, wc + L);
+    if (qc) vqc.assign(qc, qc + L);
+    if (wx) vwx.assign(wx, wx + N);
+    dtg::ForwardOptions opt;
+    opt.noise_iteration = noise_iteration;
+    opt.trace_branches = trace_branches != 0;
+    const dtg::GradResult g = dtg::simulate_gradient(
+        sc->s, make_params(L, u, k, b, a, c), dtg::RngStream(root_seed),
+        dtg::linear_quadratic_loss(vws, vqs, vwc, vqc, vwx),
+        grad_mode == 0 ? dtg::GradMode::FullTape : dtg::GradMode::Checkpointed, opt);
+    if (loss) *loss = g.loss;
+    for (int q = 0; q < 5; ++q) {
+      const std::vector<double>* blk[5] = {&g.grads.u, &g.grads.kappa, &g.grads.beta,
+                                           &g.grads.alpha, &g.grads.cost};
+      std::copy(blk[q]->begin(), blk[q]->end(), grads + static_cast<std::size_t>(q) * L);
+    }
+    if (cum_final) std::copy(g.cum_final_values.begin(), g.cum_final_values.end(), cum_final);
+    if (branch_hash) *branch_hash = g.branch_hash;
+  });
+}
+
+int dtg_probe_forward_batch(dtg_scenario* sc, int n_probes, const double* params,
+                            uint64_t root_seed, uint64_t noise_iteration, int trace_branches,
+                            double* cum_final, double* cum_sum, uint64_t* branch_hash,
+                            int* on_path) {
+  return scn_guard(sc, [&] {
+    const int L = sc->s.net.n_links();
+    std::vector<dtg::LinkParams> ps(n_probes);
+    for (int p = 0; p < n_probes; ++p) {
+      const double* d = params + static_cast<std::size_t>(p) * 5 * L;
+      ps[p] = make_params(L, d, d + L, d + 2 * L, d + 3 * L, d + 4 * L);
+    }
+    const auto res = dtg::probe_forward_batch(sc->s, ps, dtg::RngStream(root_seed),
+                                              noise_iteration, trace_branches != 0);
+    for (int p = 0; p < n_probes; ++p) {
+      if (cum_final)
+        std::copy(res[p].cum_final.begin(), res[p].cum_final.end(),
+                  cum_final + static_cast<std::size_t>(p) * L);
+      if (cum_sum) cum_sum[p] = res[p].cum_sum;
+      if (branch_hash) branch_hash[p] = res[p].branch_hash;
+      if (on_path) on_path[p] = res[p].on_path ? 1 : 0;
+    }
+  });
+}
+
+int dtg_run_gradcheck(int draws, int steps, int agents, double tol, uint64_t seed,
+                      double* max_rel_err, int* redraws, int* pass, double* per_draw_max) {
+  dtg_scenario tmp;
+  const int rc = scn_guard(&tmp, [&] {
+    const dtg::GradcheckReport r = dtg::run_gradcheck(draws, steps, agents, tol, seed);
+    if (max_rel_err) *max_rel_err = r.max_rel_err;
+    if (redraws) *redraws = r.redraws;
+    if (pass) *pass = r.pass ? 1 : 0;
+    if (per_draw_max) std::copy(r.per_draw_max.begin(), r.per_draw_max.end(), per_draw_max);
+  });
+  if (rc) g_scn_error = tmp.err;
+  return rc;
 }
 
 dtg_ctx* dtg_scenario_ctx(dtg_scenario* sc) {
