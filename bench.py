@@ -328,8 +328,8 @@ def run_ours(args):
     d2h = B * (T_STEPS * L * 8 + N * (4 + 8)) + 4 * B
     e2e = {"value": world * B * SIM_SECONDS / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "s_per_call": e2e_s,
-           "path": "dtg_simulate_forward (C-ABI, host buffers, synchronous); new parameters and noise "
-                   "every call; the scenario's initial state stays resident on the device between calls "
+           "path": "dtg_simulate_forward (C-ABI, host buffers, synchronous; count rows are copied back "
+                   "while the kernel runs, dtg_forward_read); new parameters and noise every call; the scenario's initial state stays resident on the device between calls "
                    "(unchanged scenario)"}
 
     grad = run_gradient(P, torch, world, rank, args)
@@ -464,12 +464,16 @@ def run_gradient(P, torch, world, rank, args):
     n_it = max(5, args.steps)
     walls = []
     for n in (n_it, 2 * n_it):  # per-call setup (seeding, state upload) cancels in the difference
-        barrier(world)
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        res = run(n)
-        torch.cuda.synchronize()
-        walls.append(max_over_ranks(time.perf_counter() - t, world))
+        best = None
+        for _ in range(3):  # best of three calls: host-side jitter only ever adds time
+            barrier(world)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            res = run(n)
+            torch.cuda.synchronize()
+            w = max_over_ranks(time.perf_counter() - t, world)
+            best = w if best is None else min(best, w)
+        walls.append(best)
     s_iter = (walls[1] - walls[0]) / n_it
     setup_s = walls[0] - n_it * s_iter
     # device time of the two passes (CUDA events on the engine's stream)
@@ -507,7 +511,7 @@ def run_gradient(P, torch, world, rank, args):
             "fwd_ckpt_ms_per_pass": statistics.median(fwd_ms), "adj_ms_per_pass": statistics.median(adj_ms),
             "fwd_phase_us_per_step": {k: round(x, 2) for k, x in phases_f.items()},
             "adj_phase_us_per_step": {k: round(x, 2) for k, x in phases_b.items()},
-            "timing": "wall clock per calibrate() iteration through the public API (device loss/seeds/draw sum, "
+            "timing": "wall clock per calibrate() iteration through the public API (best of 3 calls each) (device loss/seeds/draw sum, "
                       "NCCL row gather for N>1, host transform + AdamW, 1 sync per iteration): difference of "
                       "a 2n- and an n-iteration calibrate call / n; the per-call setup is reported separately"}
 

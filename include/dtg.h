@@ -126,6 +126,16 @@ int dtg_set_noise(dtg_ctx* ctx, int scenario, uint64_t root_seed,
 int dtg_forward(dtg_ctx* ctx, int n_steps, int steps_per_interval,
                 int checkpoint);
 
+/* dtg_forward followed by the read-back of its results into host buffers,
+ * overlapped with the run: the persistent kernel publishes each finished step
+ * (host-mapped counter) and finished count rows are copied on a second stream
+ * while later steps compute.  cum_per_step [B][T][L] (as dtg_read_cum_all),
+ * link_final / pos_final [B][N] (as dtg_read_state of step T); any may be
+ * NULL.  Same results as dtg_forward + the reads. */
+int dtg_forward_read(dtg_ctx* ctx, int n_steps, int steps_per_interval,
+                     int checkpoint, double* cum_per_step, int* link_final,
+                     double* pos_final);
+
 /* Wait for the context's stream and report device-side errors of the last
  * forward / backward (reads below do this implicitly). */
 int dtg_sync(dtg_ctx* ctx);

@@ -172,6 +172,13 @@ std::vector<Trajectory> simulate_forward_draws(
                                         const std::vector<std::uint64_t>& noise_iterations,
                                         bool record_states = false);
 
+/// The same run with its results streamed into host buffers while the kernel
+/// runs (dtg_forward_read): cum_per_step [D][T][L], link/pos_final [D][N].
+::dtg_ctx* simulate_forward_into(const Scenario& s, const LinkParams& params,
+                                 const RngStream& rng,
+                                 const std::vector<std::uint64_t>& noise_iterations,
+                                 double* cum_per_step, int* link_final, double* pos_final);
+
 /// What a loss sees (engine.hpp:82-87) ...
 struct LossInputs {
   const std::vector<std::vector<double>>* snapshots = nullptr;

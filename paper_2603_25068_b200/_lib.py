@@ -100,6 +100,7 @@ SIGNATURES = [
     ("dtg_set_noise", i32, [vp, i32, u64, u64]),
     ("dtg_forward", i32, [vp, i32, i32, i32]),
     ("dtg_sync", i32, [vp]),
+    ("dtg_forward_read", i32, [vp, i32, i32, i32, vp, vp, vp]),
     ("dtg_debug_force_slow_path", i32, [vp, i32]),
     ("dtg_read_cum", i32, [vp, i32, _dp]),
     ("dtg_read_cum_all", i32, [vp, _dp]),

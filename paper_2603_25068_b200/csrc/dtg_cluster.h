@@ -41,6 +41,11 @@ struct CView {
   int contig;          // 1: contiguous slot range per CTA, 0: interleaved 512-slot blocks
   int ckpt;            // keep every layout (else positions/links of the final one only)
   int dbg;             // timing experiments only (dtg_set_flag 3); results invalid when nonzero
+  // optional host-mapped step counter: after the barrier that completes step
+  // t-1 (every count of steps < t final), CTA 0 publishes t at system scope so
+  // the host can copy finished count rows while the kernel runs (grid mode)
+  volatile unsigned int* progress;
+  int progress_every;  // publish only when t is a multiple (chunk ends) or T
 };
 
 void launch_pack_succ(const DevView& d, double* srec, cudaStream_t st);

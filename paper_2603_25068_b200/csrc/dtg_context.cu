@@ -120,6 +120,15 @@ struct dtg_ctx {
   int last_grid = 0;
   double* h_stage = nullptr;  // pinned staging for count read-back
   std::size_t h_stage_n = 0;
+  // streamed read-back (dtg_forward_read): host-mapped step counter written by
+  // the persistent kernel, a copy stream, pinned staging of the final state
+  unsigned int* prog_h = nullptr;
+  int stream_progress = 0;  // >0: next fused launch publishes progress every this many steps
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t par_ev = nullptr;
+  double* h_par = nullptr;       // pinned parameter staging [5][L]
+  void* h_fin = nullptr;         // pinned final state: int link[B*N] | double pos[B*N]
+  std::size_t h_fin_n = 0;
   int mode = 0;          // 0 auto, 1 cluster, 2 grid-persistent, 3 step graph
   int cluster_cs_max = 0;
   bool stage_params = false;
@@ -221,6 +230,11 @@ struct dtg_ctx {
     drop_graphs();
     if (h_stage) cudaFreeHost(h_stage);
     if (h_red) cudaFreeHost(h_red);
+    if (prog_h) cudaFreeHost(prog_h);
+    if (h_par) cudaFreeHost(h_par);
+    if (h_fin) cudaFreeHost(h_fin);
+    if (par_ev) cudaEventDestroy(par_ev);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
@@ -253,6 +267,9 @@ struct dtg_ctx {
     pending = false;
     std::vector<int> e(B);
     CK(cudaMemcpy(e.data(), errf.p, sizeof(int) * B, cudaMemcpyDeviceToHost));
+    check_flags(e.data());
+  }
+  void check_flags(const int* e) const {
     for (int b = 0; b < B; ++b) {
       if (e[b] & dtg::kErrCandOverflow)
         throw Unsupported("more than 32 merge candidates for one link in one step (scenario " +
@@ -630,8 +647,21 @@ int dtg_set_params(dtg_ctx* c, int scenario, const double* u, const double* kapp
                    const double* beta, const double* alpha, const double* cost) {
   return guarded(c, [&] {
     if (scenario >= c->B) throw std::invalid_argument("scenario index out of range");
-    const double* src[5] = {u, kappa, beta, alpha, cost};
     const std::size_t L = c->L, BL = static_cast<std::size_t>(c->B) * L;
+    // stage through pinned memory: the uploads are then truly asynchronous and
+    // ordered before the next forward on the stream, with no host wait here
+    if (!c->h_par) {
+      CK(cudaMallocHost(&c->h_par, 5 * L * sizeof(double)));
+      CK(cudaEventCreateWithFlags(&c->par_ev, cudaEventDisableTiming));
+    } else {
+      CK(cudaEventSynchronize(c->par_ev));  // the previous upload has left the staging
+    }
+    const double* src[5] = {c->h_par, c->h_par + L, c->h_par + 2 * L, c->h_par + 3 * L,
+                            c->h_par + 4 * L};
+    {
+      const double* in[5] = {u, kappa, beta, alpha, cost};
+      for (int q = 0; q < 5; ++q) std::memcpy(c->h_par + q * L, in[q], L * sizeof(double));
+    }
     if (scenario < 0) {
       // one upload, then doubling device copies to the other scenarios
       for (int q = 0; q < 5; ++q) {
@@ -652,7 +682,7 @@ int dtg_set_params(dtg_ctx* c, int scenario, const double* u, const double* kapp
                            cudaMemcpyHostToDevice, c->stream));
       c->have_params[b] = 1;
     }
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaEventRecord(c->par_ev, c->stream));
   });
 }
 
@@ -770,6 +800,10 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       V.stage_params = c->stage_params ? 1 : 0;
       V.tstamp = nullptr;
       V.gbar = c->custom_barrier ? c->gbar.p : nullptr;
+      // grid mode: CTA 0 sees every scenario's step complete at the grid
+      // barrier; a cluster only sees its own scenario
+      V.progress = (c->stream_progress > 0 && (mode == 2 || c->B == 1)) ? c->prog_h : nullptr;
+      V.progress_every = std::max(1, c->stream_progress);
       if (mode == 1) {
         V.cs = cs;
       } else {
@@ -863,6 +897,85 @@ int dtg_read_cum_all(dtg_ctx* c, double* cum) {
     for (std::size_t b = 0; b < B; ++b)
       for (int t = 0; t < T; ++t)
         std::memcpy(cum + (b * T + t) * L, c->h_stage + (t * B + b) * L, L * 8);
+  });
+}
+
+int dtg_forward_read(dtg_ctx* c, int T, int spi, int checkpoint, double* cum, int* link,
+                     double* pos) {
+  if (!c->prog_h) {
+    const int rc = guarded(c, [&] {
+      CK(cudaHostAlloc(&c->prog_h, sizeof(unsigned int), cudaHostAllocMapped));
+      CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    });
+    if (rc) return rc;
+  }
+  // ~8 chunks of count rows; the kernel publishes its progress at chunk ends
+  const int chunk = std::max(1, (T + 7) / 8);
+  *reinterpret_cast<volatile unsigned int*>(c->prog_h) = 0;
+  c->stream_progress = (cum && T > 0) ? chunk : 0;
+  const int rc = dtg_forward(c, T, spi, checkpoint);
+  c->stream_progress = 0;
+  if (rc) return rc;
+  return guarded(c, [&] {
+    const std::size_t L = c->L, B = c->B, BL = B * L, N = c->N;
+    // everything after the kernel is enqueued right behind it (no host round
+    // trip): final-state gather, its copies and the error flags, all into one
+    // pinned block [errf B ints | link B*N ints | pos B*N doubles]
+    const std::size_t need = B * 4 + B * N * 12 + 8;
+    if (c->h_fin_n < need) {
+      if (c->h_fin) cudaFreeHost(c->h_fin);
+      c->h_fin = nullptr;
+      c->h_fin_n = 0;
+      CK(cudaMallocHost(&c->h_fin, need));
+      c->h_fin_n = need;
+    }
+    int* he = static_cast<int*>(c->h_fin);
+    int* hl = he + B;
+    double* hp = reinterpret_cast<double*>(
+        static_cast<char*>(c->h_fin) + ((B * 4 + B * N * 4 + 7) / 8) * 8);
+    if (link || pos) {
+      const dtg::DevView d = c->view();
+      dtg::launch_gather_state(d, T % c->S, c->tmp_link.p, c->tmp_pos.p, c->stream);
+      CK(cudaGetLastError());
+      if (link) CK(cudaMemcpyAsync(hl, c->tmp_link.p, B * N * 4, cudaMemcpyDeviceToHost, c->stream));
+      if (pos) CK(cudaMemcpyAsync(hp, c->tmp_pos.p, B * N * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaMemcpyAsync(he, c->errf.p, B * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (cum && T > 0) {
+      const std::size_t n = static_cast<std::size_t>(T) * BL;
+      if (c->h_stage_n < n) {
+        if (c->h_stage) cudaFreeHost(c->h_stage);
+        c->h_stage = nullptr;
+        c->h_stage_n = 0;
+        CK(cudaMallocHost(&c->h_stage, n * 8));
+        c->h_stage_n = n;
+      }
+      // copy finished count rows while the kernel runs: each chunk is issued
+      // once the kernel has published that its steps are final (or once the
+      // stream is idle: schedules without a progress counter, errors)
+      const volatile unsigned int* prog = c->prog_h;
+      int done = 0;
+      while (done < T) {
+        const int end = std::min(T, done + chunk);
+        while (static_cast<int>(*prog) < end) {
+          if (cudaStreamQuery(c->stream) != cudaErrorNotReady) break;
+        }
+        CK(cudaMemcpyAsync(c->h_stage + static_cast<std::size_t>(done) * BL,
+                           c->cumh.p + static_cast<std::size_t>(done + 1) * BL,
+                           static_cast<std::size_t>(end - done) * BL * 8, cudaMemcpyDeviceToHost,
+                           c->copy_stream));
+        CK(cudaStreamSynchronize(c->copy_stream));
+        for (std::size_t b = 0; b < B; ++b)
+          for (int t = done; t < end; ++t)
+            std::memcpy(cum + (b * T + t) * L, c->h_stage + (t * B + b) * L, L * 8);
+        done = end;
+      }
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    c->pending = false;
+    c->check_flags(he);
+    if (link) std::memcpy(link, hl, B * N * 4);
+    if (pos) std::memcpy(pos, hp, B * N * 8);
   });
 }
 

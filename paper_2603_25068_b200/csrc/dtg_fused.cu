@@ -270,6 +270,13 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
     const std::uint64_t h1l = rng_prefix1(seed_link, static_cast<std::uint64_t>(t));
     const std::uint64_t h1m = rng_prefix1(seed_merge, static_cast<std::uint64_t>(t));
     if (!last) fstamp(V, t, 0);
+    if (V.progress && t > 0 && (t % V.progress_every == 0 || last) && blockIdx.x == 0 &&
+        threadIdx.x == 0) {
+      // this thread acquired every CTA's step t-1 writes at the barrier; the
+      // system-scope fence makes them visible to the copy engine before t is
+      __threadfence_system();
+      *V.progress = static_cast<unsigned int>(t);
+    }
     const unsigned long long wst0 = V.wstamp ? gnow() : 0;
     unsigned long long wt1 = 0;
     int n_arr = 0;

@@ -501,8 +501,27 @@ std::vector<Trajectory> simulate_forward_draws(const Scenario& s, const LinkPara
                                                bool record_states) {
   const auto t0 = Clock::now();
   const Prepared p = prepare(s, params, rng, its);
-  check(p.ctx, dtg_forward(p.ctx, p.T, p.spi, record_states ? 1 : 0));
   std::vector<Trajectory> out(p.B);
+  if (!record_states) {  // results stream back while the kernel runs
+    const std::size_t TL = static_cast<std::size_t>(p.T) * p.L, N = p.N;
+    std::vector<double> cum(p.B * TL), pos(p.B * N);
+    std::vector<int> link(p.B * N);
+    check(p.ctx, dtg_forward_read(p.ctx, p.T, p.spi, 0, cum.data(), link.data(), pos.data()));
+    for (int b = 0; b < p.B; ++b) {
+      Trajectory& tr = out[b];
+      tr.steps = p.T;
+      for (int t = 0; t < p.T; ++t)
+        tr.cum_per_step.emplace_back(cum.begin() + b * TL + static_cast<std::size_t>(t) * p.L,
+                                     cum.begin() + b * TL + static_cast<std::size_t>(t + 1) * p.L);
+      tr.final_state.link.assign(link.begin() + b * N, link.begin() + (b + 1) * N);
+      tr.final_state.pos.assign(pos.begin() + b * N, pos.begin() + (b + 1) * N);
+      tr.cum_final = p.T ? tr.cum_per_step.back() : std::vector<double>(p.L, 0.0);
+    }
+    const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
+    for (auto& tr : out) tr.wall_seconds = wall;
+    return out;
+  }
+  check(p.ctx, dtg_forward(p.ctx, p.T, p.spi, 1));
   auto cums = read_cum_all(p.ctx, p.B, p.T, p.L);
   for (int b = 0; b < p.B; ++b) {
     Trajectory& tr = out[b];
@@ -516,6 +535,14 @@ std::vector<Trajectory> simulate_forward_draws(const Scenario& s, const LinkPara
   const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
   for (auto& tr : out) tr.wall_seconds = wall;
   return out;
+}
+
+dtg_ctx* simulate_forward_into(const Scenario& s, const LinkParams& params, const RngStream& rng,
+                               const std::vector<std::uint64_t>& its, double* cum_per_step,
+                               int* link_final, double* pos_final) {
+  const Prepared p = prepare(s, params, rng, its);
+  check(p.ctx, dtg_forward_read(p.ctx, p.T, p.spi, 0, cum_per_step, link_final, pos_final));
+  return p.ctx;
 }
 
 dtg_ctx* simulate_forward_device(const Scenario& s, const LinkParams& params, const RngStream& rng,
@@ -1192,10 +1219,18 @@ int dtg_simulate_forward(dtg_scenario* sc, const double* u, const double* k, con
     const auto t0 = std::chrono::steady_clock::now();
     const int L = sc->s.net.n_links();
     const std::vector<std::uint64_t> iv(its, its + n_draws);
-    // results go straight from the device into the caller's buffers
-    // ([D][T][L] counts are exactly dtg_read_cum_all's layout)
+    if (!states_link) {
+      // results stream from the device into the caller's buffers while the
+      // kernel runs ([D][T][L] counts are exactly dtg_read_cum_all's layout)
+      sc->last_ctx = dtg::simulate_forward_into(sc->s, make_params(L, u, k, b, a, c),
+                                                dtg::RngStream(root_seed), iv, cum_per_step,
+                                                link_final, pos_final);
+      if (wall_seconds)
+        *wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      return;
+    }
     dtg_ctx* ctx = dtg::simulate_forward_device(sc->s, make_params(L, u, k, b, a, c),
-                                                dtg::RngStream(root_seed), iv, states_link != nullptr);
+                                                dtg::RngStream(root_seed), iv, true);
     sc->last_ctx = ctx;
     const int T = sc->s.horizon_steps;
     const std::size_t N = static_cast<std::size_t>(sc->s.n_agents());

@@ -206,8 +206,8 @@ def simulate_forward(sc: Scenario, params: LinkParams, seed: int, noise_iteratio
     all draws run batched in one device pass and a list is returned."""
     its = _its(noise_iteration, noise_iterations)
     D, T, L, N = len(its), sc.horizon_steps, sc.n_links, sc.n_agents
-    cum = np.zeros((D, T, L))
-    lk, ps = np.zeros((D, N), np.int32), np.zeros((D, N))
+    cum = np.empty((D, T, L))  # every entry is written by the call
+    lk, ps = np.empty((D, N), np.int32), np.empty((D, N))
     sl = np.zeros((D, T, N), np.int32) if record_states else None
     sp = np.zeros((D, T, N)) if record_states else None
     wall = np.zeros(1)
