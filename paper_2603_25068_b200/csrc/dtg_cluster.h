@@ -20,6 +20,15 @@ struct Cand {
   int pad;
 };
 
+// A head decision drawn one step ahead (link choice c and own merge noise g of
+// agent aid at the next step; aid -1: none).  Both depend only on (seed, step,
+// agent, link), never on the state, so a precomputed record is exact.
+struct Spec {
+  int aid;
+  int c;
+  double g;
+};
+
 struct CView {
   DevView d;
   double* x1b;    // [2][B][N]
@@ -46,6 +55,11 @@ struct CView {
   // the host can copy finished count rows while the kernel runs (grid mode)
   volatile unsigned int* progress;
   int progress_every;  // publish only when t is a multiple (chunk ends) or T
+  // optional [2][B][L][2]: during step t's link phase the otherwise idle
+  // threads draw step t+1's decisions of every link's first two agents (the
+  // only agents that can be its arrived head at t+1); the slot phase of t+1
+  // then only registers them (null: heads draw in the slot phase)
+  Spec* spec;
 };
 
 void launch_pack_succ(const DevView& d, double* srec, cudaStream_t st);

@@ -134,6 +134,8 @@ struct dtg_ctx {
   bool stage_params = false;
   int last_mode = 0, last_cs = 0;
   DevBuf<double> srec;
+  DevBuf<dtg::Spec> spec;  // speculative head decisions [2][B][L][2]
+  bool speculate = true;
   DevBuf<unsigned int> gbar, bgbar;
   bool custom_barrier = true;
   int contig_mode = -1;
@@ -569,6 +571,9 @@ int dtg_set_flag(dtg_ctx* c, int flag, int value) {
     case 1:  // fused forward slot mapping: -1 auto, 0 interleaved, 1 contiguous
       c->contig_mode = value < 0 ? -1 : (value ? 1 : 0);
       return DTG_OK;
+    case 4:  // fused forward: speculative head decisions one step ahead (1 default, 0 off)
+      c->speculate = value != 0;
+      return DTG_OK;
     default:
       return fail(c, DTG_ERR_CONFIG, "unknown flag");
   }
@@ -816,6 +821,12 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       V.contig = c->contig_mode >= 0 ? c->contig_mode : 0;
       c->last_grid = c->B * V.cs;
       c->last_cs = V.cs;
+      // speculative head draws: 8 lanes per link besides the link threads, one round
+      V.spec = nullptr;
+      if (c->speculate && V.cs * dtg::kClusterThreads >= 9 * c->L) {
+        c->spec.ensure(static_cast<std::size_t>(4) * BL);
+        V.spec = c->spec.p;
+      }
       V.wstamp = nullptr;
       if (c->want_wstamp) {
         c->wst.ensure(static_cast<std::size_t>(T) * c->B * V.cs * (dtg::kClusterThreads / 32) * 4 + 4);

@@ -50,9 +50,11 @@ constexpr int kFastDeg = 5;  // successor counts up to this take the unrolled he
 // chains are independent instructions the scheduler interleaves (the heads are
 // the critical path of the slot phase); the softmax runs on registers with the
 // same operations in the same order as softmax_stage2.
-__device__ __forceinline__ void head_choice(const CView& V, std::size_t bl, std::uint64_t h1l,
-                                            std::uint64_t h1m, int k, int j, int a, const int* soff_s,
-                                            const double* slz) {
+// The decision of agent a at the end of link j: chosen successor c and its own
+// merge Gumbel g'(t, c, a) (h1l / h1m: the step's stream prefixes).
+__device__ __forceinline__ void head_draw(const CView& V, std::uint64_t h1l, std::uint64_t h1m, int j,
+                                          int a, const int* soff_s, const double* slz, int& c_out,
+                                          double& g_out) {
   const DevView& d = V.d;
   const int sb = soff_s[j], deg = soff_s[j + 1] - sb;
   const double* lz = slz + static_cast<std::size_t>(j) * d.maxdeg;
@@ -80,14 +82,130 @@ __device__ __forceinline__ void head_choice(const CView& V, std::size_t bl, std:
     for (int e = 0; e < deg; ++e) g[e] = gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(d.succ[sb + e])));
     c = d.succ[sb + softmax_stage2<kMaxDeg>(deg, lz, g, d.kinv, pi)];
   }
-  Cand cd;
-  cd.alpha = d.alpha[bl + j];
   {
     int bad = 0;
     const std::uint64_t mb = rng_final(rng_prefix2(h1m, static_cast<std::uint64_t>(c)), static_cast<std::uint64_t>(a));
-    cd.g = gumbel_sl(mb, bad);
-    if (bad) cd.g = gumbel_bits(mb);
+    g_out = gumbel_sl(mb, bad);
+    if (bad) g_out = gumbel_bits(mb);
   }
+  c_out = c;
+}
+
+// Speculative decisions of the next step, 4 lanes per candidate: candidate
+// u = 2 j + which is the which-th agent (0 leader, 1 follower) of link j in
+// layout t (ids `aid`, step-t positions `x1`).  Lane e of the segment draws the
+// link Gumbels of successors e and e + 4 and the agent's merge Gumbels for
+// them (four independent chains); lane 0 gathers the y values, takes the first
+// argmax with softmax_first_argmax's exact rule (the same operations as
+// head_draw) and picks the chosen successor's merge draw.  A candidate is
+// skipped when it cannot reach the arrival threshold in one step: its next
+// position is at most fl(x1 + dxf), so fl(x1 + dxf) < L - 0.01 rules the
+// arrival out exactly.  Links with more than 8 successors: lane 0 alone.
+// Called warp-uniformly (every lane of the warp runs every shuffle).
+constexpr int kSpecLanes = 4;
+constexpr int kSpecDeg = 2 * kSpecLanes;
+__device__ __forceinline__ void spec_segment(const CView& V, std::uint64_t h1l, std::uint64_t h1m,
+                                             const int* aid, const double* x1, const int* offB,
+                                             const int* soff_s, const double* slz, const double* dxf_l,
+                                             const double* len_l, int v, int L, Spec* out) {
+  const DevView& d = V.d;
+  const int lane = threadIdx.x & 31, e = v & (kSpecLanes - 1), lead = lane & ~(kSpecLanes - 1);
+  const int u = v / kSpecLanes;
+  const bool in = u < 2 * L;
+  const int j = in ? (u >> 1) : 0, which = u & 1;
+  const int sb = soff_s[j], deg = soff_s[j + 1] - sb;
+  const bool wide = deg > kSpecDeg;
+  bool act = in && which < offB[j + 1] - offB[j] && deg > 0;
+  // every global load of the segment issued together (one memory latency)
+  const int k = act ? offB[j] + which : 0;
+  const double xk = act ? x1[k] : 0.0;
+  const int a = act ? aid[k] : -1;
+  const double* lz = slz + static_cast<std::size_t>(j) * d.maxdeg;
+  int sjv[2];
+  double lzv[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int ee = e + h * kSpecLanes;
+    const int ec = (act && !wide && ee < deg) ? ee : 0;
+    sjv[h] = act ? d.succ[sb + ec] : 0;
+    lzv[h] = act ? lz[ec] : 0.0;
+  }
+  act = act && xk + dxf_l[j] >= len_l[j] - kArrivalTol;
+  double y[2] = {0.0, 0.0}, gm[2] = {0.0, 0.0};
+  if (act && !wide) {
+    const std::uint64_t h2l = rng_prefix2(h1l, static_cast<std::uint64_t>(a));
+    std::uint64_t bl_[2], bm[2];
+    int bad = 0;
+    double gl[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const std::uint64_t sj = static_cast<std::uint64_t>(sjv[h]);
+      bl_[h] = rng_final(h2l, sj);
+      bm[h] = rng_final(rng_prefix2(h1m, sj), static_cast<std::uint64_t>(a));
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      gl[h] = gumbel_sl(bl_[h], bad);
+      gm[h] = gumbel_sl(bm[h], bad);
+    }
+    if (bad) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        gl[h] = gumbel_bits(bl_[h]);
+        gm[h] = gumbel_bits(bm[h]);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) y[h] = (lzv[h] + gl[h]) * d.kinv;
+  }
+  double yv[kSpecDeg], ex[kSpecDeg];
+#pragma unroll
+  for (int q = 0; q < kSpecLanes; ++q) {
+    yv[q] = __shfl_sync(0xffffffffu, y[0], lead + q);
+    yv[q + kSpecLanes] = __shfl_sync(0xffffffffu, y[1], lead + q);
+  }
+  int best = 0;
+  if (act && !wide && e == 0) best = softmax_first_argmax<kSpecDeg>(deg, yv, ex);
+  best = __shfl_sync(0xffffffffu, best, lead);
+  const double g0 = __shfl_sync(0xffffffffu, gm[0], lead + (best & (kSpecLanes - 1)));
+  const double g1 = __shfl_sync(0xffffffffu, gm[1], lead + (best & (kSpecLanes - 1)));
+  if (e != 0 || !in) return;
+  Spec r;
+  r.aid = -1;
+  r.c = -1;
+  r.g = 0.0;
+  if (act) {
+    r.aid = a;
+    if (!wide) {
+      r.c = d.succ[sb + best];
+      r.g = best < kSpecLanes ? g0 : g1;
+    } else {
+      head_draw(V, h1l, h1m, j, a, soff_s, slz, r.c, r.g);
+    }
+  }
+  out[u] = r;
+}
+
+// Link choice of one arrived head and its merge registration; the decision
+// comes from the speculative records when one of them is this agent's.
+__device__ __forceinline__ void head_choice(const CView& V, std::size_t bl, std::uint64_t h1l,
+                                            std::uint64_t h1m, int k, int j, int a, const int* soff_s,
+                                            const double* slz, const Spec* sp) {
+  const DevView& d = V.d;
+  int c;
+  double g;
+  if (sp && sp[0].aid == a) {
+    c = sp[0].c;
+    g = sp[0].g;
+  } else if (sp && sp[1].aid == a) {
+    c = sp[1].c;
+    g = sp[1].g;
+  } else {
+    head_draw(V, h1l, h1m, j, a, soff_s, slz, c, g);
+  }
+  Cand cd;
+  cd.alpha = d.alpha[bl + j];
+  cd.g = g;
   cd.slot = k;
   cd.aid = a;
   cd.link = j;
@@ -269,6 +387,8 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
     const int cur = t & 1, prv = cur ^ 1;
     const std::uint64_t h1l = rng_prefix1(seed_link, static_cast<std::uint64_t>(t));
     const std::uint64_t h1m = rng_prefix1(seed_merge, static_cast<std::uint64_t>(t));
+    // this step's speculative head decisions (drawn in step t-1's link phase)
+    const Spec* spec_t = (V.spec && t > 0) ? V.spec + ((t & 1) * BL + bl) * 2 : nullptr;
     if (!last) fstamp(V, t, 0);
     if (V.progress && t > 0 && (t % V.progress_every == 0 || last) && blockIdx.x == 0 &&
         threadIdx.x == 0) {
@@ -480,7 +600,8 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
               hq[kHeadCap + hi] = j;
               hq[2 * kHeadCap + hi] = aa[q];
             } else {
-              head_choice(V, bl, h1l, h1m, k, j, aa[q], soff_s, slz);
+              head_choice(V, bl, h1l, h1m, k, j, aa[q], soff_s, slz,
+                          spec_t ? spec_t + static_cast<std::size_t>(j) * 2 : nullptr);
             }
           }
         }
@@ -489,7 +610,8 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
         __syncthreads();
         const int nh = min(*hcnt, kHeadCap);
         for (int i = threadIdx.x; i < nh; i += blockDim.x)
-          head_choice(V, bl, h1l, h1m, hq[i], hq[kHeadCap + i], hq[2 * kHeadCap + i], soff_s, slz);
+          head_choice(V, bl, h1l, h1m, hq[i], hq[kHeadCap + i], hq[2 * kHeadCap + i], soff_s, slz,
+                      spec_t ? spec_t + static_cast<std::size_t>(hq[kHeadCap + i]) * 2 : nullptr);
       }
     }
     if (V.wstamp && active && !last) {
@@ -576,6 +698,25 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
           }
         }
         V.win[bl + i] = w;
+      }
+      // threads without a link draw step t+1's decisions of every link's
+      // first two agents while the merges run
+      if (V.spec && t + 1 < V.T) {
+        // whole warps past the link threads (Lr: L rounded up to a warp)
+        const int Lr = (L + 31) & ~31;
+        const int i0 = gw0 * 32 + (threadIdx.x & 31);
+        if (i0 >= Lr) {
+          const std::uint64_t n1l = rng_prefix1(seed_link, static_cast<std::uint64_t>(t + 1));
+          const std::uint64_t n1m = rng_prefix1(seed_merge, static_cast<std::uint64_t>(t + 1));
+          Spec* out = V.spec + (((t + 1) & 1) * BL + bl) * 2;
+          const int* aid_t = d.aid + sidx(d, t % d.S, bb);
+          const double* x1_t = V.x1b + cur * BN + bn;
+          const double* dxf_l = V.stage_params ? dxf_s : d.dxf + bl;
+          const double* len_l = V.stage_params ? len_s : d.len;
+          const int lane = threadIdx.x & 31;
+          for (int v = i0 - Lr; v - lane < 2 * L * kSpecLanes; v += nthr - Lr)
+            spec_segment(V, n1l, n1m, aid_t, x1_t, offB, soff_s, slz, dxf_l, len_l, v, L, out);
+        }
       }
     }
     fstamp(V, t, 3);

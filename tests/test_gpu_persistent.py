@@ -111,3 +111,31 @@ def test_dn1_full_hour_invariants_and_schedules():
         out.append((e.read_cum_all(), e.read_state(0, -1)))
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1][0], out[1][1][0]) and np.array_equal(out[0][1][1], out[1][1][1])
+
+
+@pytest.mark.parametrize("n,length,veh,dn,T,B,mode", [
+    (4, 400.0, 1000, 1, 600, 1, 2),
+    (23, 1609.34, 1000020, 30, 120, 1, 2),
+    (23, 1609.34, 1000020, 30, 120, 1, 1),
+    (23, 1609.34, 1000020, 1, 40, 1, 2),
+])
+def test_speculative_head_decisions_are_exact(n, length, veh, dn, T, B, mode):
+    """Heads whose decision was drawn one step ahead in the link phase
+    (dtg_set_flag 4, CView::spec) give the same trajectory bit for bit as
+    heads drawing in the slot phase."""
+    sc = P.Scenario.grid(n, length, 42, 1000.0).configure(veh, dn, T, 300)
+    p = sc.sample_parameters(3)
+    lk, ps = sc.seed_agents()
+    out = []
+    for spec in (1, 0):
+        e = P.Engine(sc, B, T)
+        e.set_mode(mode)
+        e.set_flag(4, spec)
+        e.set_params(p)
+        e.set_state(lk, ps)
+        e.set_noise(7, 5, 0)
+        e.forward(T, sc.steps_per_interval, checkpoint=True)
+        out.append((e.read_cum(0), e.read_state(0, T), e.read_state(0, T // 2)))
+    assert np.array_equal(out[0][0], out[1][0])
+    for a, b in zip(out[0][1:], out[1][1:]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
