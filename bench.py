@@ -90,7 +90,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -101,6 +101,21 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_first(self, timeout=5.0):
+        """Block until nvidia-smi delivers its first sample (its start-up takes
+        longer than a short timed region)."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.01)
+        self.mark = len(self.lines)
+
+    def under_load(self, fn, min_samples=3, max_s=2.0):
+        """Keep the same workload running (untimed) until the sampler has seen
+        `min_samples` samples since wait_first()."""
+        t0 = time.time()
+        while self.proc and len(self.lines) - getattr(self, "mark", 0) < min_samples and time.time() - t0 < max_s:
+            fn()
 
     def __exit__(self, *a):
         if self.proc:
@@ -114,7 +129,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "mark", 0):]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -268,12 +283,21 @@ def run_ours(args):
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        clk.wait_first()
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
             eng.forward(T_STEPS, SPI, checkpoint=False)
             ends[i].record(stream)
         torch.cuda.synchronize()
+
+        def more():  # the same workload, untimed, while the sampler catches up
+            for _ in range(20):
+                flush.zero_()
+                eng.forward(T_STEPS, SPI, checkpoint=False)
+            torch.cuda.synchronize()
+
+        clk.under_load(more)
     barrier(world)
     eng.sync()
     launches_per_step = eng.last_launches
