@@ -411,6 +411,64 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
         // all global loads of this thread's links first (one memory latency),
         // then the shared-memory updates
         constexpr int kPro = 8;
+        const int per = (L + blockDim.x - 1) / blockDim.x;
+        if (per <= kPro) {
+          // each thread owns the contiguous links [j0, j0 + per): the new
+          // segment sizes stay in registers for the scan (one CTA barrier less
+          // than writing them to shared memory for scan_f)
+          const int j0 = min(L, static_cast<int>(threadIdx.x) * per);
+          const int j1 = min(L, j0 + per);
+          int na_r[kPro], dp_r[kPro], w_r[kPro], sz[kPro];
+#pragma unroll
+          for (int u = 0; u < kPro; ++u) {
+            const int j = j0 + u;
+            const bool on = j < j1;
+            na_r[u] = on ? nAp[j] : 0;
+            dp_r[u] = on ? depp[j] : 0;
+            w_r[u] = on ? V.win[bl + j] : -1;
+          }
+          int sum = 0;
+#pragma unroll
+          for (int u = 0; u < kPro; ++u) {
+            const int j = j0 + u;
+            sz[u] = 0;
+            if (j < j1) {
+              const int nold = offA[j + 1] - offA[j];
+              na_s[j] = nold ? na_r[u] : 0;
+              dep_s[j] = dp_r[u];
+              win_s[j] = w_r[u];
+              sz[u] = nold - dp_r[u] + (w_r[u] >= 0 ? 1 : 0);
+              sum += sz[u];
+            }
+          }
+          // exclusive block scan of the per-thread sums (as scan_f)
+          const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+          int x = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          if (lane == 31) tmp[wid] = x;
+          __syncthreads();
+          int wt = lane < nw ? tmp[lane] : 0;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, wt, o);
+            if (lane >= o) wt += y;
+          }
+          const int before = __shfl_sync(0xffffffffu, wt, wid > 0 ? wid - 1 : 0);
+          const int total = __shfl_sync(0xffffffffu, wt, nw - 1);
+          int run = (wid ? before : 0) + x - sum;
+#pragma unroll
+          for (int u = 0; u < kPro; ++u)
+            if (j0 + u < j1) {
+              offB[j0 + u] = run;
+              run += sz[u];
+            }
+          if (threadIdx.x == 0) offB[L] = total;
+          __syncthreads();
+        } else {
         for (int j0 = threadIdx.x; j0 < L; j0 += kPro * blockDim.x) {
           int na_r[kPro], dp_r[kPro], w_r[kPro];
 #pragma unroll
@@ -435,6 +493,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
         }
         __syncthreads();
         scan_f(offB, L, tmp);
+        }
         if (rank == 0) {
           int* on = d.off + oidx(d, t % d.S, bb);
           for (int j = threadIdx.x; j <= L; j += blockDim.x) on[j] = offB[j];
