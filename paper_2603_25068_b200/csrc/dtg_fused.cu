@@ -190,14 +190,20 @@ __device__ __forceinline__ void spec_segment(const CView& V, std::uint64_t h1l, 
 // comes from the speculative records when one of them is this agent's.
 __device__ __forceinline__ void head_choice(const CView& V, std::size_t bl, std::uint64_t h1l,
                                             std::uint64_t h1m, int k, int j, int a, const int* soff_s,
-                                            const double* slz, const Spec* sp) {
+                                            const double* slz, const Spec* sp, const Spec* pre = nullptr) {
   const DevView& d = V.d;
   int c;
   double g;
-  if (sp && sp[0].aid == a) {
+  if (pre && pre[0].aid == a) {  // records prefetched by the caller
+    c = pre[0].c;
+    g = pre[0].g;
+  } else if (pre && pre[1].aid == a) {
+    c = pre[1].c;
+    g = pre[1].g;
+  } else if (!pre && sp && sp[0].aid == a) {
     c = sp[0].c;
     g = sp[0].g;
-  } else if (sp && sp[1].aid == a) {
+  } else if (!pre && sp && sp[1].aid == a) {
     c = sp[1].c;
     g = sp[1].g;
   } else {
@@ -575,6 +581,15 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
           rr[q] = k - offB[j];
           nn[q] = offB[j + 1] - offB[j];
         }
+        // one slot per thread: a leader slot prefetches its link's speculative
+        // records with the pulls (they are read only if it turns out arrived)
+        Spec pre[2];
+        pre[0].aid = pre[1].aid = -1;
+        const bool use_pre = kBatch == 1 && spec_t != nullptr && !last;
+        if (use_pre && kk[0] < N && rr[0] == 0) {
+          pre[0] = spec_t[static_cast<std::size_t>(jj[0]) * 2];
+          pre[1] = spec_t[static_cast<std::size_t>(jj[0]) * 2 + 1];
+        }
 #pragma unroll
         for (int q = 0; q < kBatch; ++q) {  // pull (all loads issued before use)
           const int k = kk[q], j = jj[q], r = rr[q], n = nn[q];
@@ -660,7 +675,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
               hq[2 * kHeadCap + hi] = aa[q];
             } else {
               head_choice(V, bl, h1l, h1m, k, j, aa[q], soff_s, slz,
-                          spec_t ? spec_t + static_cast<std::size_t>(j) * 2 : nullptr);
+                          spec_t ? spec_t + static_cast<std::size_t>(j) * 2 : nullptr, use_pre ? pre : nullptr);
             }
           }
         }
