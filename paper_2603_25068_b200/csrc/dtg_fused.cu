@@ -318,7 +318,10 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ep
 
 }  // namespace
 
-template <bool kCluster, int kBatch>
+// kFeat: the optional features (host-mapped progress, speculative head
+// decisions) are compiled in; without them the kernel is the plain schedule
+// (their mere presence costs the many-slots-per-thread variant ~10%).
+template <bool kCluster, int kBatch, bool kFeat>
 __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const DevView& d = V.d;
@@ -394,9 +397,9 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
     const std::uint64_t h1l = rng_prefix1(seed_link, static_cast<std::uint64_t>(t));
     const std::uint64_t h1m = rng_prefix1(seed_merge, static_cast<std::uint64_t>(t));
     // this step's speculative head decisions (drawn in step t-1's link phase)
-    const Spec* spec_t = (V.spec && t > 0) ? V.spec + ((t & 1) * BL + bl) * 2 : nullptr;
+    const Spec* spec_t = (kFeat && V.spec && t > 0) ? V.spec + ((t & 1) * BL + bl) * 2 : nullptr;
     if (!last) fstamp(V, t, 0);
-    if (V.progress && t > 0 && (t % V.progress_every == 0 || last) && blockIdx.x == 0 &&
+    if (kFeat && V.progress && t > 0 && (t % V.progress_every == 0 || last) && blockIdx.x == 0 &&
         threadIdx.x == 0) {
       // this thread acquired every CTA's step t-1 writes at the barrier; the
       // system-scope fence makes them visible to the copy engine before t is
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
         // records with the pulls (they are read only if it turns out arrived)
         Spec pre[2];
         pre[0].aid = pre[1].aid = -1;
-        const bool use_pre = kBatch == 1 && spec_t != nullptr && !last;
+        const bool use_pre = kFeat && kBatch == 1 && spec_t != nullptr && !last;
         if (use_pre && kk[0] < N && rr[0] == 0) {
           pre[0] = spec_t[static_cast<std::size_t>(jj[0]) * 2];
           pre[1] = spec_t[static_cast<std::size_t>(jj[0]) * 2 + 1];
@@ -775,7 +778,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
       }
       // threads without a link draw step t+1's decisions of every link's
       // first two agents while the merges run
-      if (V.spec && t + 1 < V.T) {
+      if (kFeat && V.spec && t + 1 < V.T) {
         // whole warps past the link threads (Lr: L rounded up to a warp)
         const int Lr = (L + 31) & ~31;
         const int i0 = gw0 * 32 + (threadIdx.x & 31);
@@ -803,10 +806,14 @@ int fused_smem_bytes(int L, bool stage_params) {
 }
 
 namespace {
-template <int KB>
+template <int KB, bool F>
 const void* fused_fn(bool cluster) {
-  return cluster ? reinterpret_cast<const void*>(k_forward_fused<true, KB>)
-                 : reinterpret_cast<const void*>(k_forward_fused<false, KB>);
+  return cluster ? reinterpret_cast<const void*>(k_forward_fused<true, KB, F>)
+                 : reinterpret_cast<const void*>(k_forward_fused<false, KB, F>);
+}
+const void* fused_pick(bool cluster, bool one, bool feat) {
+  if (one) return feat ? fused_fn<1, true>(cluster) : fused_fn<1, false>(cluster);
+  return feat ? fused_fn<4, true>(cluster) : fused_fn<4, false>(cluster);
 }
 }  // namespace
 
@@ -814,9 +821,11 @@ cudaError_t launch_forward_fused(const CView& V, bool cluster, cudaStream_t st) 
   const int smem = fused_smem_bytes(V.d.L, V.stage_params != 0);
   // one slot per thread -> kBatch 1
   const bool one = V.d.N <= V.cs * kClusterThreads;
-  const void* fn = one ? fused_fn<1>(cluster) : fused_fn<4>(cluster);
+  const bool feat = V.progress != nullptr || V.spec != nullptr;
+  const void* fn = fused_pick(cluster, one, feat);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
+  void* args[] = {const_cast<CView*>(&V)};
   if (cluster) {
     if (V.cs > 8) {
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -834,9 +843,8 @@ cudaError_t launch_forward_fused(const CView& V, bool cluster, cudaStream_t st) 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return one ? cudaLaunchKernelEx(&cfg, k_forward_fused<true, 1>, V) : cudaLaunchKernelEx(&cfg, k_forward_fused<true, 4>, V);
+    return cudaLaunchKernelExC(&cfg, fn, args);
   }
-  void* args[] = {const_cast<CView*>(&V)};
   return cudaLaunchCooperativeKernel(fn, dim3(V.d.B * V.cs), dim3(kClusterThreads), args, smem, st);
 }
 
@@ -845,26 +853,33 @@ int fused_max_grid(int L, bool stage_params) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int smem = fused_smem_bytes(L, stage_params);
-  for (const void* fn : {fused_fn<4>(false), fused_fn<1>(false)})
+  for (const void* fn : {fused_fn<4, false>(false), fused_fn<1, false>(false), fused_fn<4, true>(false),
+                         fused_fn<1, true>(false)})
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
       cudaGetLastError();
       return 0;
     }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_fn<4>(false), kClusterThreads, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, fused_fn<1>(false), kClusterThreads, smem);
-  return std::min(occ, occ1) * sms;
+  int best = INT_MAX;
+  for (const void* fn : {fused_fn<4, false>(false), fused_fn<1, false>(false), fused_fn<4, true>(false),
+                         fused_fn<1, true>(false)}) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kClusterThreads, smem);
+    best = std::min(best, occ);
+  }
+  (void)occ1;
+  return best * sms;
 }
 
 int fused_max_cluster(int L, bool stage_params) {
   const int smem = fused_smem_bytes(L, stage_params);
-  for (const void* fn : {fused_fn<4>(true), fused_fn<1>(true)}) {
+  for (const void* fn : {fused_fn<4, false>(true), fused_fn<1, false>(true), fused_fn<4, true>(true),
+                         fused_fn<1, true>(true)}) {
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
       cudaGetLastError();
       return 0;
     }
     cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
-  const void* fn = fused_fn<4>(true);
+  const void* fn = fused_fn<4, true>(true);
   for (int cs = 16; cs >= 1; cs >>= 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
