@@ -159,3 +159,27 @@ def test_c3_dn1_gradient_short(port):
     assert abs(g.loss - r["loss"]) <= 1e-9 * max(1.0, abs(r["loss"]))
     for blk in range(5):
         assert normwise(g.grads[blk], r["grads"][blk]) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("n_draws", [3, 160])
+def test_streamed_readback_matches_plain_reads(n_draws):
+    """dtg_simulate_forward streams count rows back while the kernel runs
+    (dtg_forward_read: progress counter in the persistent schedules, a plain
+    post-run copy in the step-graph schedule B > resident grid uses); the
+    results equal dtg_forward + dtg_read_cum_all / dtg_read_state."""
+    sc = P.Scenario.grid(4, 400.0, 42, 1000.0).configure(1000, 1, 90, 300)
+    p = sc.sample_parameters(3)
+    its = list(range(10, 10 + n_draws))
+    trs = P.simulate_forward(sc, p, seed=7, noise_iterations=its)
+    lk, ps = sc.seed_agents()
+    e = P.Engine(sc, n_draws, 90)
+    e.set_params(p)
+    e.set_state(lk, ps)
+    for b, it in enumerate(its):
+        e.set_noise(7, it, b)
+    e.forward(90, sc.steps_per_interval)
+    cum = e.read_cum_all()
+    for b, tr in enumerate(trs):
+        assert np.array_equal(tr.cum_per_step, cum[b])
+        lk_b, ps_b = e.read_state(b, -1)
+        assert np.array_equal(tr.link_final, lk_b) and np.array_equal(tr.pos_final, ps_b)
