@@ -127,6 +127,7 @@ struct dtg_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t par_ev = nullptr;
   double* h_par = nullptr;       // pinned parameter staging [5][L]
+  DevBuf<double> d_par;          // its device copy (broadcast to the scenarios by a kernel)
   void* h_fin = nullptr;         // pinned final state: int link[B*N] | double pos[B*N]
   std::size_t h_fin_n = 0;
   int mode = 0;          // 0 auto, 1 cluster, 2 grid-persistent, 3 step graph
@@ -648,6 +649,21 @@ int dtg_set_graphs(dtg_ctx* c, int enabled) {
   return DTG_OK;
 }
 
+namespace {
+// params [5][B][L] <- staging [5][L] for scenarios [b0, b0 + nb)
+__global__ void k_broadcast_params(const double* __restrict__ src, double* __restrict__ dst, int L, int B,
+                                   int b0, int nb) {
+  const std::size_t n = static_cast<std::size_t>(5) * nb * L;
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const int l = static_cast<int>(i % L);
+    const std::size_t r = i / L;
+    const int b = static_cast<int>(r % nb) + b0, q = static_cast<int>(r / nb);
+    dst[(static_cast<std::size_t>(q) * B + b) * L + l] = src[static_cast<std::size_t>(q) * L + l];
+  }
+}
+}  // namespace
+
 int dtg_set_params(dtg_ctx* c, int scenario, const double* u, const double* kappa,
                    const double* beta, const double* alpha, const double* cost) {
   return guarded(c, [&] {
@@ -661,33 +677,21 @@ int dtg_set_params(dtg_ctx* c, int scenario, const double* u, const double* kapp
     } else {
       CK(cudaEventSynchronize(c->par_ev));  // the previous upload has left the staging
     }
-    const double* src[5] = {c->h_par, c->h_par + L, c->h_par + 2 * L, c->h_par + 3 * L,
-                            c->h_par + 4 * L};
     {
       const double* in[5] = {u, kappa, beta, alpha, cost};
       for (int q = 0; q < 5; ++q) std::memcpy(c->h_par + q * L, in[q], L * sizeof(double));
     }
-    if (scenario < 0) {
-      // one upload, then doubling device copies to the other scenarios
-      for (int q = 0; q < 5; ++q) {
-        double* base = c->params.p + q * BL;
-        CK(cudaMemcpyAsync(base, src[q], L * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        for (std::size_t have = 1; have < static_cast<std::size_t>(c->B); have *= 2) {
-          const std::size_t n = std::min<std::size_t>(have, c->B - have);
-          CK(cudaMemcpyAsync(base + have * L, base, n * L * sizeof(double),
-                             cudaMemcpyDeviceToDevice, c->stream));
-        }
-      }
-      for (int b = 0; b < c->B; ++b) c->have_params[b] = 1;
-    }
-    for (int b = 0; b < c->B && scenario >= 0; ++b) {
-      if (b != scenario) continue;
-      for (int q = 0; q < 5; ++q)
-        CK(cudaMemcpyAsync(c->params.p + q * BL + b * L, src[q], L * sizeof(double),
-                           cudaMemcpyHostToDevice, c->stream));
-      c->have_params[b] = 1;
-    }
+    // one upload of [5][L], then one kernel writes it to the scenario(s)
+    c->d_par.ensure(5 * L);
+    CK(cudaMemcpyAsync(c->d_par.p, c->h_par, 5 * L * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     CK(cudaEventRecord(c->par_ev, c->stream));
+    const int b0 = scenario < 0 ? 0 : scenario, nb = scenario < 0 ? c->B : 1;
+    const std::size_t n = 5 * static_cast<std::size_t>(nb) * L;
+    const int grid = static_cast<int>(std::min<std::size_t>((n + 255) / 256, 1184));
+    k_broadcast_params<<<grid, 256, 0, c->stream>>>(c->d_par.p, c->params.p, static_cast<int>(L), c->B, b0, nb);
+    CK(cudaGetLastError());
+    for (int b = b0; b < b0 + nb; ++b) c->have_params[b] = 1;
+    (void)BL;
   });
 }
 
