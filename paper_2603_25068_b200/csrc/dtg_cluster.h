@@ -63,6 +63,26 @@ struct CView {
 };
 
 void launch_pack_succ(const DevView& d, double* srec, cudaStream_t st);
+
+// Pre-step state of the persistent forward (k_forward_init, dtg_cluster.cu).
+struct ForwardInit {
+  DevView d;
+  double *jam, *dxf, *pref, *srec;
+  double* pos;
+  const double* pos0;
+  int* aid;
+  const int* aid0;
+  int* lnk;
+  const int* lnk0;
+  int* off;
+  const int* off0;
+  double* qh;
+  const double* q0;
+  double* cumh;
+  int *errf, *ccnt, *depb;
+  unsigned int* gbar;
+};
+void launch_forward_init(const ForwardInit& a, cudaStream_t st);
 int fused_smem_bytes(int L, bool stage_params);
 int fused_max_grid(int L, bool stage_params);
 int fused_max_cluster(int L, bool stage_params);

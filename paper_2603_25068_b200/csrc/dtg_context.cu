@@ -128,6 +128,8 @@ struct dtg_ctx {
   cudaEvent_t par_ev = nullptr;
   double* h_par = nullptr;       // pinned parameter staging [5][L]
   DevBuf<double> d_par;          // its device copy (broadcast to the scenarios by a kernel)
+  std::uint64_t* h_seed_pin = nullptr;  // pinned seed staging [2][B]
+  cudaEvent_t seed_ev = nullptr;
   void* h_fin = nullptr;         // pinned final state: int link[B*N] | double pos[B*N]
   std::size_t h_fin_n = 0;
   int mode = 0;          // 0 auto, 1 cluster, 2 grid-persistent, 3 step graph
@@ -237,6 +239,8 @@ struct dtg_ctx {
     if (h_par) cudaFreeHost(h_par);
     if (h_fin) cudaFreeHost(h_fin);
     if (par_ev) cudaEventDestroy(par_ev);
+    if (h_seed_pin) cudaFreeHost(h_seed_pin);
+    if (seed_ev) cudaEventDestroy(seed_ev);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -743,8 +747,18 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
                                     " has no parameters or initial state");
     c->ensure_history(T, checkpoint);
     cudaStream_t st = c->stream;
-    CK(cudaMemcpyAsync(c->seeds.p, c->h_seeds.data(), sizeof(std::uint64_t) * 2 * c->B,
-                       cudaMemcpyHostToDevice, st));
+    {  // seeds through pinned staging: an asynchronous upload, no host wait
+      const std::size_t sb = sizeof(std::uint64_t) * 2 * c->B;
+      if (!c->h_seed_pin) {
+        CK(cudaMallocHost(&c->h_seed_pin, sb));
+        CK(cudaEventCreateWithFlags(&c->seed_ev, cudaEventDisableTiming));
+      } else {
+        CK(cudaEventSynchronize(c->seed_ev));
+      }
+      std::memcpy(c->h_seed_pin, c->h_seeds.data(), sb);
+      CK(cudaMemcpyAsync(c->seeds.p, c->h_seed_pin, sb, cudaMemcpyHostToDevice, st));
+      CK(cudaEventRecord(c->seed_ev, st));
+    }
     const dtg::DevView d = c->view();
     const std::size_t BN = static_cast<std::size_t>(c->B) * c->N;
     const std::size_t BL = static_cast<std::size_t>(c->B) * c->L;
@@ -778,19 +792,31 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
     if (!c->persistent && c->mode == 0) mode = 3;
     c->last_mode = mode;
     if ((mode == 1 || mode == 2) && T > 0) {
-      dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
-      dtg::launch_pack_succ(d, c->srec.p, st);
-      CK(cudaMemcpyAsync(c->pos.p, c->pos0.p, BN * 8, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(c->aid.p, c->aid0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(c->lnk.p, c->lnk0.p, BN * 4, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(c->off.p, c->off0.p, static_cast<std::size_t>(c->B) * (c->L + 1) * 4,
-                         cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(c->qh.p, c->q0.p, BL * 8, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemsetAsync(c->cumh.p, 0, BL * 8, st));
-      CK(cudaMemsetAsync(c->errf.p, 0, sizeof(int) * c->B, st));
-      CK(cudaMemsetAsync(c->ccnt.p, 0, BL * 4, st));
-      CK(cudaMemsetAsync(c->depb.p, 0, 2 * BL * 4, st));
-      CK(cudaMemsetAsync(c->gbar.p, 0, sizeof(unsigned int), st));
+      {  // one launch for the per-link constants, the initial layout and the counters
+        dtg::ForwardInit in{};
+        in.d = d;
+        in.jam = c->derived.p;
+        in.dxf = c->derived.p + BL;
+        in.pref = c->derived.p + 2 * BL;
+        in.srec = c->srec.p;
+        in.pos = c->pos.p;
+        in.pos0 = c->pos0.p;
+        in.aid = c->aid.p;
+        in.aid0 = c->aid0.p;
+        in.lnk = c->lnk.p;
+        in.lnk0 = c->lnk0.p;
+        in.off = c->off.p;
+        in.off0 = c->off0.p;
+        in.qh = c->qh.p;
+        in.q0 = c->q0.p;
+        in.cumh = c->cumh.p;
+        in.errf = c->errf.p;
+        in.ccnt = c->ccnt.p;
+        in.depb = c->depb.p;
+        in.gbar = c->gbar.p;
+        dtg::launch_forward_init(in, st);
+        CK(cudaGetLastError());
+      }
       dtg::CView V{};
       V.d = d;
       V.x1b = c->x1b.p;
