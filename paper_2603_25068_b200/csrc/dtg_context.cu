@@ -867,7 +867,7 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
         V.tstamp = c->stamps.p;
       }
       CK(dtg::launch_forward_fused(V, mode == 1, st));
-      c->launches = 3;
+      c->launches = 2;  // k_forward_init + k_forward_fused
       c->last_T = T;
       c->last_spi = spi;
       c->last_ckpt = checkpoint;
