@@ -36,8 +36,11 @@ namespace dtg {
 
 namespace {
 
-// kBatch: slots per thread in flight together (4; 1 when every thread owns at
-// most one slot, which leaves the arrived-head draw chains more registers)
+// kBatch: slots per thread in flight together (2; 1 when every thread owns at
+// most one slot, which leaves the arrived-head draw chains more registers).
+// Measured at dn=1 (1M agents): 2 beats 4 by 11% (4 slots' state under the
+// 128-register cap made ptxas rematerialise addresses in the loop) and 1 and 3
+// are slower.
 constexpr int kHeadCap = 1024;  // deferred arrived heads per CTA (overflow runs inline)
 
 constexpr int kFastDeg = 5;  // successor counts up to this take the unrolled head path
@@ -813,7 +816,7 @@ const void* fused_fn(bool cluster) {
 }
 const void* fused_pick(bool cluster, bool one, bool feat) {
   if (one) return feat ? fused_fn<1, true>(cluster) : fused_fn<1, false>(cluster);
-  return feat ? fused_fn<4, true>(cluster) : fused_fn<4, false>(cluster);
+  return feat ? fused_fn<2, true>(cluster) : fused_fn<2, false>(cluster);
 }
 }  // namespace
 
@@ -853,14 +856,14 @@ int fused_max_grid(int L, bool stage_params) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int smem = fused_smem_bytes(L, stage_params);
-  for (const void* fn : {fused_fn<4, false>(false), fused_fn<1, false>(false), fused_fn<4, true>(false),
+  for (const void* fn : {fused_fn<2, false>(false), fused_fn<1, false>(false), fused_fn<2, true>(false),
                          fused_fn<1, true>(false)})
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
       cudaGetLastError();
       return 0;
     }
   int best = INT_MAX;
-  for (const void* fn : {fused_fn<4, false>(false), fused_fn<1, false>(false), fused_fn<4, true>(false),
+  for (const void* fn : {fused_fn<2, false>(false), fused_fn<1, false>(false), fused_fn<2, true>(false),
                          fused_fn<1, true>(false)}) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kClusterThreads, smem);
     best = std::min(best, occ);
@@ -871,7 +874,7 @@ int fused_max_grid(int L, bool stage_params) {
 
 int fused_max_cluster(int L, bool stage_params) {
   const int smem = fused_smem_bytes(L, stage_params);
-  for (const void* fn : {fused_fn<4, false>(true), fused_fn<1, false>(true), fused_fn<4, true>(true),
+  for (const void* fn : {fused_fn<2, false>(true), fused_fn<1, false>(true), fused_fn<2, true>(true),
                          fused_fn<1, true>(true)}) {
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
       cudaGetLastError();
@@ -879,7 +882,7 @@ int fused_max_cluster(int L, bool stage_params) {
     }
     cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
-  const void* fn = fused_fn<4, true>(true);
+  const void* fn = fused_fn<2, true>(true);
   for (int cs = 16; cs >= 1; cs >>= 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
