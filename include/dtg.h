@@ -90,6 +90,8 @@ int dtg_set_mode(dtg_ctx* ctx, int mode);
  * %globaltimer stamps; phase_us[8] = mean per-step span (us) of R1, barrier,
  * R2, barrier, R3, barrier, R4 (and 0). */
 int dtg_profile_backward(dtg_ctx* ctx, double* phase_us, int* grid_out);
+/* Measurement hook: raw per-CTA stamps [T][grid][8] (ns) of that run. */
+int dtg_debug_bwd_stamps(dtg_ctx* ctx, unsigned long long* out, int* grid);
 int dtg_last_mode(const dtg_ctx* ctx);
 /* Tuning knobs: flag 0 = grid barrier implementation (1: release/acquire
  * counter, default; 0: cooperative_groups grid.sync); flag 1 = fused

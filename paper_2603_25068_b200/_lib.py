@@ -154,6 +154,7 @@ SIGNATURES = [
     ("dtg_debug_microbench", i32, [i32, i32, i32, _dp]),
     ("dtg_debug_log_check", i32, [u64, C.c_longlong, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     ("dtg_debug_warp_records", i32, [vp, i32, i32, vp, C.POINTER(C.c_int)]),
+    ("dtg_debug_bwd_stamps", i32, [vp, vp, C.POINTER(C.c_int)]),
     ("dtg_scenario_last_error", C.c_char_p, [vp]),
     # FD-validation instrumentation
     ("dtg_surrogate_create", vp, []),

@@ -595,6 +595,16 @@ int dtg_last_mode(const dtg_ctx* c) { return c->last_mode * 100 + c->last_cs; }
 static void run_backward(dtg_ctx* c, const double* snap, const double* cum, const double* xs,
                          cudaMemcpyKind kind, bool seeds_ready = false);
 
+// Measurement hook: the raw per-CTA phase stamps [T][grid][8] (ns) of the last
+// dtg_profile_backward run.
+int dtg_debug_bwd_stamps(dtg_ctx* c, unsigned long long* out, int* grid) {
+  return guarded(c, [&] {
+    const int T = c->last_T, G = c->last_bgrid;
+    *grid = G;
+    if (out) CK(cudaMemcpy(out, c->stamps.p, static_cast<std::size_t>(T) * G * 8 * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
 int dtg_profile_backward(dtg_ctx* c, double* phase_us, int* grid_out) {
   return guarded(c, [&] {
     if (c->last_T < 1 || !c->last_ckpt) throw std::runtime_error("needs a checkpointed forward");
