@@ -60,6 +60,10 @@ struct CView {
   // only agents that can be its arrived head at t+1); the slot phase of t+1
   // then only registers them (null: heads draw in the slot phase)
   Spec* spec;
+  // 1: the speculative draws run in warps 2.. of each CTA between arriving at
+  // and waiting on barrier 1 (needs every link's merge thread in warps 0-1,
+  // i.e. 64 cs >= L; one slot per thread; grid schedule)
+  int spec_split;
 };
 
 void launch_pack_succ(const DevView& d, double* srec, cudaStream_t st);

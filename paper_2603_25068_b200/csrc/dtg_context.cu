@@ -139,6 +139,7 @@ struct dtg_ctx {
   DevBuf<double> srec;
   DevBuf<dtg::Spec> spec;  // speculative head decisions [2][B][L][2]
   bool speculate = true;
+  bool spec_split = true;  // flag 5
   DevBuf<unsigned int> gbar, bgbar;
   bool custom_barrier = true;
   int contig_mode = -1;
@@ -579,6 +580,9 @@ int dtg_set_flag(dtg_ctx* c, int flag, int value) {
     case 4:  // fused forward: speculative head decisions one step ahead (1 default, 0 off)
       c->speculate = value != 0;
       return DTG_OK;
+    case 5:  // ... drawn by warps 2.. during barrier 1 (1 default) or by idle link-phase lanes (0)
+      c->spec_split = value != 0;
+      return DTG_OK;
     default:
       return fail(c, DTG_ERR_CONFIG, "unknown flag");
   }
@@ -867,6 +871,10 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
         c->spec.ensure(static_cast<std::size_t>(4) * BL);
         V.spec = c->spec.p;
       }
+      V.spec_split = (c->spec_split && V.spec && mode == 2 && V.gbar && V.cs * 64 >= c->L &&
+                      c->N <= V.cs * dtg::kClusterThreads)
+                         ? 1
+                         : 0;
       V.wstamp = nullptr;
       if (c->want_wstamp) {
         c->wst.ensure(static_cast<std::size_t>(T) * c->B * V.cs * (dtg::kClusterThreads / 32) * 4 + 4);

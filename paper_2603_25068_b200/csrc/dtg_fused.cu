@@ -189,6 +189,24 @@ __device__ __forceinline__ void spec_segment(const CView& V, std::uint64_t h1l, 
   out[u] = r;
 }
 
+// The same decisions for a CTA-local candidate list (split schedule): entry i
+// of the list is (link, which, agent), already filtered by its slot owner.
+// One lane per candidate (head_draw's chain; the ~3.5 us the link warps spend
+// on the grid barrier and the link phase cover it) over warps 2.. of the CTA,
+// so even a CTA whose 512 slots hold hundreds of short links finishes in one
+// round.
+__device__ __forceinline__ void spec_list(const CView& V, std::uint64_t h1l, std::uint64_t h1m,
+                                          const int* lst, int n, int cap, const int* soff_s,
+                                          const double* slz, Spec* out) {
+  for (int ci = static_cast<int>(threadIdx.x) - 64; ci < n; ci += static_cast<int>(blockDim.x) - 64) {
+    const int j = lst[ci], which = lst[cap + ci], a = lst[2 * cap + ci];
+    Spec r;
+    r.aid = a;
+    head_draw(V, h1l, h1m, j, a, soff_s, slz, r.c, r.g);
+    out[static_cast<std::size_t>(j) * 2 + which] = r;
+  }
+}
+
 // Link choice of one arrived head and its merge registration; the decision
 // comes from the speculative records when one of them is this agent's.
 __device__ __forceinline__ void head_choice(const CView& V, std::size_t bl, std::uint64_t h1l,
@@ -401,6 +419,9 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
     const std::uint64_t h1m = rng_prefix1(seed_merge, static_cast<std::uint64_t>(t));
     // this step's speculative head decisions (drawn in step t-1's link phase)
     const Spec* spec_t = (kFeat && V.spec && t > 0) ? V.spec + ((t & 1) * BL + bl) * 2 : nullptr;
+    // split schedule: the slot owners list the next step's candidates in shared
+    // memory; warps 2.. draw them while warps 0-1 wait at the grid barrier
+    const bool split = kFeat && kBatch == 1 && !kCluster && V.spec && V.spec_split && V.gbar && !last;
     if (!last) fstamp(V, t, 0);
     if (kFeat && V.progress && t > 0 && (t % V.progress_every == 0 || last) && blockIdx.x == 0 &&
         threadIdx.x == 0) {
@@ -547,7 +568,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
       // shared memory and their link choices run after the loop, one per
       // thread, instead of serialising a draw chain into every batch.
       const bool defer = limit - off0 > stride;
-      if (defer) {
+      if (defer || split) {
         if (threadIdx.x == 0) *hcnt = 0;
         __syncthreads();
       }
@@ -665,6 +686,15 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
             fa_n = nx.x1 >= thr;
           }
           const bool fo = me.x1 >= ctr, fa = me.x1 >= thr;
+          if (split && t + 1 < V.T && r <= 1 && soff_s[j + 1] > soff_s[j] && me.x1 + dxf >= thr) {
+            // can head link j at step t+1 (fl(x1 + u dt) < L - 0.01 rules it out exactly)
+            const int li = atomicAdd(hcnt, 1);
+            if (li < kHeadCap) {
+              hq[li] = j;
+              hq[kHeadCap + li] = r;
+              hq[2 * kHeadCap + li] = aa[q];
+            }
+          }
           if (r == 0 && !fo) qnc[j] = 0;
           if (fo && !fo_n) qnc[j] = r + 1;
           if (r == 0 && !fa) nAc[j] = 0;
@@ -708,8 +738,35 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
     }
     if (last) break;
     fstamp(V, t, 1);
-    barrier();
-    fstamp(V, t, 2);
+    if (split && active) {
+      __syncthreads();  // the slot phase and the candidate list are complete
+      if (threadIdx.x == 0) {
+        ++epoch;
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(V.gbar), "r"(1u) : "memory");
+      }
+      if (threadIdx.x < 64) {  // warps 0-1: the link phase after the barrier
+        if (threadIdx.x == 0) {
+          const unsigned int target = epoch * gridDim.x;
+          unsigned int v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(V.gbar) : "memory");
+          } while (v < target);
+        }
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+      } else if (t + 1 < V.T) {  // warps 2..: the next step's decisions (no cross-CTA inputs)
+        spec_list(V, rng_prefix1(seed_link, static_cast<std::uint64_t>(t + 1)),
+                  rng_prefix1(seed_merge, static_cast<std::uint64_t>(t + 1)), hq, min(*hcnt, kHeadCap),
+                  kHeadCap, soff_s, slz, V.spec + (((t + 1) & 1) * BL + bl) * 2);
+      }
+      if (V.tstamp && threadIdx.x == 0) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        V.tstamp[(static_cast<std::size_t>(t) * gridDim.x + blockIdx.x) * 4 + 2] = ns;
+      }
+    } else {
+      barrier();
+      fstamp(V, t, 2);
+    }
     if (active) {
       // ---------------- link phase ----------------
       double* tailc = V.tailb + cur * BL + bl;
@@ -781,7 +838,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
       }
       // threads without a link draw step t+1's decisions of every link's
       // first two agents while the merges run
-      if (kFeat && V.spec && t + 1 < V.T) {
+      if (kFeat && V.spec && !split && t + 1 < V.T) {
         // whole warps past the link threads (Lr: L rounded up to a warp)
         const int Lr = (L + 31) & ~31;
         const int i0 = gw0 * 32 + (threadIdx.x & 31);
