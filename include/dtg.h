@@ -96,8 +96,10 @@ int dtg_last_mode(const dtg_ctx* ctx);
 /* Tuning knobs: flag 0 = grid barrier implementation (1: release/acquire
  * counter, default; 0: cooperative_groups grid.sync); flag 1 = fused
  * forward slot mapping (-1 auto, 0 interleaved blocks, 1 contiguous);
- * flag 4 = fused forward draws the next step's head decisions in the link
- * phase (1, default) or in the slot phase (0).  Results are identical. */
+ * flag 4 = fused forward draws the next step's head decisions ahead of time
+ * (1, default) or in the slot phase (0); flag 5 = those draws run in warps
+ * 2.. of each CTA during barrier 1 (1, default) or in idle link-phase lanes
+ * (0).  Results are identical. */
 int dtg_set_flag(dtg_ctx* ctx, int flag, int value);
 /* Measurement hook: one persistent forward with %globaltimer stamps; returns
  * the mean per-step span (us) of [slot phase, barrier 1, link phase,

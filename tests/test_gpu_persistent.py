@@ -127,15 +127,17 @@ def test_speculative_head_decisions_are_exact(n, length, veh, dn, T, B, mode):
     p = sc.sample_parameters(3)
     lk, ps = sc.seed_agents()
     out = []
-    for spec in (1, 0):
+    for spec, split in ((1, 1), (1, 0), (0, 0)):  # barrier-1 warps, link-phase lanes, off
         e = P.Engine(sc, B, T)
         e.set_mode(mode)
         e.set_flag(4, spec)
+        e.set_flag(5, split)
         e.set_params(p)
         e.set_state(lk, ps)
         e.set_noise(7, 5, 0)
         e.forward(T, sc.steps_per_interval, checkpoint=True)
         out.append((e.read_cum(0), e.read_state(0, T), e.read_state(0, T // 2)))
-    assert np.array_equal(out[0][0], out[1][0])
-    for a, b in zip(out[0][1:], out[1][1:]):
-        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for o in out[1:]:
+        assert np.array_equal(out[0][0], o[0])
+        for a, b in zip(out[0][1:], o[1:]):
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
