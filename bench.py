@@ -487,9 +487,10 @@ def run_gradient(P, torch, world, rank, args):
     run(2)  # warm-up: context, graphs, loss buffers
     n_it = max(5, args.steps)
     walls = []
-    for n in (n_it, 2 * n_it):  # per-call setup (seeding, state upload) cancels in the difference
+    sizes = (n_it, 2 * n_it, 3 * n_it)
+    for n in sizes:  # per-call setup (seeding, state upload) is the intercept of the fit
         best = None
-        for _ in range(3):  # best of three calls: host-side jitter only ever adds time
+        for _ in range(5):  # best of five calls: host-side jitter only ever adds time
             barrier(world)
             torch.cuda.synchronize()
             t = time.perf_counter()
@@ -498,8 +499,9 @@ def run_gradient(P, torch, world, rank, args):
             w = max_over_ranks(time.perf_counter() - t, world)
             best = w if best is None else min(best, w)
         walls.append(best)
-    s_iter = (walls[1] - walls[0]) / n_it
-    setup_s = walls[0] - n_it * s_iter
+    mx, my = statistics.mean(sizes), statistics.mean(walls)
+    s_iter = sum((x - mx) * (y - my) for x, y in zip(sizes, walls)) / sum((x - mx) ** 2 for x in sizes)
+    setup_s = my - s_iter * mx
     # device time of the two passes (CUDA events on the engine's stream)
     local = CAL_DRAWS // world
     eng = P.Engine(sc, n_scenarios=local, max_steps=T)
@@ -526,7 +528,7 @@ def run_gradient(P, torch, world, rank, args):
     eng.forward(T, SPI, checkpoint=True)
     phases_b, grid_b = eng.profile_backward()
     return {"s_per_iter": s_iter, "setup_s_per_calibrate_call": setup_s,
-            "wall_s": {f"{n_it}_it": walls[0], f"{2 * n_it}_it": walls[1]},
+            "wall_s": {f"{n}_it": w for n, w in zip(sizes, walls)},
             "draws": CAL_DRAWS, "draws_per_gpu": local, "steps": T,
             "iterations_timed": n_it, "params": 4 * L, "loss_first": float(res.loss_curve[0]),
             "loss_last": float(res.loss_curve[-1]),
@@ -535,9 +537,10 @@ def run_gradient(P, torch, world, rank, args):
             "fwd_ckpt_ms_per_pass": statistics.median(fwd_ms), "adj_ms_per_pass": statistics.median(adj_ms),
             "fwd_phase_us_per_step": {k: round(x, 2) for k, x in phases_f.items()},
             "adj_phase_us_per_step": {k: round(x, 2) for k, x in phases_b.items()},
-            "timing": "wall clock per calibrate() iteration through the public API (best of 3 calls each) (device loss/seeds/draw sum, "
-                      "NCCL row gather for N>1, host transform + AdamW, 1 sync per iteration): difference of "
-                      "a 2n- and an n-iteration calibrate call / n; the per-call setup is reported separately"}
+            "timing": "wall clock per calibrate() iteration through the public API (device loss/seeds/draw "
+                      "sum, NCCL row gather for N>1, host transform + AdamW, 1 sync per iteration): least-squares "
+                      "slope of the best-of-5 wall times of n-, 2n- and 3n-iteration calibrate calls; the per-call "
+                      "setup (the intercept) is reported separately"}
 
 
 # ---- reference arm -----------------------------------------------------------------------
