@@ -457,6 +457,22 @@ def run_throughput(P, torch, sc, p, lk0, ps0, args):
                         "note": "16 MB/step of algorithmic traffic against a ~50 MB working set that stays "
                                 "L2-resident; latency/issue-bound (profiles/r01/ncu_fused_dn1_summary.md)"}
     del eng
+    # C2 (BASELINE configs[1]): 50x50 grid, 400 m links, 100,000 vehicles at dn = 1, 1 h
+    sc2 = P.Scenario.grid(50, 400.0, NET_SEED, VIRT_LEN).configure(100000, 1, 3600, OBS_S)
+    p2 = sc2.sample_parameters(PARAM_SEED)
+    l2, q2 = sc2.seed_agents()
+    eng = P.Engine(sc2, n_scenarios=1, max_steps=3600)
+    eng.set_stream(torch.cuda.current_stream().cuda_stream)
+    eng.set_params(p2)
+    eng.set_state(l2, q2)
+    eng.set_noise(SIM_SEED, 0, 0)
+    s = timed(eng, 3600, sc2.steps_per_interval, reps=2)
+    N2, L2 = sc2.n_agents, sc2.n_links
+    alg = 3600 * (16 * N2 + 64 * L2)
+    out["c2_dn1_B1"] = {"agents": N2, "links": L2, "steps": 3600, "ms_per_nowcast": s * 1e3,
+                        "rtf": SIM_SECONDS / s, "us_per_step": s / 3600 * 1e6, "alg_GBps": alg / s / 1e9,
+                        "hbm_frac": alg / s / 1e9 / peak, "schedule": eng.last_mode}
+    del eng
     return out
 
 
