@@ -64,6 +64,7 @@ struct CView {
   // and waiting on barrier 1 (needs every link's merge thread in warps 0-1,
   // i.e. 64 cs >= L; one slot per thread; grid schedule)
   int spec_split;
+  int lean;  // fused_lean(L): the per-link shared-memory arrays are read from global memory
 };
 
 void launch_pack_succ(const DevView& d, double* srec, cudaStream_t st);
@@ -88,6 +89,7 @@ struct ForwardInit {
 };
 void launch_forward_init(const ForwardInit& a, cudaStream_t st);
 int fused_smem_bytes(int L, bool stage_params);
+bool fused_lean(int L);  // per-link arrays in global memory (large networks)
 int fused_max_grid(int L, bool stage_params);
 int fused_max_cluster(int L, bool stage_params);
 cudaError_t launch_forward_fused(const CView& V, bool cluster, cudaStream_t st);

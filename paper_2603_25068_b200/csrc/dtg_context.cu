@@ -474,7 +474,7 @@ int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
     c->winp.alloc(BL);
     c->ccnt.alloc(BL);
     c->clist.alloc(1);
-    c->stage_params = dtg::fused_smem_bytes(L, true) <= 200 * 1024;
+    c->stage_params = !dtg::fused_lean(L) && dtg::fused_smem_bytes(L, true) <= 200 * 1024;
     c->pgrid_max = dtg::fused_max_grid(L, c->stage_params);
     c->bgrid_max = dtg::backward_max_grid(L, c->maxdeg);
     c->cluster_cs_max = dtg::fused_max_cluster(L, c->stage_params);
@@ -847,6 +847,7 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       V.ckpt = checkpoint ? 1 : 0;
       V.dbg = c->fwd_dbg;
       V.stage_params = c->stage_params ? 1 : 0;
+      V.lean = dtg::fused_lean(c->L) ? 1 : 0;
       V.tstamp = nullptr;
       V.gbar = c->custom_barrier ? c->gbar.p : nullptr;
       // grid mode: CTA 0 sees every scenario's step complete at the grid

@@ -253,6 +253,7 @@ __device__ __forceinline__ int find_link_w(const int* off_s, int lo, int hi, int
   return lo;
 }
 
+template <bool kMask = false>
 __device__ __forceinline__ int pull_f(int j, int rn, const int* offA, const int* offB, const int* na_s,
                                       const int* dep_s, const int* win_s, const int* wonp, bool* entrant) {
   const int w = win_s[j];
@@ -262,7 +263,7 @@ __device__ __forceinline__ int pull_f(int j, int rn, const int* offA, const int*
   }
   *entrant = false;
   const int ob = offA[j];
-  const int na = na_s[j];
+  const int na = (!kMask || offA[j + 1] > ob) ? na_s[j] : 0;  // lean layout: the unmasked global array
   const int dp = dep_s[j];
   if (rn >= na - dp) return ob + rn + dp;
   int c = -1;
@@ -342,7 +343,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ep
 // kFeat: the optional features (host-mapped progress, speculative head
 // decisions) are compiled in; without them the kernel is the plain schedule
 // (their mere presence costs the many-slots-per-thread variant ~10%).
-template <bool kCluster, int kBatch, bool kFeat>
+template <bool kCluster, int kBatch, bool kFeat, bool kLean>
 __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const DevView& d = V.d;
@@ -378,12 +379,32 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
   int* ip = reinterpret_cast<int*>(dp);
   int* offA = ip;
   int* offB = ip + (L + 1);
-  int* na_s = ip + 2 * (L + 1);
-  int* dep_s = na_s + L;
-  int* win_s = dep_s + L;
-  int* soff_s = win_s + L;  // succ_off, L + 1
-  int* poff_s = soff_s + (L + 1);  // pred_off, L + 1
-  int* tmp = poff_s + (L + 1);
+  // lean layout (networks whose per-link arrays do not fit shared memory):
+  // succ_off / pred_off are read from global memory, and the pulls read the
+  // previous step's arrived / departure / winner arrays directly
+  const int* na_s;
+  const int* dep_s;
+  const int* win_s;
+  int *na_w = nullptr, *dep_w = nullptr, *win_w = nullptr;
+  const int* soff_s;
+  const int* poff_s;
+  int* tmp;
+  if (!kLean) {
+    na_w = ip + 2 * (L + 1);
+    dep_w = na_w + L;
+    win_w = dep_w + L;
+    na_s = na_w;
+    dep_s = dep_w;
+    win_s = win_w;
+    soff_s = win_w + L;               // succ_off, L + 1
+    poff_s = soff_s + (L + 1);        // pred_off, L + 1
+    tmp = const_cast<int*>(poff_s) + (L + 1);
+  } else {
+    na_s = dep_s = win_s = nullptr;
+    soff_s = d.succ_off;
+    poff_s = d.pred_off;
+    tmp = ip + 2 * (L + 1);
+  }
   int* hcnt = tmp + 34;              // deferred-head count
   int* hq = tmp + 36;                // [3][kHeadCap] deferred heads: slot, link, agent
   const int bb = active ? b : 0;
@@ -398,12 +419,14 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
         dxf_s[j] = d.dxf[bl + j];
         len_s[j] = d.len[j];
       }
-      soff_s[j] = d.succ_off[j];
-      poff_s[j] = d.pred_off[j];
+      if (!kLean) {
+        const_cast<int*>(soff_s)[j] = d.succ_off[j];
+        const_cast<int*>(poff_s)[j] = d.pred_off[j];
+      }
     }
-    if (threadIdx.x == 0) {
-      soff_s[L] = d.succ_off[L];
-      poff_s[L] = d.pred_off[L];
+    if (threadIdx.x == 0 && !kLean) {
+      const_cast<int*>(soff_s)[L] = d.succ_off[L];
+      const_cast<int*>(poff_s)[L] = d.pred_off[L];
     }
     const int* og = d.off + oidx(d, 0, bb);
     for (int j = threadIdx.x; j <= L; j += blockDim.x) offB[j] = og[j];
@@ -441,6 +464,11 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
         offB = sw;
         const int* nAp = V.nAb + prv * BL + bl;
         const int* depp = V.depb + prv * BL + bl;
+        if (kLean) {
+          na_s = nAp;
+          dep_s = depp;
+          win_s = V.win + bl;
+        }
         // all global loads of this thread's links first (one memory latency),
         // then the shared-memory updates
         constexpr int kPro = 8;
@@ -467,9 +495,11 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
             sz[u] = 0;
             if (j < j1) {
               const int nold = offA[j + 1] - offA[j];
-              na_s[j] = nold ? na_r[u] : 0;
-              dep_s[j] = dp_r[u];
-              win_s[j] = w_r[u];
+              if (!kLean) {
+                na_w[j] = nold ? na_r[u] : 0;
+                dep_w[j] = dp_r[u];
+                win_w[j] = w_r[u];
+              }
               sz[u] = nold - dp_r[u] + (w_r[u] >= 0 ? 1 : 0);
               sum += sz[u];
             }
@@ -517,9 +547,11 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
             const int j = j0 + u * blockDim.x;
             if (j < L) {
               const int nold = offA[j + 1] - offA[j];
-              na_s[j] = nold ? na_r[u] : 0;
-              dep_s[j] = dp_r[u];
-              win_s[j] = w_r[u];
+              if (!kLean) {
+                na_w[j] = nold ? na_r[u] : 0;
+                dep_w[j] = dp_r[u];
+                win_w[j] = w_r[u];
+              }
               offB[j] = nold - dp_r[u] + (w_r[u] >= 0 ? 1 : 0);
             }
           }
@@ -635,9 +667,9 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
             if (need_l || need_n) xl[q] = d.pos[so + k + (need_l ? -1 : 1)];
           } else {
             bool e0, e1 = false;
-            const int s0 = pull_f(j, r, offA, offB, na_s, dep_s, win_s, wonp, &e0);
+            const int s0 = pull_f<kLean>(j, r, offA, offB, na_s, dep_s, win_s, wonp, &e0);
             int s1 = s0;
-            if (need_l || need_n) s1 = pull_f(j, need_l ? r - 1 : r + 1, offA, offB, na_s, dep_s, win_s, wonp, &e1);
+            if (need_l || need_n) s1 = pull_f<kLean>(j, need_l ? r - 1 : r + 1, offA, offB, na_s, dep_s, win_s, wonp, &e1);
             const double v0 = x1p[s0], v1 = x1p[s1];
             aa[q] = d.aid[sp + s0];
             xx[q] = e0 ? 0.0 : v0;  // entrant: -M + M == 0.0 exactly
@@ -861,17 +893,30 @@ __global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
   }
 }
 
-int fused_smem_bytes(int L, bool stage_params) {
+static int fused_smem_full(int L, bool stage_params) {
   return (stage_params ? 3 * L * 8 : 0) + (2 * (L + 1) + 3 * L + 2 * (L + 1) + 36 + 3 * kHeadCap) * 4;
+}
+bool fused_lean(int L) { return fused_smem_full(L, false) > 200 * 1024; }
+int fused_smem_bytes(int L, bool stage_params) {
+  if (fused_lean(L)) return (2 * (L + 1) + 36 + 3 * kHeadCap) * 4;
+  return fused_smem_full(L, stage_params);
 }
 
 namespace {
 template <int KB, bool F>
 const void* fused_fn(bool cluster) {
-  return cluster ? reinterpret_cast<const void*>(k_forward_fused<true, KB, F>)
-                 : reinterpret_cast<const void*>(k_forward_fused<false, KB, F>);
+  return cluster ? reinterpret_cast<const void*>(k_forward_fused<true, KB, F, false>)
+                 : reinterpret_cast<const void*>(k_forward_fused<false, KB, F, false>);
 }
-const void* fused_pick(bool cluster, bool one, bool feat) {
+template <int KB, bool F>
+const void* fused_fn_lean() {  // large networks: grid schedule only
+  return reinterpret_cast<const void*>(k_forward_fused<false, KB, F, true>);
+}
+const void* fused_pick(bool cluster, bool one, bool feat, bool lean) {
+  if (lean) {
+    if (one) return feat ? fused_fn_lean<1, true>() : fused_fn_lean<1, false>();
+    return feat ? fused_fn_lean<2, true>() : fused_fn_lean<2, false>();
+  }
   if (one) return feat ? fused_fn<1, true>(cluster) : fused_fn<1, false>(cluster);
   return feat ? fused_fn<2, true>(cluster) : fused_fn<2, false>(cluster);
 }
@@ -882,7 +927,8 @@ cudaError_t launch_forward_fused(const CView& V, bool cluster, cudaStream_t st) 
   // one slot per thread -> kBatch 1
   const bool one = V.d.N <= V.cs * kClusterThreads;
   const bool feat = V.progress != nullptr || V.spec != nullptr;
-  const void* fn = fused_pick(cluster, one, feat);
+  if (V.lean && cluster) return cudaErrorInvalidConfiguration;  // lean layout: grid schedule only
+  const void* fn = fused_pick(cluster, one, feat, V.lean != 0);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   void* args[] = {const_cast<CView*>(&V)};
@@ -913,15 +959,18 @@ int fused_max_grid(int L, bool stage_params) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int smem = fused_smem_bytes(L, stage_params);
-  for (const void* fn : {fused_fn<2, false>(false), fused_fn<1, false>(false), fused_fn<2, true>(false),
-                         fused_fn<1, true>(false)})
+  const bool lean = fused_lean(L);
+  const void* fns[4] = {lean ? fused_fn_lean<2, false>() : fused_fn<2, false>(false),
+                        lean ? fused_fn_lean<1, false>() : fused_fn<1, false>(false),
+                        lean ? fused_fn_lean<2, true>() : fused_fn<2, true>(false),
+                        lean ? fused_fn_lean<1, true>() : fused_fn<1, true>(false)};
+  for (const void* fn : fns)
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
       cudaGetLastError();
       return 0;
     }
   int best = INT_MAX;
-  for (const void* fn : {fused_fn<2, false>(false), fused_fn<1, false>(false), fused_fn<2, true>(false),
-                         fused_fn<1, true>(false)}) {
+  for (const void* fn : fns) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kClusterThreads, smem);
     best = std::min(best, occ);
   }
@@ -930,6 +979,7 @@ int fused_max_grid(int L, bool stage_params) {
 }
 
 int fused_max_cluster(int L, bool stage_params) {
+  if (fused_lean(L)) return 0;  // the lean layout runs the grid schedule only
   const int smem = fused_smem_bytes(L, stage_params);
   for (const void* fn : {fused_fn<2, false>(true), fused_fn<1, false>(true), fused_fn<2, true>(true),
                          fused_fn<1, true>(true)}) {

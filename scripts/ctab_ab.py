@@ -5,8 +5,8 @@ import numpy as np
 import paper_2603_25068_b200 as P
 
 
-def case(name, dn, T, B, ckpt=False):
-    sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, dn, T, 300)
+def case(name, dn, T, B, ckpt=False, n=23, ln=1609.34, veh=1000020):
+    sc = P.Scenario.grid(n, ln, 42, 1000.0).configure(veh, dn, T, 300)
     p = sc.sample_parameters(3)
     lk, ps = sc.seed_agents()
     e = P.Engine(sc, B, T)
@@ -31,4 +31,5 @@ def case(name, dn, T, B, ckpt=False):
 case("C3 dn30 B=1", 30, 120, 1)
 case("C4 fwd ckpt B=8", 30, 60, 8, ckpt=True)
 case("C3 dn30 B=64", 30, 120, 64)
-case("C2-like dn1 B=1", 1, 300, 1)
+case("C3 dn1 B=1", 1, 300, 1)
+case("C2 50x50 dn1 B=1", 1, 300, 1, n=50, ln=400.0, veh=100000)
