@@ -139,6 +139,7 @@ struct dtg_ctx {
   DevBuf<double> srec;
   DevBuf<dtg::Spec> spec;  // speculative head decisions [2][B][L][2]
   bool speculate = true;
+  int cs_override = 0;  // flag 7: CTAs per scenario of the grid schedule (0 auto)
   bool spec_split = true;  // flag 5
   DevBuf<unsigned int> gbar, bgbar;
   bool custom_barrier = true;
@@ -583,6 +584,9 @@ int dtg_set_flag(dtg_ctx* c, int flag, int value) {
     case 5:  // ... drawn by warps 2.. during barrier 1 (1 default) or by idle link-phase lanes (0)
       c->spec_split = value != 0;
       return DTG_OK;
+    case 7:  // grid schedule: CTAs per scenario (0 auto: one slot per thread, capped by the grid)
+      c->cs_override = value < 0 ? 0 : value;
+      return DTG_OK;
     default:
       return fail(c, DTG_ERR_CONFIG, "unknown flag");
   }
@@ -858,7 +862,8 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
         V.cs = cs;
       } else {
         // CTAs per scenario: one slot per thread, capped by the resident grid
-        const int want = (std::max(c->N, c->L) + dtg::kClusterThreads - 1) / dtg::kClusterThreads;
+        int want = (std::max(c->N, c->L) + dtg::kClusterThreads - 1) / dtg::kClusterThreads;
+        if (c->cs_override > 0) want = c->cs_override;  // tuning experiments (flag 7)
         V.cs = std::max(1, std::min(want, c->pgrid_max / c->B));
       }
       // interleaved 512-slot blocks by default (measured faster at C3 dn30
