@@ -79,10 +79,10 @@ const char* dtg_last_error(const dtg_ctx* ctx);
 /* Run on this cudaStream_t (default: a stream owned by the context). */
 int dtg_set_stream(dtg_ctx* ctx, void* cuda_stream);
 /* Forward as one persistent cooperative kernel for all steps (default on);
- * off = one CUDA graph of 4 kernels per step (same results). */
+ * off = one CUDA graph of 5 kernels per step (same results). */
 int dtg_set_persistent(dtg_ctx* ctx, int enabled);
 /* Forward schedule: 0 auto (default), 1 one thread-block cluster per
- * scenario, 2 one persistent cooperative grid, 3 CUDA graph of 4 kernels per
+ * scenario, 2 one persistent cooperative grid, 3 CUDA graph of 5 kernels per
  * step.  All produce identical results.  dtg_last_mode returns
  * 100 * mode + cluster size of the last forward. */
 int dtg_set_mode(dtg_ctx* ctx, int mode);

@@ -4,7 +4,9 @@
 //   k_step_cf       one thread per agent slot: Newell car-following with the
 //                   leader in the previous slot, per-link midpoint count and
 //                   arrived-prefix length as segment-boundary writes, vacancy
-//                   tail, and the Gumbel-softmax link choice of arrived agents.
+//                   tail.
+//   k_step_choice   one thread per link: the Gumbel-softmax link choice of its
+//                   arrived agents.
 //   k_step_merge    one thread per link: count/cumulative update, vacancy,
 //                   merge-choice over the arrived heads of the predecessor links.
 //   k_step_scan     one CTA per scenario: departures, new segment sizes and the
@@ -13,7 +15,7 @@
 //                   (winners enter their new link at position 0.0, everyone
 //                   else keeps x1 and its order).
 // Reverse step (the per-step segment VJP of engine.cpp:388-415) replays the
-// first three kernels from the step's checkpoint, then:
+// first four kernels from the step's checkpoint, then:
 //   k_adj_node    per link: count adjoint and the merge-row VJP (transfer VJP
 //                 seeds, softmax VJP, targeted routing to the first candidate).
 //   k_adj_a0      per scenario: rows the reference routes to the first arrived
@@ -74,11 +76,32 @@ __global__ void __launch_bounds__(256) k_step_cf(DevView d, int t, int s_cur) {
   if (fa) {
     d.won[bn + k] = 0;
     if (d.alist) d.alist[bn + atomicAdd(&d.acount[b], 1)] = k;  // reverse sweep only
+  }
+}
+
+// Link choice of the arrived heads (node_model.cpp:45-97), one thread per
+// link over its nA arrived agents.  Kept out of k_step_cf: the draw's
+// registers and local arrays halved that kernel's occupancy while only ~8% of
+// its threads ever draw.
+__global__ void __launch_bounds__(128) k_step_choice(DevView d, int t, int s_cur) {
+  const int b = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.L) return;
+  const int* off = d.off + oidx(d, s_cur, b);
+  const int base = off[j];
+  if (off[j + 1] == base) return;  // empty segment: nA[j] is stale
+  const std::size_t pl = static_cast<std::size_t>(b) * d.L + j;
+  const int na = d.nA[pl];
+  if (na == 0) return;
+  const std::size_t so = sidx(d, s_cur, b);
+  const std::size_t bn = static_cast<std::size_t>(b) * d.N;
+  const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
+  const double* lz = d.slogz + pl * d.maxdeg;
+  for (int r = 0; r < na; ++r) {
+    const int k = base + r;
     int c = -1;
-    const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
-    if (deg > 0) {  // link_choice (node_model.cpp:45-97)
+    if (deg > 0) {
       const int agent = d.aid[so + k];
-      const double* lz = d.slogz + (static_cast<std::size_t>(b) * d.L + j) * d.maxdeg;
       if (deg <= kFastSucc) {  // registers, straight-line logs, argmax from the logits
         const std::uint64_t h2 = rng_prefix2(rng_prefix1(d.seed_link[b], static_cast<std::uint64_t>(t)),
                                              static_cast<std::uint64_t>(agent));
@@ -825,10 +848,10 @@ __global__ void k_derive(DevView d, double* jam, double* dxf, double* pref) {
 // ---------------------------------------------------------------------------------
 static inline dim3 grid_n(int n, int bs, int B) { return dim3((n + bs - 1) / bs, B); }
 
-const char* const kFwdKernelNames[kFwdKernels] = {"k_step_cf", "k_step_merge",
+const char* const kFwdKernelNames[kFwdKernels] = {"k_step_cf", "k_step_choice", "k_step_merge",
                                                  "k_step_scan", "k_step_transfer"};
 const char* const kBwdKernelNames[kBwdKernels] = {
-    "k_step_cf(replay)", "k_step_merge(replay)", "k_step_scan(replay)", "k_adj_node",
+    "k_step_cf(replay)", "k_step_choice(replay)", "k_step_merge(replay)", "k_step_scan(replay)", "k_adj_node",
     "k_adj_a0",          "k_adj_choice",         "k_adj_slot",          "k_adj_link"};
 
 void launch_fwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next,
@@ -838,9 +861,12 @@ void launch_fwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
       k_step_cf<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, t, s_cur);
       break;
     case 1:
-      k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 0);
+      k_step_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);
       break;
     case 2:
+      k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 0);
+      break;
+    case 3:
       k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 0);
       break;
     default:
@@ -863,22 +889,25 @@ void launch_bwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
       k_step_cf<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, t, s_cur);
       break;
     case 1:
-      k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 1);
+      k_step_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);
       break;
     case 2:
-      k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 1);
+      k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 1);
       break;
     case 3:
+      k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 1);
+      break;
+    case 4:
       k_adj_node<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, s_next, xbar_next,
                                                           snap_seed, snap_k, K);
       break;
-    case 4:
+    case 5:
       k_adj_a0<<<d.B, kA0Threads, 0, st>>>(d, t, s_cur, s_next, xbar_next, sort_scratch, force_slow);
       break;
-    case 5:
+    case 6:
       k_adj_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);
       break;
-    case 6:
+    case 7:
       k_adj_slot<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s_cur, s_next, xbar_next, xbar_cur);
       break;
     default:

@@ -24,8 +24,8 @@ void launch_gumbel_batch(std::uint64_t seed, std::uint64_t key, const std::uint6
                          const std::uint64_t* cols, int n, double* out, cudaStream_t st);
 
 
-constexpr int kFwdKernels = 4;
-constexpr int kBwdKernels = 8;
+constexpr int kFwdKernels = 5;
+constexpr int kBwdKernels = 9;
 constexpr int kLaunchesPerForwardStep = kFwdKernels;
 constexpr int kLaunchesPerBackwardStep = kBwdKernels;
 extern const char* const kFwdKernelNames[kFwdKernels];

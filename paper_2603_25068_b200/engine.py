@@ -502,7 +502,9 @@ class Engine:
     def profile_kernels(self, T: int, steps_per_interval: int, backward: bool = False):
         """Per-kernel-kind device time (ms, CUDA events) of one forward (or the
         reverse sweep of the preceding checkpointed forward)."""
-        nk = 8 if backward else 4
+        nk = 0
+        while self._lib.dtg_kernel_name(int(backward), nk):
+            nk += 1
         ms = np.zeros(nk)
         n = C.c_int64()
         self._check(self._lib.dtg_profile_kernels(self._h, T, steps_per_interval, int(backward), ms, C.byref(n)))

@@ -1,5 +1,5 @@
 """The cluster-per-scenario kernel, the persistent cooperative grid kernel and
-the 4-kernel step graph are three schedules of the same arithmetic: results must be bit-identical, in all
+the 5-kernel step graph are three schedules of the same arithmetic: results must be bit-identical, in all
 three grid-assignment modes (several CTAs per scenario, capped CTAs per
 scenario, several scenarios per CTA)."""
 import numpy as np
@@ -43,7 +43,7 @@ def test_persistent_equals_step_graph(n, length, veh, dn, T, B):
     sc = P.Scenario.grid(n, length, 42, 1000.0).configure(veh, dn, T, 300 if dn <= 2 else 30 * dn * 10)
     p = sc.sample_parameters(3)
     spi = sc.steps_per_interval
-    ref = run(sc, p, B, 3, T, spi)  # 4-kernel step graph
+    ref = run(sc, p, B, 3, T, spi)  # 5-kernel step graph
     for mode in (1, 2):           # cluster per scenario, persistent grid
         a = run(sc, p, B, mode, T, spi)
         assert np.array_equal(a[0], ref[0]), mode
@@ -88,7 +88,7 @@ def test_dn1_full_hour_invariants_and_schedules():
     """C3 at dn=1 (1,000,020 agents) for the full hour (3,600 steps) — sizes the
     oracle cannot run: cumulative counts never decrease, every agent ends on a
     valid link inside it, reruns are bit-identical, and the fused grid kernel
-    equals the 4-kernel step graph over the first 300 steps."""
+    equals the 5-kernel step graph over the first 300 steps."""
     sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 1, 3600, 300)
     p = sc.sample_parameters(3)
     a = P.simulate_forward(sc, p, seed=7)
