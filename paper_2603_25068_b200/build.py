@@ -25,7 +25,8 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr",
-              "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v"] + ARCH
+              "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v"] + ARCH + \
+    os.environ.get("DTG_NVCC_EXTRA", "").split()  # tuning experiments only (scripts/)
 CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
              f"-I{CUDA_HOME}/include"]
 

@@ -804,10 +804,11 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
     if (mode == 0) mode = c->persistent ? 2 : 3;
     if (mode == 1 && !cluster_ok) mode = 2;
     if (mode == 2 && (c->pgrid_max <= 0 || c->B > c->pgrid_max)) mode = 3;
-    // auto: with fewer than 3 CTAs per scenario the fused kernel loses to the
-    // step graph (C3 ms/nowcast fused vs graph: B=40 (3 CTAs) 6.53 vs 5.94,
-    // B=48 (3) 6.58 vs 6.69, B=64 (2) 9.91 vs 8.61; scripts/graph_time.py)
-    if (c->mode == 0 && mode == 2 && c->N > dtg::kClusterThreads && 3 * c->B > c->pgrid_max) mode = 3;
+    // auto: with fewer than 4 CTAs per scenario the fused kernel loses to the
+    // step graph (C3 ms/nowcast fused vs graph: B=32 (4 CTAs) 5.32 vs 5.30,
+    // B=40 (3) 6.53 vs 5.94, B=48 (3) 6.68 vs 6.39, B=64 (2) 9.91 vs 8.07;
+    // scripts/graph_time.py)
+    if (c->mode == 0 && mode == 2 && c->N > dtg::kClusterThreads && 4 * c->B > c->pgrid_max) mode = 3;
     if (!c->persistent && c->mode == 0) mode = 3;
     c->last_mode = mode;
     if ((mode == 1 || mode == 2) && T > 0) {

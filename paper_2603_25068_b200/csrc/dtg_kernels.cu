@@ -39,43 +39,80 @@ constexpr int kFastSucc = 5;  // successor / candidate counts up to this use reg
 // ---------------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_step_cf(DevView d, int t, int s_cur) {
+// kCfPer slots per thread, strided by the block size, all loads of a round
+// issued before use (as in k_step_transfer: the lnk -> link-constant chain is
+// latency-, not bandwidth-bound with one slot per thread).  Measured (C3
+// B=256, ms per nowcast): 1 slot 9.2, 2 slots at <= 64 registers 8.0, 4 slots
+// 9.5 (110 registers).
+#ifndef DTG_CF_PER
+#define DTG_CF_PER 2
+#endif
+#ifndef DTG_CF_MINB
+#define DTG_CF_MINB 4
+#endif
+constexpr int kCfPer = DTG_CF_PER;
+constexpr int kCfThreads = 256;
+
+__global__ void __launch_bounds__(kCfThreads, DTG_CF_MINB) k_step_cf(DevView d, int t, int s_cur) {
+  (void)t;
   const int b = blockIdx.y;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= d.N) return;
+  const int k0 = blockIdx.x * (kCfThreads * kCfPer) + threadIdx.x;
   const std::size_t so = sidx(d, s_cur, b);
   const double* pos = d.pos + so;
   const int* off = d.off + oidx(d, s_cur, b);
-  const int j = d.lnk[so + k];
-  const int base = off[j], n = off[j + 1] - base, r = k - base;
-  const std::size_t pl = static_cast<std::size_t>(b) * d.L + j;
-  const double jam = d.jam[pl], dxf = d.dxf[pl], len = d.len[j];
-  const double ctr = d.ctr[j], thr = d.thr[j];
-  const double x = pos[k];
-  // headway: leader gets M (car_following.cpp:547-553)
-  const CfPick me = cf_step(x, r == 0 ? d.M : pos[k - 1] - x, jam, dxf, len);
   const std::size_t bn = static_cast<std::size_t>(b) * d.N;
-  d.x1[bn + k] = me.x1;
-  bool fo_n = false, fa_n = false;
-  if (r + 1 < n) {
-    const double xn = pos[k + 1];
-    const CfPick nx = cf_step(xn, x - xn, jam, dxf, len);
-    fo_n = nx.x1 >= ctr;
-    fa_n = nx.x1 >= thr;
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  int j[kCfPer];
+  double xm[kCfPer], x[kCfPer], xp[kCfPer];
+#pragma unroll
+  for (int i = 0; i < kCfPer; ++i) {
+    const int k = k0 + i * kCfThreads;
+    const int kk = k < d.N ? k : d.N - 1;
+    j[i] = d.lnk[so + kk];
+    x[i] = pos[kk];
+    xm[i] = pos[kk > 0 ? kk - 1 : 0];
+    xp[i] = pos[kk + 1 < d.N ? kk + 1 : kk];
   }
-  const bool fo = me.x1 >= ctr, fa = me.x1 >= thr;
-  // x1 stays ordered inside the segment, so {x1 >= o} and {x1 >= L-0.01} are
-  // prefixes: their lengths are written by the unique boundary slot.
-  int* qn = d.qn + static_cast<std::size_t>(b) * d.L;
-  int* nA = d.nA + static_cast<std::size_t>(b) * d.L;
-  if (r == 0 && !fo) qn[j] = 0;
-  if (fo && !fo_n) qn[j] = r + 1;
-  if (r == 0 && !fa) nA[j] = 0;
-  if (fa && !fa_n) nA[j] = r + 1;
-  if (r == n - 1) d.tail[pl] = me.x1;  // min x1 = vacancy (node_model.cpp:27-41)
-  if (fa) {
-    d.won[bn + k] = 0;
-    if (d.alist) d.alist[bn + atomicAdd(&d.acount[b], 1)] = k;  // reverse sweep only
+  int base[kCfPer], n[kCfPer];
+  double jam[kCfPer], dxf[kCfPer], len[kCfPer], ctr[kCfPer], thr[kCfPer];
+#pragma unroll
+  for (int i = 0; i < kCfPer; ++i) {
+    base[i] = off[j[i]];
+    n[i] = off[j[i] + 1] - base[i];
+    jam[i] = d.jam[bl + j[i]];
+    dxf[i] = d.dxf[bl + j[i]];
+    len[i] = d.len[j[i]];
+    ctr[i] = d.ctr[j[i]];
+    thr[i] = d.thr[j[i]];
+  }
+  int* qn = d.qn + bl;
+  int* nA = d.nA + bl;
+#pragma unroll
+  for (int i = 0; i < kCfPer; ++i) {
+    const int k = k0 + i * kCfThreads;
+    if (k >= d.N) break;
+    const int r = k - base[i];
+    // headway: leader gets M (car_following.cpp:547-553)
+    const CfPick me = cf_step(x[i], r == 0 ? d.M : xm[i] - x[i], jam[i], dxf[i], len[i]);
+    d.x1[bn + k] = me.x1;
+    bool fo_n = false, fa_n = false;
+    if (r + 1 < n[i]) {
+      const CfPick nx = cf_step(xp[i], x[i] - xp[i], jam[i], dxf[i], len[i]);
+      fo_n = nx.x1 >= ctr[i];
+      fa_n = nx.x1 >= thr[i];
+    }
+    const bool fo = me.x1 >= ctr[i], fa = me.x1 >= thr[i];
+    // x1 stays ordered inside the segment, so {x1 >= o} and {x1 >= L-0.01} are
+    // prefixes: their lengths are written by the unique boundary slot.
+    if (r == 0 && !fo) qn[j[i]] = 0;
+    if (fo && !fo_n) qn[j[i]] = r + 1;
+    if (r == 0 && !fa) nA[j[i]] = 0;
+    if (fa && !fa_n) nA[j[i]] = r + 1;
+    if (r == n[i] - 1) d.tail[bl + j[i]] = me.x1;  // min x1 = vacancy (node_model.cpp:27-41)
+    if (fa) {
+      d.won[bn + k] = 0;
+      if (d.alist) d.alist[bn + atomicAdd(&d.acount[b], 1)] = k;  // reverse sweep only
+    }
   }
 }
 
@@ -376,25 +413,61 @@ __device__ __forceinline__ int next_slot(const DevView& d, std::size_t bn,
   return offn[j] + r - dd;
 }
 
-__global__ void __launch_bounds__(256) k_step_transfer(DevView d, int s_cur,
-                                                        int s_next) {
+// kTransferPer slots per thread, strided by the block size (coalesced), with
+// every slot's loads issued before any is used: the dependent chain
+// lnk -> (off, nA, dep, offn) -> store is ~3 memory latencies deep, so one slot
+// per thread left the kernel latency-bound at ~2.5 TB/s (B=256).  Measured
+// (C3 B=256, ms per nowcast): 1 slot 9.3, 2 slots 7.6, 4 slots 9.0.
+#ifndef DTG_TR_PER
+#define DTG_TR_PER 2
+#endif
+constexpr int kTransferPer = DTG_TR_PER;
+constexpr int kTransferThreads = 256;
+
+__global__ void __launch_bounds__(kTransferThreads) k_step_transfer(DevView d, int s_cur,
+                                                                     int s_next) {
   const int b = blockIdx.y;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= d.N) return;
+  const int k0 = blockIdx.x * (kTransferThreads * kTransferPer) + threadIdx.x;
   const std::size_t so = sidx(d, s_cur, b), sn = sidx(d, s_next, b);
   const std::size_t bl = static_cast<std::size_t>(b) * d.L;
   const std::size_t bn = static_cast<std::size_t>(b) * d.N;
   const int* off = d.off + oidx(d, s_cur, b);
   const int* offn = d.off + oidx(d, s_next, b);
-  const int j = d.lnk[so + k];
-  const int base = off[j], r = k - base;
-  const int na = d.nA[bl + j];
-  bool mover;
-  const int ns = next_slot(d, bn, bl, offn, k, j, base, r, na, &mover);
-  // transfer (node_model.cpp:122-149): -M + M == 0.0 exactly on the new link
-  d.pos[sn + ns] = mover ? 0.0 : d.x1[bn + k];
-  d.aid[sn + ns] = d.aid[so + k];
-  d.lnk[sn + ns] = mover ? d.choice[bn + k] : j;
+  int j[kTransferPer], id[kTransferPer], base[kTransferPer], na[kTransferPer], sh[kTransferPer];
+  double x[kTransferPer];
+#pragma unroll
+  for (int i = 0; i < kTransferPer; ++i) {
+    const int k = k0 + i * kTransferThreads;
+    const int kk = k < d.N ? k : d.N - 1;
+    j[i] = d.lnk[so + kk];
+    x[i] = d.x1[bn + kk];
+    id[i] = d.aid[so + kk];
+  }
+#pragma unroll
+  for (int i = 0; i < kTransferPer; ++i) {
+    base[i] = off[j[i]];
+    na[i] = d.nA[bl + j[i]];
+    sh[i] = offn[j[i]] - d.dep[bl + j[i]];  // non-arrived slots: ns = offn + r - dep
+  }
+#pragma unroll
+  for (int i = 0; i < kTransferPer; ++i) {
+    const int k = k0 + i * kTransferThreads;
+    if (k >= d.N) break;
+    const int r = k - base[i];
+    int ns = sh[i] + r, lk = j[i];
+    double xo = x[i];
+    if (r < na[i]) {  // arrived: winner moves, the others shift past earlier winners
+      bool mover;
+      ns = next_slot(d, bn, bl, offn, k, j[i], base[i], r, na[i], &mover);
+      if (mover) {
+        xo = 0.0;  // transfer (node_model.cpp:122-149): -M + M == 0.0 exactly on the new link
+        lk = d.choice[bn + k];
+      }
+    }
+    d.pos[sn + ns] = xo;
+    d.aid[sn + ns] = id[i];
+    d.lnk[sn + ns] = lk;
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -858,7 +931,7 @@ void launch_fwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
                        cudaStream_t st) {
   switch (which) {
     case 0:
-      k_step_cf<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, t, s_cur);
+      k_step_cf<<<grid_n(d.N, kCfThreads * kCfPer, d.B), kCfThreads, 0, st>>>(d, t, s_cur);
       break;
     case 1:
       k_step_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);
@@ -870,7 +943,8 @@ void launch_fwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
       k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 0);
       break;
     default:
-      k_step_transfer<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, s_cur, s_next);
+      k_step_transfer<<<grid_n(d.N, kTransferThreads * kTransferPer, d.B), kTransferThreads, 0, st>>>(
+          d, s_cur, s_next);
   }
 }
 
@@ -886,7 +960,7 @@ void launch_bwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
                        cudaStream_t st) {
   switch (which) {
     case 0:
-      k_step_cf<<<grid_n(d.N, 256, d.B), 256, 0, st>>>(d, t, s_cur);
+      k_step_cf<<<grid_n(d.N, kCfThreads * kCfPer, d.B), kCfThreads, 0, st>>>(d, t, s_cur);
       break;
     case 1:
       k_step_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);

@@ -4,7 +4,7 @@ graph_time.py B [B ...]."""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("DTG_VARIANT_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 import paper_2603_25068_b200 as P
