@@ -434,8 +434,7 @@ def run_throughput(P, torch, sc, p, lk0, ps0, args):
         s = timed(eng, T_STEPS, SPI)
         alg = B * T_STEPS * (16 * N + 64 * L)
         out[f"c3_dn30_B{B}_mode{mode}"] = {
-            "scenarios": B, "schedule": {2: "fused persistent grid", 3: "5-kernel step graph"}.get(
-                eng.last_mode // 100, str(eng.last_mode)),
+            "scenarios": B, **eng.last_schedule,
             "ms_per_batch": s * 1e3, "rtf_aggregate": B * SIM_SECONDS / s,
             "alg_GBps": alg / s / 1e9, "hbm_frac": alg / s / 1e9 / peak}
         del eng
@@ -453,7 +452,7 @@ def run_throughput(P, torch, sc, p, lk0, ps0, args):
     alg = 3600 * (16 * N1 + 64 * L)
     out["c3_dn1_B1"] = {"agents": N1, "steps": 3600, "ms_per_nowcast": s * 1e3, "rtf": SIM_SECONDS / s,
                         "us_per_step": s / 3600 * 1e6, "alg_GBps": alg / s / 1e9, "hbm_frac": alg / s / 1e9 / peak,
-                        "schedule": eng.last_mode,
+                        **eng.last_schedule,
                         "note": "16 MB/step of algorithmic traffic against a ~50 MB working set that stays "
                                 "L2-resident; latency/issue-bound (profiles/r01/ncu_fused_dn1_summary.md)"}
     del eng
@@ -471,7 +470,7 @@ def run_throughput(P, torch, sc, p, lk0, ps0, args):
     alg = 3600 * (16 * N2 + 64 * L2)
     out["c2_dn1_B1"] = {"agents": N2, "links": L2, "steps": 3600, "ms_per_nowcast": s * 1e3,
                         "rtf": SIM_SECONDS / s, "us_per_step": s / 3600 * 1e6, "alg_GBps": alg / s / 1e9,
-                        "hbm_frac": alg / s / 1e9 / peak, "schedule": eng.last_mode}
+                        "hbm_frac": alg / s / 1e9 / peak, **eng.last_schedule}
     del eng
     return out
 

@@ -84,7 +84,7 @@ int dtg_set_persistent(dtg_ctx* ctx, int enabled);
 /* Forward schedule: 0 auto (default), 1 one thread-block cluster per
  * scenario, 2 one persistent cooperative grid, 3 CUDA graph of 5 kernels per
  * step.  All produce identical results.  dtg_last_mode returns
- * 100 * mode + cluster size of the last forward. */
+ * 1000 * mode + CTAs per scenario of the last forward (0 for the graph). */
 int dtg_set_mode(dtg_ctx* ctx, int mode);
 /* Measurement hook: one persistent reverse sweep (zero seeds) with
  * %globaltimer stamps; phase_us[8] = mean per-step span (us) of R1, barrier,

@@ -598,7 +598,7 @@ int dtg_set_mode(dtg_ctx* c, int mode) {
   return DTG_OK;
 }
 
-int dtg_last_mode(const dtg_ctx* c) { return c->last_mode * 100 + c->last_cs; }
+int dtg_last_mode(const dtg_ctx* c) { return c->last_mode * 1000 + (c->last_mode == 3 ? 0 : c->last_cs); }
 
 static void run_backward(dtg_ctx* c, const double* snap, const double* cum, const double* xs,
                          cudaMemcpyKind kind, bool seeds_ready = false);

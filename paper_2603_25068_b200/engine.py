@@ -409,7 +409,15 @@ class Engine:
 
     @property
     def last_mode(self) -> int:
+        """1000 * schedule (1 cluster, 2 persistent grid, 3 step graph) + CTAs
+        per scenario of the last forward."""
         return int(self._lib.dtg_last_mode(self._h))
+
+    @property
+    def last_schedule(self) -> dict:
+        m = self.last_mode
+        names = {1: "cluster per scenario", 2: "fused persistent grid", 3: "5-kernel step graph"}
+        return {"schedule": names.get(m // 1000, str(m)), "ctas_per_scenario": m % 1000 or None}
 
     def set_persistent(self, on: bool):
         self._check(self._lib.dtg_set_persistent(self._h, int(on)))
