@@ -281,7 +281,8 @@ struct dtg_ctx {
   void check_flags(const int* e) const {
     for (int b = 0; b < B; ++b) {
       if (e[b] & dtg::kErrCandOverflow)
-        throw Unsupported("more than 32 merge candidates for one link in one step (scenario " +
+        throw Unsupported("more merge candidates for one link in one step than the schedule holds (16 in the "
+                          "persistent kernels, 32 in the step graph; scenario " +
                           std::to_string(b) + ")");
       if (e[b] & dtg::kErrZeroAlpha)
         throw Unsupported("zero merge priority (alpha) on a candidate link is not supported");
