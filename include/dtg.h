@@ -99,7 +99,8 @@ int dtg_last_mode(const dtg_ctx* ctx);
  * flag 4 = fused forward draws the next step's head decisions ahead of time
  * (1, default) or in the slot phase (0); flag 5 = those draws run in warps
  * 2.. of each CTA during barrier 1 (1, default) or in idle link-phase lanes
- * (0); flag 7 = CTAs per scenario of the grid schedule (0 = auto).  Results
+ * (0); flag 7 = CTAs per scenario of the grid schedule (0 = auto); flag 8 =
+ * scenario branches of the step graph (0 = auto: 2 from B = 8, 4 from 32).  Results
  * are identical. */
 int dtg_set_flag(dtg_ctx* ctx, int flag, int value);
 /* Measurement hook: one persistent forward with %globaltimer stamps; returns

@@ -140,6 +140,10 @@ struct dtg_ctx {
   DevBuf<dtg::Spec> spec;  // speculative head decisions [2][B][L][2]
   bool speculate = true;
   int cs_override = 0;  // flag 7: CTAs per scenario of the grid schedule (0 auto)
+  int graph_split = 0;  // flag 8: scenario branches of the step graph (0 auto)
+  std::vector<cudaStream_t> side;  // step-graph branch streams
+  cudaEvent_t fork_ev = nullptr;
+  std::vector<cudaEvent_t> join_ev;
   bool spec_split = true;  // flag 5
   DevBuf<unsigned int> gbar, bgbar;
   bool custom_barrier = true;
@@ -244,7 +248,48 @@ struct dtg_ctx {
     if (h_seed_pin) cudaFreeHost(h_seed_pin);
     if (seed_ev) cudaEventDestroy(seed_ev);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (auto x : side) cudaStreamDestroy(x);
+    for (auto e : join_ev) cudaEventDestroy(e);
+    if (fork_ev) cudaEventDestroy(fork_ev);
     if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  // Step-graph branches: independent scenario ranges run their T-step
+  // chains side by side, so one range's kernel tails (the serial draw chains
+  // of long queues in k_step_choice / k_step_merge) overlap the other's work.
+  int graph_branches() const {
+    if (graph_split > 0) return std::min(graph_split, B);
+    // measured (C3, ms per nowcast, 1 / 2 / 4 branches): B=32 -- / 5.12 / 5.05,
+    // B=64 8.12 / 7.63 / 7.41, B=128 14.73 / 13.30 / 13.04, B=256 27.30 /
+    // 26.16 / 26.04 (8 branches 27.46)
+    return B >= 32 ? 4 : (B >= 8 ? 2 : 1);
+  }
+  template <class F>
+  void fork_branches(int nsp, cudaStream_t st, F&& run) {
+    if (nsp <= 1) {
+      run(0, B, st);
+      return;
+    }
+    while (static_cast<int>(side.size()) < nsp - 1) {
+      cudaStream_t x;
+      cudaEvent_t e;
+      CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      side.push_back(x);
+      join_ev.push_back(e);
+    }
+    if (!fork_ev) CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(fork_ev, st));
+    for (int q = 1; q < nsp; ++q) CK(cudaStreamWaitEvent(side[q - 1], fork_ev, 0));
+    for (int q = 0; q < nsp; ++q) {
+      const int b0 = static_cast<int>(static_cast<long long>(q) * B / nsp);
+      const int b1 = static_cast<int>(static_cast<long long>(q + 1) * B / nsp);
+      run(b0, b1 - b0, q ? side[q - 1] : st);
+    }
+    for (int q = 1; q < nsp; ++q) {
+      CK(cudaEventRecord(join_ev[q - 1], side[q - 1]));
+      CK(cudaStreamWaitEvent(st, join_ev[q - 1], 0));
+    }
   }
 
   void ensure_history(int T, int ckpt) {
@@ -588,6 +633,9 @@ int dtg_set_flag(dtg_ctx* c, int flag, int value) {
     case 7:  // grid schedule: CTAs per scenario (0 auto: one slot per thread, capped by the grid)
       c->cs_override = value < 0 ? 0 : value;
       return DTG_OK;
+    case 8:  // step graph: scenario branches (0 auto)
+      c->graph_split = value < 0 ? 0 : value;
+      return DTG_OK;
     default:
       return fail(c, DTG_ERR_CONFIG, "unknown flag");
   }
@@ -781,6 +829,7 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
     const dtg::DevView d = c->view();
     const std::size_t BN = static_cast<std::size_t>(c->B) * c->N;
     const std::size_t BL = static_cast<std::size_t>(c->B) * c->L;
+    const int nsp = c->graph_branches();
     auto body = [&] {
       dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
       dtg::launch_pack_succ(d, c->srec.p, st);
@@ -792,8 +841,12 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       CK(cudaMemcpyAsync(c->qh.p, c->q0.p, BL * 8, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemsetAsync(c->cumh.p, 0, BL * 8, st));
       CK(cudaMemsetAsync(c->errf.p, 0, sizeof(int) * c->B, st));
-      for (int t = 0; t < T; ++t)
-        dtg::launch_step_forward(d, t, t % c->S, (t + 1) % c->S, st);
+      c->fork_branches(nsp, st, [&](int b0, int nb, cudaStream_t sq) {
+        dtg::DevView dq = d;
+        dq.b0 = b0;
+        dq.nb = nb;
+        for (int t = 0; t < T; ++t) dtg::launch_step_forward(dq, t, t % c->S, (t + 1) % c->S, sq);
+      });
     };
     // cluster-per-scenario mode: <= 8 slots per thread inside one cluster
     int cs_need = (c->N + dtg::kClusterThreads * 8 - 1) / (dtg::kClusterThreads * 8);
@@ -805,11 +858,11 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
     if (mode == 0) mode = c->persistent ? 2 : 3;
     if (mode == 1 && !cluster_ok) mode = 2;
     if (mode == 2 && (c->pgrid_max <= 0 || c->B > c->pgrid_max)) mode = 3;
-    // auto: with fewer than 4 CTAs per scenario the fused kernel loses to the
-    // step graph (C3 ms/nowcast fused vs graph: B=32 (4 CTAs) 5.32 vs 5.30,
-    // B=40 (3) 6.53 vs 5.94, B=48 (3) 6.68 vs 6.39, B=64 (2) 9.91 vs 8.07;
-    // scripts/graph_time.py)
-    if (c->mode == 0 && mode == 2 && c->N > dtg::kClusterThreads && 4 * c->B > c->pgrid_max) mode = 3;
+    // auto: with fewer than 5 CTAs per scenario the fused kernel loses to the
+    // step graph (C3 ms/nowcast fused vs graph with 4 branches: B=24 (6 CTAs)
+    // 3.82 vs 4.68, B=32 (4) 5.33 vs 5.05, B=48 (3) 6.68 vs 6.10, B=64 (2)
+    // 9.91 vs 7.41; scripts/graph_time.py)
+    if (c->mode == 0 && mode == 2 && c->N > dtg::kClusterThreads && 5 * c->B > c->pgrid_max) mode = 3;
     if (!c->persistent && c->mode == 0) mode = 3;
     c->last_mode = mode;
     if ((mode == 1 || mode == 2) && T > 0) {
@@ -902,7 +955,7 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       c->pending = true;
       return;
     }
-    const long long key = (static_cast<long long>(T) << 20) ^ (c->S << 1) ^ 1;
+    const long long key = (static_cast<long long>(T) << 20) ^ (c->S << 1) ^ 1 ^ (static_cast<long long>(nsp) << 50);
     if (c->graphs && T > 0) {
       if (c->fwd_key != key || !c->fwd_exec) {
         if (c->fwd_exec) cudaGraphExecDestroy(c->fwd_exec);

@@ -55,7 +55,7 @@ constexpr int kCfThreads = 256;
 
 __global__ void __launch_bounds__(kCfThreads, DTG_CF_MINB) k_step_cf(DevView d, int t, int s_cur) {
   (void)t;
-  const int b = blockIdx.y;
+  const int b = d.b0 + blockIdx.y;
   const int k0 = blockIdx.x * (kCfThreads * kCfPer) + threadIdx.x;
   const std::size_t so = sidx(d, s_cur, b);
   const double* pos = d.pos + so;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kCfThreads, DTG_CF_MINB) k_step_cf(DevView d, 
 // registers and local arrays halved that kernel's occupancy while only ~8% of
 // its threads ever draw.
 __global__ void __launch_bounds__(128) k_step_choice(DevView d, int t, int s_cur) {
-  const int b = blockIdx.y;
+  const int b = d.b0 + blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d.L) return;
   const int* off = d.off + oidx(d, s_cur, b);
@@ -279,7 +279,7 @@ __device__ __forceinline__ int merge_softmax(const DevView& d, int b, int t, int
 
 __global__ void __launch_bounds__(128) k_step_merge(DevView d, int t, int s_cur,
                                                      int replay) {
-  const int b = blockIdx.y;
+  const int b = d.b0 + blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.L) return;
   const std::size_t so = sidx(d, s_cur, b);
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(1024) k_step_scan(DevView d, int s_cur,
                                                      int s_next, int replay) {
   __shared__ int sm[32];
   __shared__ unsigned long long smin[32];
-  const int b = blockIdx.x;
+  const int b = d.b0 + blockIdx.x;
   const std::size_t so = sidx(d, s_cur, b);
   const int* off = d.off + oidx(d, s_cur, b);
   int* offn = d.off + oidx(d, s_next, b);
@@ -426,7 +426,7 @@ constexpr int kTransferThreads = 256;
 
 __global__ void __launch_bounds__(kTransferThreads) k_step_transfer(DevView d, int s_cur,
                                                                      int s_next) {
-  const int b = blockIdx.y;
+  const int b = d.b0 + blockIdx.y;
   const int k0 = blockIdx.x * (kTransferThreads * kTransferPer) + threadIdx.x;
   const std::size_t so = sidx(d, s_cur, b), sn = sidx(d, s_next, b);
   const std::size_t bl = static_cast<std::size_t>(b) * d.L;
@@ -920,6 +920,8 @@ __global__ void k_derive(DevView d, double* jam, double* dxf, double* pref) {
 // launch wrappers
 // ---------------------------------------------------------------------------------
 static inline dim3 grid_n(int n, int bs, int B) { return dim3((n + bs - 1) / bs, B); }
+// scenarios of one forward launch: [b0, b0 + nb) (nb 0: all B)
+static inline int nbl(const DevView& d) { return d.nb ? d.nb : d.B; }
 
 const char* const kFwdKernelNames[kFwdKernels] = {"k_step_cf", "k_step_choice", "k_step_merge",
                                                  "k_step_scan", "k_step_transfer"};
@@ -931,19 +933,19 @@ void launch_fwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
                        cudaStream_t st) {
   switch (which) {
     case 0:
-      k_step_cf<<<grid_n(d.N, kCfThreads * kCfPer, d.B), kCfThreads, 0, st>>>(d, t, s_cur);
+      k_step_cf<<<grid_n(d.N, kCfThreads * kCfPer, nbl(d)), kCfThreads, 0, st>>>(d, t, s_cur);
       break;
     case 1:
-      k_step_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);
+      k_step_choice<<<grid_n(d.L, 128, nbl(d)), 128, 0, st>>>(d, t, s_cur);
       break;
     case 2:
-      k_step_merge<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur, 0);
+      k_step_merge<<<grid_n(d.L, 128, nbl(d)), 128, 0, st>>>(d, t, s_cur, 0);
       break;
     case 3:
-      k_step_scan<<<d.B, 1024, 0, st>>>(d, s_cur, s_next, 0);
+      k_step_scan<<<nbl(d), 1024, 0, st>>>(d, s_cur, s_next, 0);
       break;
     default:
-      k_step_transfer<<<grid_n(d.N, kTransferThreads * kTransferPer, d.B), kTransferThreads, 0, st>>>(
+      k_step_transfer<<<grid_n(d.N, kTransferThreads * kTransferPer, nbl(d)), kTransferThreads, 0, st>>>(
           d, s_cur, s_next);
   }
 }

@@ -1,6 +1,6 @@
 """Forward timing on C3 (dn=30, 120 steps) at B scenarios in the auto (0) and
 step-graph (3) schedules, plus the graph's per-kernel split:
-graph_time.py B [B ...]."""
+graph_time.py B [B ...]; DTG_SPLIT=k sets the graph's scenario branches (flag 8)."""
 import os
 import sys
 
@@ -20,6 +20,7 @@ for B, mode in ((int(a), m) for a in sys.argv[1:] for m in (0, 3)):
     e.set_params(p)
     e.set_state(lk, ps)
     e.set_mode(mode)
+    e.set_flag(8, int(os.environ.get("DTG_SPLIT", "0")))
     for b in range(B):
         e.set_noise(7, 1000 + b, b)
     for _ in range(2):

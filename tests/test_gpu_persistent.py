@@ -37,6 +37,7 @@ def run(sc, p, B, mode, T, spi, ckpt=True):
     (6, 300.0, 2400, 2, 300, 5),
     (23, 1609.34, 1000020, 30, 120, 8),
     (4, 400.0, 1000, 1, 200, 300),  # more scenarios than resident CTAs -> scenario loop
+    (4, 400.0, 1000, 1, 100, 37),   # step graph in 4 uneven scenario branches (9, 9, 9, 10)
     (50, 400.0, 100000, 1, 60, 1),  # C2: 12,300 links -> lean layout (per-link arrays in global memory)
 ])
 def test_persistent_equals_step_graph(n, length, veh, dn, T, B):
