@@ -1,3 +1,2 @@
-timeout 200 python scripts/graph_time.py 32 64 256 2>&1 | cut -c1-60
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+echo lanes2; timeout 200 python scripts/graph_time.py 64 256 2>&1 | grep "{}"
+for v in ch1 ch4; do echo $v; DTG_VARIANT_ROOT=scripts/_var/$v timeout 200 python scripts/graph_time.py 64 256 2>&1 | grep "{}"; done
