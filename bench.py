@@ -223,6 +223,8 @@ def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"bench.py --gpus {n_gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if world > 1:
         import torch.distributed as dist
 
@@ -673,6 +675,25 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def relaunch_under_torchrun(n_gpus):
+    """`python bench.py --gpus N` without a launcher: start N ranks (one per
+    GPU) under torch.distributed.run on this node and exit with its status, so
+    a plain invocation measures N GPUs instead of silently running one."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    # NCCL's init log (communicator size / rank lines) stays on for the driver
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execvpe(sys.executable, cmd, env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -684,6 +705,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-throughput", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
     if args.impl == "reference":
         run_reference(args)
     else:

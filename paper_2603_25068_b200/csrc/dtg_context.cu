@@ -558,6 +558,13 @@ int dtg_set_stream(dtg_ctx* c, void* s) {
   });
 }
 
+int dtg_get_stream(const dtg_ctx* c, void** stream, int* owned) {
+  if (!c) return DTG_ERR_RUNTIME;
+  if (stream) *stream = c->stream;
+  if (owned) *owned = c->own_stream ? 1 : 0;
+  return DTG_OK;
+}
+
 int dtg_profile_persistent(dtg_ctx* c, int T, int spi, double* phase_us, int* grid_out) {
   return guarded(c, [&] {
     c->want_stamps = true;
@@ -1163,7 +1170,9 @@ static void run_backward_persistent(dtg_ctx* c, cudaStream_t st) {
   ch |= c->bsort.ensure(B * MD * N);
   ch |= c->ba0part.ensure(B * nblk * MD * 32);
   ch |= c->vbar.ensure(2 * BN * MD);
-  (void)ch;
+  // vbar is shared with the step-graph reverse sweep, whose cached graph
+  // (bwd_exec) captured its old pointer: a reallocation must invalidate it
+  if (ch) c->drop_graphs();
   CK(cudaMemsetAsync(c->bccnt.p, 0, BL * 4, st));
   CK(cudaMemsetAsync(c->bdep.p, 0, BL * 4, st));
   CK(cudaMemsetAsync(c->bacount.p, 0, 2 * B * 4, st));
@@ -1332,6 +1341,10 @@ int dtg_set_loss_mse(dtg_ctx* c, int k_obs, int n_obs, const int* link_ids,
   return guarded(c, [&] {
     if (k_obs < 0 || n_obs < 1 || !link_ids || (k_obs > 0 && !values))
       throw std::invalid_argument("loss: no observed links");
+    if (n_obs > dtg::max_mse_obs(k_obs))
+      throw std::invalid_argument("loss: " + std::to_string(n_obs) + " observed links exceed the device MSE "
+                                  "kernel's shared-memory capacity (" + std::to_string(dtg::max_mse_obs(k_obs)) +
+                                  " links for " + std::to_string(k_obs) + " intervals)");
     std::vector<int> first(n_obs, 1), next(n_obs, -1);
     for (int q = 0; q < n_obs; ++q) {
       if (link_ids[q] < 0 || link_ids[q] >= c->L)
@@ -1415,7 +1428,7 @@ int dtg_gradient_device_loss(dtg_ctx* c, double* d_rows) {
     v.cum_seed = c->cum_seed.p;
     v.loss = c->loss_val.p;
     v.extra = c->loss_extra.p;
-    dtg::launch_device_loss(v, st);
+    CK(dtg::launch_device_loss(v, st));
     CK(cudaGetLastError());
     if (c->last_T > 0) {
       run_backward(c, nullptr, nullptr, nullptr, cudaMemcpyDeviceToDevice, true);

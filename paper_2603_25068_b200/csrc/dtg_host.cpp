@@ -803,12 +803,27 @@ class DeviceLoop {
     first_ = ex ? ex->rank * local_ : 0;
     if (ex && world > 1 && (!ex->d_local || !ex->d_full || !ex->gather))
       throw std::invalid_argument("draw exchange needs d_local, d_full and gather");
+    // the gather is ordered after this rank's rows (and the reduction after the
+    // gather) only through a stream both sides share
+    if (ex && world > 1 && !ex->stream)
+      throw std::invalid_argument("draw exchange with world > 1 needs the CUDA stream of its gather");
     ctx_ = detail::context_for(s, N_, local_, s.horizon_steps);
     detail::invalidate(ctx_);  // state and parameters are set directly below
-    if (ex && ex->stream) check(ctx_, dtg_set_stream(ctx_, ex->stream));
+    if (ex && ex->stream) {
+      // the cached scenario context outlives this loop: remember its stream
+      // and hand it back when the loop ends (the caller's stream may be gone)
+      check(ctx_, dtg_get_stream(ctx_, &prev_stream_, &prev_owned_));
+      check(ctx_, dtg_set_stream(ctx_, ex->stream));
+      rebound_ = true;
+    }
     check(ctx_, dtg_set_state(ctx_, -1, init.link.data(), init.pos.data()));
     red_.resize(5 * static_cast<std::size_t>(L_) + 2);
   }
+  ~DeviceLoop() {
+    if (rebound_) dtg_set_stream(ctx_, prev_owned_ ? nullptr : prev_stream_);
+  }
+  DeviceLoop(const DeviceLoop&) = delete;
+  DeviceLoop& operator=(const DeviceLoop&) = delete;
   dtg_ctx* ctx() const { return ctx_; }
 
   /// Runs this rank's draws of one iteration; returns the draw-reduced row over
@@ -834,6 +849,9 @@ class DeviceLoop {
   const DrawExchange* ex_;
   dtg_ctx* ctx_ = nullptr;
   std::vector<double> red_;
+  void* prev_stream_ = nullptr;
+  int prev_owned_ = 1;
+  bool rebound_ = false;
 };
 
 bool all_finite(const double* v, std::size_t n) {

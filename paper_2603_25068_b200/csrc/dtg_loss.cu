@@ -116,18 +116,28 @@ __global__ void k_reduce_rows(int D, int L, const double* __restrict__ rows, int
 
 }  // namespace
 
-void launch_device_loss(const LossView& v, cudaStream_t st) {
+constexpr std::size_t kMseSmemCap = 227 * 1024;
+
+int max_mse_obs(int k_obs) {
+  return static_cast<int>(kMseSmemCap / sizeof(double)) - (k_obs + 1);
+}
+
+cudaError_t launch_device_loss(const LossView& v, cudaStream_t st) {
   if (v.kind == kLossMse) {
     // as many intervals' residuals in shared memory as fit in ~160 KB
     const int n = v.nobs > 0 ? v.nobs : 1;
+    if (n > max_mse_obs(v.kobs)) return cudaErrorInvalidValue;  // rejected by dtg_set_loss_mse
     int kchunk = static_cast<int>((160 * 1024 / 8 - (v.kobs + 1)) / n);
     kchunk = std::max(1, std::min(kchunk, v.kobs > 0 ? v.kobs : 1));
     const std::size_t smem = sizeof(double) * (static_cast<std::size_t>(kchunk) * n + v.kobs + 1);
-    cudaFuncSetAttribute(k_loss_mse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const cudaError_t e = cudaFuncSetAttribute(k_loss_mse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
     k_loss_mse<<<v.B, 512, smem, st>>>(v, kchunk);
   } else if (v.kind == kLossControl) {
     k_loss_control<<<(v.B + 127) / 128, 128, 0, st>>>(v);
   }
+  return cudaGetLastError();
 }
 
 void launch_pack_rows(int B, int L, const double* grads, const double* loss,

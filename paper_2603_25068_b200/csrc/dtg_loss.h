@@ -41,7 +41,10 @@ struct LossView {
   double* extra;      // [B] control: achieved count cum_final[target] * dn
 };
 
-void launch_device_loss(const LossView& v, cudaStream_t st);
+// Largest observed-link count the MSE kernel holds in shared memory (one
+// interval of residuals plus the interval sums must fit 227 KB).
+int max_mse_obs(int k_obs);
+cudaError_t launch_device_loss(const LossView& v, cudaStream_t st);
 
 /// rows[b] = [grads u|kappa|beta|alpha|cost (5L), loss, extra] for b < B.
 void launch_pack_rows(int B, int L, const double* grads, const double* loss,

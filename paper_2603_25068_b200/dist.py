@@ -107,7 +107,12 @@ class DeviceDrawExchange:
     bit for bit for any world size.  Only O(L) bytes per draw cross NVLink per
     iteration; nothing goes through host memory except the reduced row."""
 
-    def __init__(self, n_links: int, n_draws: int, world: int, rank: int, group=None, stream=None):
+    def __init__(self, n_links: int, n_draws: int, world: int, rank: int, group=None, stream=None,
+                 host_staged: bool = False):
+        """host_staged: gather through host memory with a CPU backend (gloo)
+        instead of NCCL on the device — the same rows in the same order, for
+        process groups without NCCL (e.g. several ranks sharing one GPU in a
+        test)."""
         import torch
         import torch.distributed as dist
 
@@ -120,17 +125,25 @@ class DeviceDrawExchange:
         self.full = torch.zeros((n_draws, R), dtype=torch.float64, device="cuda")
         self.group = group
         self.calls = 0
+        self.error = None
 
         def _gather(_user):
             try:
                 with torch.cuda.stream(self.stream):
-                    if world > 1:
+                    if world > 1 and host_staged:
+                        self.stream.synchronize()  # the rows are written on this stream
+                        h_local = self.local.cpu()
+                        h_full = torch.empty(self.full.shape, dtype=self.full.dtype)
+                        dist.all_gather_into_tensor(h_full, h_local, group=self.group)
+                        self.full.copy_(h_full)
+                    elif world > 1:
                         dist.all_gather_into_tensor(self.full, self.local, group=self.group)
                     else:
                         self.full.copy_(self.local)
                 self.calls += 1
                 return 0
-            except Exception:  # reported as a runtime error by the C++ loop
+            except Exception as e:  # reported as a runtime error by the C++ loop
+                self.error = e
                 return 1
 
         self._cb = GatherFn(_gather)  # keep the trampoline alive
@@ -139,23 +152,24 @@ class DeviceDrawExchange:
 
 
 def calibrate_sharded(sc, obs_ids, obs_values, seed: int, cfg=None, bounds=None, init=None,
-                      world: int = 1, rank: int = 0, group=None, stream=None):
+                      world: int = 1, rank: int = 0, group=None, stream=None, host_staged: bool = False):
     """calibrate() with the iteration's noise draws sharded over `world` GPUs."""
     from .engine import OptimizeConfig, calibrate
 
     cfg = cfg or OptimizeConfig()
     draws = max(1, cfg.noise_draws) if cfg.resample_noise else 1
-    ex = DeviceDrawExchange(sc.n_links, draws, world, rank, group, stream)
+    ex = DeviceDrawExchange(sc.n_links, draws, world, rank, group, stream, host_staged)
     return calibrate(sc, obs_ids, obs_values, seed, bounds=bounds, cfg=cfg, init=init, exchange=ex.c)
 
 
 def optimize_control_sharded(sc, calibrated, target_link: int, desired: float, seed: int, cfg=None,
-                             cost_floor: float = 0.05, world: int = 1, rank: int = 0, group=None, stream=None):
+                             cost_floor: float = 0.05, world: int = 1, rank: int = 0, group=None, stream=None,
+                             host_staged: bool = False):
     """optimize_control() with the iteration's noise draws sharded over `world` GPUs."""
     from .engine import OptimizeConfig, optimize_control
 
     cfg = cfg or OptimizeConfig()
     draws = max(1, cfg.noise_draws) if cfg.resample_noise else 1
-    ex = DeviceDrawExchange(sc.n_links, draws, world, rank, group, stream)
+    ex = DeviceDrawExchange(sc.n_links, draws, world, rank, group, stream, host_staged)
     return optimize_control(sc, calibrated, target_link, desired, seed, cfg=cfg, cost_floor=cost_floor,
                             exchange=ex.c)

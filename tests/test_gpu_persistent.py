@@ -143,3 +143,29 @@ def test_speculative_head_decisions_are_exact(n, length, veh, dn, T, B, mode):
         assert np.array_equal(out[0][0], o[0])
         for a, b in zip(out[0][1:], o[1:]):
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_mode_toggles_on_one_engine_keep_backward_exact():
+    """One context, reverse sweeps alternating between the step graph (mode 3)
+    and the persistent kernel (mode 0): the persistent sweep grows the shared
+    vbar buffer, which the cached step-graph sweep captured, so the graph must
+    be rebuilt (stale vbar pointer in bwd_exec)."""
+    sc = P.Scenario.grid(6, 300.0, 42, 1000.0).configure(2400, 2, 120, 300)
+    p = sc.sample_parameters(3)
+    spi, T, B = sc.steps_per_interval, 120, 3
+    lk, ps = sc.seed_agents()
+    rng = np.random.default_rng(11)
+    snap = rng.normal(size=(B, T // spi, sc.n_links))
+    xs = rng.normal(size=(B, sc.n_agents))
+    e = P.Engine(sc, B, T)
+    e.set_params(p)
+    e.set_state(lk, ps)
+    for b in range(B):
+        e.set_noise(7, 40 + b, b)
+    got = []
+    for mode in (3, 0, 3, 0, 3):
+        e.set_mode(mode)
+        e.forward(T, spi, checkpoint=True)
+        got.append(e.backward(snap_seeds=snap, x_seeds=xs))
+    for g in got[1:]:
+        assert np.array_equal(g, got[0])
