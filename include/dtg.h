@@ -76,8 +76,11 @@ void dtg_destroy(dtg_ctx* ctx);
 /* Last error message of this context (or of the failed dtg_create when
  * ctx == NULL). */
 const char* dtg_last_error(const dtg_ctx* ctx);
-/* Run on this cudaStream_t (default: a stream owned by the context). */
+/* Run on this cudaStream_t (default: a stream owned by the context).  NULL
+ * returns the context to a private non-blocking stream of its own. */
 int dtg_set_stream(dtg_ctx* ctx, void* cuda_stream);
+/* The stream the context runs on; *owned = 1 when it is the context's own. */
+int dtg_get_stream(const dtg_ctx* ctx, void** cuda_stream, int* owned);
 /* Forward as one persistent cooperative kernel for all steps (default on);
  * off = one CUDA graph of 5 kernels per step (same results). */
 int dtg_set_persistent(dtg_ctx* ctx, int enabled);
@@ -160,11 +163,19 @@ int dtg_debug_gumbel(uint64_t seed, uint64_t key, int n, const uint64_t* rows,
  * (which: 0 Gumbel draw, 1 log, 2 exp, 3 division, 4 L2 pointer chase,
  * 5 counter-RNG uniform; 100 = empty grid.sync with `grid` CTAs of 512). */
 int dtg_debug_microbench(int which, int n, int grid, double* result);
-/* Test hook: bitwise check of the straight-line log / Gumbel against
- * libdevice on n inputs per kind; mismatches must be 0, flagged counts the
- * arguments routed to the libdevice fallback. */
+/* Test hook: the device's interleaved glibc log / Gumbel (several draws per
+ * chain) against its scalar glibc log on n inputs per kind; mismatches must
+ * be 0 and flagged stays 0. */
 int dtg_debug_log_check(uint64_t seed, long long n, unsigned long long* mismatches,
                         unsigned long long* flagged);
+/* Test hook: the glibc-identical exp / log (csrc/dtg_libm.h) against this
+ * host's libm (the reference's), bit for bit, on n inputs of kind `which`:
+ * 0 log(u) of Gumbel uniforms, 1 log(-log u), 2 the whole Gumbel -log(-log u),
+ * 3 log of any positive double, 4 log near 1, 5 exp on [-750, 710],
+ * 6 exp on [-60, 0], 7 exp of any finite double.  on_device: evaluate on the
+ * GPU (else the host build of the same code). */
+int dtg_debug_libm_check(int which, uint64_t seed, long long n, int on_device,
+                         unsigned long long* mismatches);
 /* Test hook: one fused forward recording, per step and warp, the slot-phase
  * start, end of the offsets prologue, end of the slot loop (globaltimer ns)
  * and the number of arrived agents in the warp: out[T][n_warps][4]. */
@@ -354,7 +365,10 @@ typedef struct {
  * gather(user) — which must all-gather d_local of every rank, rank-major,
  * into d_full [D][5L+2], ordered on `stream` (e.g. NCCL all_gather) — and
  * reduces all D rows in draw order, so every rank gets the single-GPU result
- * bit for bit.  The context runs on `stream` (cudaStream_t, may be NULL). */
+ * bit for bit.  The context runs on `stream` (cudaStream_t) for the duration
+ * of the loop and returns to its previous stream afterwards; `stream` is
+ * required when world > 1 (the gather is ordered after the rows only through
+ * it) and may be NULL for world == 1. */
 typedef int (*dtg_gather_fn)(void* user);
 typedef struct {
   int world;

@@ -45,6 +45,15 @@ double port_rng_uniform(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
   return ((double)(port_rng_bits(seed, a, b, c) >> 11) + 0.5) *
          (1.0 / 9007199254740992.0);
 }
+uint64_t port_fnv1a64(const void* data, size_t n, uint64_t h) {
+  const unsigned char* b = (const unsigned char*)data;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= b[i];
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
 double port_gumbel(uint64_t seed, uint64_t key, uint64_t row, uint64_t col) {
   /* tensor.cpp:694-695 */
   const double u = port_rng_uniform(seed, key, row, col);

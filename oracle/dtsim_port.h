@@ -9,6 +9,7 @@
  */
 #ifndef DTSIM_PORT_H
 #define DTSIM_PORT_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -67,6 +68,8 @@ uint64_t port_rng_fork(uint64_t seed, uint64_t label);
 uint64_t port_rng_bits(uint64_t seed, uint64_t a, uint64_t b, uint64_t c);
 double port_rng_uniform(uint64_t seed, uint64_t a, uint64_t b, uint64_t c);
 double port_gumbel(uint64_t seed, uint64_t key, uint64_t row, uint64_t col);
+/* FNV-1a 64 over n bytes continuing from h (the SURVEY §8c KAT fingerprints). */
+uint64_t port_fnv1a64(const void* data, size_t n, uint64_t h);
 
 const char* port_last_error(void);
 

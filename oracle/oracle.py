@@ -51,6 +51,16 @@ def fnv1a64_fast(*arrays: np.ndarray) -> int:
     return h
 
 
+def fnv1a64_c(*arrays: np.ndarray) -> int:
+    """fnv1a64 computed by the C port (for arrays of hundreds of MB)."""
+    lib = PortLib().lib
+    h = 0xCBF29CE484222325
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h = lib.port_fnv1a64(a.ctypes.data, a.nbytes, h)
+    return int(h)
+
+
 def grid_links(n: int, length: float):
     """The synthetic grid generator of SURVEY §8d: for each (r, c) in row-major
     order push the east pair then the south pair."""
@@ -84,6 +94,7 @@ class RefLib:
     def __init__(self, path: str = REF_SO):
         if not os.path.exists(path):
             raise FileNotFoundError(path)
+        self.path = path
         L = self.lib = C.CDLL(path)
         L.ref_last_error.restype = C.c_char_p
         L.ref_rng_fork.restype = u64
@@ -98,6 +109,9 @@ class RefLib:
         L.ref_scenario_links.argtypes = [C.c_int, C.c_int, _ip, _ip, _dp, _ip]
         L.ref_scenario_grid.restype = C.c_void_p
         L.ref_scenario_grid.argtypes = [C.c_int, C.c_double, u64, C.c_double]
+        L.ref_scenario_tntp.restype = C.c_void_p
+        L.ref_scenario_tntp.argtypes = [C.c_char_p, C.c_double, u64, C.c_double]
+        L.ref_scenario_attach_virtual.argtypes = [C.c_void_p, u64, C.c_double]
         L.ref_scenario_free.argtypes = [C.c_void_p]
         L.ref_scenario_config.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int]
         L.ref_scenario_custom_init.argtypes = [C.c_void_p, C.c_int, _ip, _dp]
@@ -207,6 +221,44 @@ class RefScenario:
     @classmethod
     def grid(cls, lib: RefLib, n: int, length: float, net_seed: int = 42, virt_len: float = 1000.0):
         return cls(lib, lib.lib.ref_scenario_grid(n, length, net_seed, virt_len))
+
+    @classmethod
+    def tntp(cls, lib: RefLib, text: str, unit_scale: float, net_seed: int = 42, virt_len: float = 1000.0):
+        """parse_tntp_text + attach_virtual_links (build_network, pipeline.cpp:165-170).
+
+        The reference's parser (its ``istream >> double``) crashes inside a
+        process that has numpy's bundled runtime libraries loaded, so the text
+        is parsed by the reference in a numpy-free subprocess; its physical
+        links are rebuilt here with make_network (network.cpp:238-247 — the
+        same Network parse_tntp_text returns) and the virtual links attached
+        in-process.
+        """
+        import json
+        import subprocess
+        import sys
+
+        # physical links only: parse without attaching (virtual links are appended after them)
+        code = ("import ctypes as C, json, sys\n"
+                f"L = C.CDLL({lib.path!r})\n"
+                "L.ref_tntp_physical.restype = C.c_int\n"
+                "L.ref_tntp_physical.argtypes = [C.c_char_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]\n"
+                "L.ref_last_error.restype = C.c_char_p\n"
+                "txt = sys.stdin.buffer.read()\n"
+                "n = L.ref_tntp_physical(txt, float(sys.argv[1]), None, None, None, None)\n"
+                "assert n >= 0, L.ref_last_error()\n"
+                "f, t = (C.c_int * n)(), (C.c_int * n)()\n"
+                "ln = (C.c_double * n)()\n"
+                "nn = C.c_int(0)\n"
+                "L.ref_tntp_physical(txt, float(sys.argv[1]), f, t, ln, C.byref(nn))\n"
+                "print(json.dumps(dict(n_nodes=nn.value, frm=list(f), to=list(t), length=[x.hex() for x in ln])))\n")
+        r = subprocess.run([sys.executable, "-c", code, repr(float(unit_scale))], input=text.encode(),
+                           capture_output=True, check=True)
+        d = json.loads(r.stdout)
+        n = len(d["frm"])
+        sc = cls.from_links(lib, d["n_nodes"], d["frm"], d["to"], [float.fromhex(x) for x in d["length"]],
+                            [0] * n)
+        lib.check(lib.lib.ref_scenario_attach_virtual(sc.h, net_seed, virt_len))
+        return sc
 
     @classmethod
     def from_links(cls, lib: RefLib, n_nodes, frm, to, length, kind):
@@ -436,6 +488,8 @@ class PortLib:
         L.port_rng_uniform.argtypes = [u64, u64, u64, u64]
         L.port_gumbel.restype = C.c_double
         L.port_gumbel.argtypes = [u64, u64, u64, u64]
+        L.port_fnv1a64.restype = u64
+        L.port_fnv1a64.argtypes = [C.c_void_p, C.c_size_t, u64]
         vp = C.c_void_p
         L.port_forward.argtypes = [vp, vp, u64, u64, C.c_int, _ip, _dp, C.c_int, _dp, _ip, _dp, vp, vp]
         L.port_gradient.argtypes = [vp, vp, u64, u64, C.c_int, _ip, _dp, C.c_int, C.c_int,

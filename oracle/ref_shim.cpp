@@ -146,6 +146,50 @@ void* ref_scenario_grid(int n, double len, uint64_t net_seed, double virt_len) {
   return out;
 }
 
+/// parse_tntp_text (network.cpp:58-118) + attach_virtual_links with
+/// RngStream(net_seed), as build_network does (pipeline.cpp:165-170).
+void* ref_scenario_tntp(const char* text, double unit_scale, uint64_t net_seed,
+                        double virt_len) {
+  void* out = nullptr;
+  if (guarded([&] {
+        Network phys = parse_tntp_text(std::string(text), unit_scale);
+        auto* rs = new RefScn;
+        rs->s.net = attach_virtual_links(phys, RngStream(net_seed), virt_len);
+        out = rs;
+      }))
+    return nullptr;
+  return out;
+}
+
+/// parse_tntp_text alone: the physical links (n_links returned, -1 on error;
+/// arrays may be NULL to query the size).
+int ref_tntp_physical(const char* text, double unit_scale, int* from, int* to,
+                      double* len, int* n_nodes) {
+  int n = -1;
+  if (guarded([&] {
+        Network net = parse_tntp_text(std::string(text), unit_scale);
+        n = net.n_links();
+        if (from)
+          for (int i = 0; i < n; ++i) {
+            from[i] = net.links[i].from_node;
+            to[i] = net.links[i].to_node;
+            len[i] = net.links[i].length;
+          }
+        if (n_nodes) *n_nodes = net.n_nodes;
+      }))
+    return -1;
+  return n;
+}
+
+/// attach_virtual_links (network.cpp:151-201) applied in place to a scenario
+/// whose network holds physical links only.
+int ref_scenario_attach_virtual(void* h, uint64_t net_seed, double virt_len) {
+  return guarded([&] {
+    auto& s = static_cast<RefScn*>(h)->s;
+    s.net = attach_virtual_links(s.net, RngStream(net_seed), virt_len);
+  });
+}
+
 void ref_scenario_free(void* h) { delete static_cast<RefScn*>(h); }
 
 void ref_scenario_config(void* h, int n_vehicles, int delta_n, double tau,

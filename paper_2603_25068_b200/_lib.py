@@ -88,6 +88,7 @@ SIGNATURES = [
     ("dtg_destroy", None, [vp]),
     ("dtg_last_error", C.c_char_p, [vp]),
     ("dtg_set_stream", i32, [vp, vp]),
+    ("dtg_get_stream", i32, [vp, C.POINTER(vp), C.POINTER(C.c_int)]),
     ("dtg_set_graphs", i32, [vp, i32]),
     ("dtg_set_persistent", i32, [vp, i32]),
     ("dtg_set_mode", i32, [vp, i32]),
@@ -153,6 +154,7 @@ SIGNATURES = [
     ("dtg_debug_gumbel", i32, [u64, u64, i32, _u64p, _u64p, _dp]),
     ("dtg_debug_microbench", i32, [i32, i32, i32, _dp]),
     ("dtg_debug_log_check", i32, [u64, C.c_longlong, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
+    ("dtg_debug_libm_check", i32, [i32, u64, C.c_longlong, i32, C.POINTER(C.c_ulonglong)]),
     ("dtg_debug_warp_records", i32, [vp, i32, i32, vp, C.POINTER(C.c_int)]),
     ("dtg_debug_bwd_stamps", i32, [vp, vp, C.POINTER(C.c_int)]),
     ("dtg_scenario_last_error", C.c_char_p, [vp]),

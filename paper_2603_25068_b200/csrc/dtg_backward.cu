@@ -127,7 +127,7 @@ __device__ __forceinline__ double x1_bar_p(const BView& V, int b, int k, int j, 
     const double len = d.len[j];
     const double sc = d.sc[j];
     const double z = (x1 + (-(0.5 * len))) * sc;
-    const double sg = z >= 0.0 ? 1.0 / (1.0 + exp(-z)) : exp(z) / (1.0 + exp(z));
+    const double sg = z >= 0.0 ? 1.0 / (1.0 + dexp(-z)) : dexp(z) / (1.0 + dexp(z));
     xb = xb + (((qt * 1.0) * sg) * (1.0 - sg)) * sc;
   }
   return xb;
@@ -161,15 +161,10 @@ __device__ __forceinline__ void replay_head(const BView& V, int b, int t, int k,
       double y[kFastDeg], ex[kFastDeg];
 #pragma unroll
       for (int e = 0; e < kFastDeg; ++e) sc[e] = d.succ[s0 + (e < deg ? e : 0)];
-      int bad = 0;  // straight-line logs: the five draw chains interleave
+      double gg[kFastDeg];  // the five draw chains batched
+      gumbel_draws<kFastDeg>(h2l, sc, gg);
 #pragma unroll
-      for (int e = 0; e < kFastDeg; ++e)
-        y[e] = (lz[e < deg ? e : 0] + gumbel_sl(rng_final(h2l, static_cast<std::uint64_t>(sc[e])), bad)) * d.kinv;
-      if (bad) {
-#pragma unroll
-        for (int e = 0; e < kFastDeg; ++e)
-          y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sc[e])))) * d.kinv;
-      }
+      for (int e = 0; e < kFastDeg; ++e) y[e] = (lz[e < deg ? e : 0] + gg[e]) * d.kinv;
       // the logits are kept (R4 forms pi from them with softmax_stage2's
       // operations); the choice is the first argmax, read off the logits
 #pragma unroll
@@ -525,7 +520,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           const int c0 = d.lnk[so + a0s];
           const int s0 = d.succ_off[c0], deg0 = d.succ_off[c0 + 1] - s0;
           const double vv = 0.0 - kMaskLarge;
-          const double lzv = log(static_cast<double>(nA) * 1.0) + vv;
+          const double lzv = dlog(static_cast<double>(nA) * 1.0) + vv;
           const double logz = vv - lzv;
           // one draw per thread: items (row e, arrived q) row-major with each row
           // padded to whole warps, so a warp reduces a single row; every warp
@@ -642,7 +637,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
 #pragma unroll
             for (int e = 0; e < kFastDeg; ++e)
               if (e < cnt) {
-                const double bv = bar[e] - exp(lz[e]) * gs;
+                const double bv = bar[e] - dexp(lz[e]) * gs;
                 const int s = cf[e].slot;
                 V.lbar_row[bn + s] = (e == 0 ? 0.0 + abar_w : 0.0) + bv * cf[e].alpha;
                 V.prio_bar[bn + s] = 0.0 + bv * 1.0;
@@ -719,19 +714,19 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
                     keys[m + 1] = kk;
                   }
                   const double vv = 0.0 - kMaskLarge;
-                  const double lzv = log(static_cast<double>(nA) * 1.0) + vv;
+                  const double lzv = dlog(static_cast<double>(nA) * 1.0) + vv;
                   const double logz = vv - lzv;
                   double z2 = 0.0;
                   for (int q = 0; q < nA; ++q) {
                     const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
                                             static_cast<std::uint64_t>(i), keys[q] >> 32);
-                    z2 += exp((logz + g) * d.kinv - x.y1);
+                    z2 += dexp((logz + g) * d.kinv - x.y1);
                   }
                   double bp = -1.0;
                   for (int q = 0; q < nA; ++q) {
                     const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t),
                                             static_cast<std::uint64_t>(i), keys[q] >> 32);
-                    const double pv = exp((logz + g) * d.kinv - x.y1) / z2;
+                    const double pv = dexp((logz + g) * d.kinv - x.y1) / z2;
                     if (pv > bp) {
                       bp = pv;
                       ws = static_cast<int>(keys[q] & 0xffffffffull);
@@ -855,7 +850,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               double z2 = 0.0;
 #pragma unroll
               for (int e = 0; e < kFastDeg; ++e) {
-                pi[e] = exp(yv[e] - m2);
+                pi[e] = dexp(yv[e] - m2);
                 if (e < deg) z2 += pi[e];
               }
 #pragma unroll
@@ -881,7 +876,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               }
 #pragma unroll
             for (int e = 0; e < kFastDeg; ++e)
-              if (e < deg) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e] - exp(lz[e]) * gs;
+              if (e < deg) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e] - dexp(lz[e]) * gs;
           } else {
             double bar[kMaxDeg], pi[kMaxDeg];
             {  // pi from the replayed logits: softmax_stage2's operations
@@ -889,8 +884,8 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               for (int e = 1; e < deg; ++e)
                 if (m2 < lp[e]) m2 = lp[e];
               double z2 = 0.0;
-              for (int e = 0; e < deg; ++e) z2 += exp(lp[e] - m2);
-              for (int e = 0; e < deg; ++e) pi[e] = exp(lp[e] - m2) / z2;
+              for (int e = 0; e < deg; ++e) z2 += dexp(lp[e] - m2);
+              for (int e = 0; e < deg; ++e) pi[e] = dexp(lp[e] - m2) / z2;
             }
             for (int e = 0; e < deg; ++e) bar[e] = 0.0;
             if (hit) bar[ed] = lrow;

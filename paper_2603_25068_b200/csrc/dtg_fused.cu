@@ -68,16 +68,11 @@ __device__ __forceinline__ void head_draw(const CView& V, std::uint64_t h1l, std
     double y[kFastDeg], ex[kFastDeg];
 #pragma unroll
     for (int e = 0; e < kFastDeg; ++e) sj[e] = d.succ[sb + (e < deg ? e : 0)];
-    // straight-line logs (dtg_device.cuh): the five draw chains interleave
-    int bad = 0;
+    // the five draw chains batched (dtg_device.cuh gumbel_draws)
+    double gg[kFastDeg];
+    gumbel_draws<kFastDeg>(h2l, sj, gg);
 #pragma unroll
-    for (int e = 0; e < kFastDeg; ++e)
-      y[e] = (lz[e < deg ? e : 0] + gumbel_sl(rng_final(h2l, static_cast<std::uint64_t>(sj[e])), bad)) * d.kinv;
-    if (bad) {
-#pragma unroll
-      for (int e = 0; e < kFastDeg; ++e)
-        y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2l, static_cast<std::uint64_t>(sj[e])))) * d.kinv;
-    }
+    for (int e = 0; e < kFastDeg; ++e) y[e] = (lz[e < deg ? e : 0] + gg[e]) * d.kinv;
     const int best = softmax_first_argmax<kFastDeg>(deg, y, ex);
     c = sj[best];
   } else {
@@ -137,29 +132,22 @@ __device__ __forceinline__ void spec_segment(const CView& V, std::uint64_t h1l, 
   double y[2] = {0.0, 0.0}, gm[2] = {0.0, 0.0};
   if (act && !wide) {
     const std::uint64_t h2l = rng_prefix2(h1l, static_cast<std::uint64_t>(a));
-    std::uint64_t bl_[2], bm[2];
-    int bad = 0;
-    double gl[2];
+    // the four chains (two link, two merge draws) batched
+    std::uint64_t bb[4];
+    double gg[4];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const std::uint64_t sj = static_cast<std::uint64_t>(sjv[h]);
-      bl_[h] = rng_final(h2l, sj);
-      bm[h] = rng_final(rng_prefix2(h1m, sj), static_cast<std::uint64_t>(a));
+      bb[h] = rng_final(h2l, sj);
+      bb[2 + h] = rng_final(rng_prefix2(h1m, sj), static_cast<std::uint64_t>(a));
     }
+    int bad = 0;
+    gumbel_sl_v<4>(bb, gg, bad);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      gl[h] = gumbel_sl(bl_[h], bad);
-      gm[h] = gumbel_sl(bm[h], bad);
+      gm[h] = gg[2 + h];
+      y[h] = (lzv[h] + gg[h]) * d.kinv;
     }
-    if (bad) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        gl[h] = gumbel_bits(bl_[h]);
-        gm[h] = gumbel_bits(bm[h]);
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) y[h] = (lzv[h] + gl[h]) * d.kinv;
   }
   double yv[kSpecDeg], ex[kSpecDeg];
 #pragma unroll
@@ -344,7 +332,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ep
 // decisions) are compiled in; without them the kernel is the plain schedule
 // (their mere presence costs the many-slots-per-thread variant ~10%).
 template <bool kCluster, int kBatch, bool kFeat, bool kLean>
-__global__ void __launch_bounds__(kClusterThreads) k_forward_fused(CView V) {
+__global__ void __launch_bounds__(kClusterThreads, 1) k_forward_fused(CView V) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const DevView& d = V.d;
   const int L = d.L, N = d.N;

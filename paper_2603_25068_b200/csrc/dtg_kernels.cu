@@ -143,18 +143,12 @@ __global__ void __launch_bounds__(128) k_step_choice(DevView d, int t, int s_cur
         const std::uint64_t h2 = rng_prefix2(rng_prefix1(d.seed_link[b], static_cast<std::uint64_t>(t)),
                                              static_cast<std::uint64_t>(agent));
         int sj[kFastSucc];
-        double y[kFastSucc], ex[kFastSucc];
-        int bad = 0;
+        double y[kFastSucc], ex[kFastSucc], gg[kFastSucc];
 #pragma unroll
-        for (int e = 0; e < kFastSucc; ++e) {
-          sj[e] = d.succ[s0 + (e < deg ? e : 0)];
-          y[e] = (lz[e < deg ? e : 0] + gumbel_sl(rng_final(h2, static_cast<std::uint64_t>(sj[e])), bad)) * d.kinv;
-        }
-        if (bad) {
+        for (int e = 0; e < kFastSucc; ++e) sj[e] = d.succ[s0 + (e < deg ? e : 0)];
+        gumbel_draws<kFastSucc>(h2, sj, gg);  // the draw chains batched
 #pragma unroll
-          for (int e = 0; e < kFastSucc; ++e)
-            y[e] = (lz[e < deg ? e : 0] + gumbel_bits(rng_final(h2, static_cast<std::uint64_t>(sj[e])))) * d.kinv;
-        }
+        for (int e = 0; e < kFastSucc; ++e) y[e] = (lz[e < deg ? e : 0] + gg[e]) * d.kinv;
         const int best = softmax_first_argmax<kFastSucc>(deg, y, ex);
         c = sj[0];
 #pragma unroll
@@ -222,17 +216,17 @@ __device__ __forceinline__ int merge_softmax(const DevView& d, int b, int t, int
     const std::uint64_t h2 = rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
                                          static_cast<std::uint64_t>(i));
     double v[kFastSucc], y[kFastSucc], ex[kFastSucc];
-    int bad = 0;
+    {
+      int key[kFastSucc];
+#pragma unroll
+      for (int e = 0; e < kFastSucc; ++e) key[e] = e < nc ? cid[e] : 0;
+      gumbel_draws<kFastSucc>(h2, key, y);  // the draw chains batched
+    }
 #pragma unroll
     for (int e = 0; e < kFastSucc; ++e) {
       v[e] = e < nc ? d.alpha[bl + clink[e]] : 0.0;
       if (e < nc && v[e] == 0.0) atomicOr(&d.err[b], kErrZeroAlpha);
-      y[e] = e < nc ? gumbel_sl(rng_final(h2, static_cast<std::uint64_t>(cid[e])), bad) : 0.0;
-    }
-    if (bad) {
-#pragma unroll
-      for (int e = 0; e < kFastSucc; ++e)
-        y[e] = e < nc ? gumbel_bits(rng_final(h2, static_cast<std::uint64_t>(cid[e]))) : 0.0;
+      if (e >= nc) y[e] = 0.0;
     }
     {  // winner from alpha + g when the top two are clearly apart (bound in dtg_merge.cuh)
       int best = 0;
@@ -260,8 +254,8 @@ __device__ __forceinline__ int merge_softmax(const DevView& d, int b, int t, int
     double z = 0.0;
 #pragma unroll
     for (int e = 0; e < kFastSucc; ++e)
-      if (e < nc) z += exp(v[e] - m);
-    const double lzz = log(z) + m;
+      if (e < nc) z += dexp(v[e] - m);
+    const double lzz = dlog(z) + m;
 #pragma unroll
     for (int e = 0; e < kFastSucc; ++e) y[e] = ((v[e] - lzz) + y[e]) * d.kinv;
     return softmax_first_argmax<kFastSucc>(nc, y, ex);
@@ -632,7 +626,7 @@ __global__ void __launch_bounds__(kA0Threads) k_adj_a0(DevView d, int t, int s_c
   const int* alist = d.alist + bn;
   // uniform first stage: v = -1e12 everywhere, z = |A| exactly
   const double v = 0.0 - kMaskLarge;
-  const double lzv = log(static_cast<double>(nA) * 1.0) + v;
+  const double lzv = dlog(static_cast<double>(nA) * 1.0) + v;
   const double logz = v - lzv;
   Top2 tp[kMaxDeg];
   for (int r = 0; r < nr; ++r) tp[r] = Top2{-INFINITY, -INFINITY, INT_MAX, -1};
@@ -702,13 +696,13 @@ __global__ void __launch_bounds__(kA0Threads) k_adj_a0(DevView d, int t, int s_c
         for (int q = 0; q < nA; ++q) {
           const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t), static_cast<std::uint64_t>(i),
                                   keys[q] >> 32);
-          z2 += exp((logz + g) * d.kinv - m2);
+          z2 += dexp((logz + g) * d.kinv - m2);
         }
         double bp = -1.0;
         for (int q = 0; q < nA; ++q) {
           const double g = gumbel(d.seed_merge[b], static_cast<std::uint64_t>(t), static_cast<std::uint64_t>(i),
                                   keys[q] >> 32);
-          const double pv = exp((logz + g) * d.kinv - m2) / z2;
+          const double pv = dexp((logz + g) * d.kinv - m2) / z2;
           if (pv > bp) {
             bp = pv;
             best_all.id1 = static_cast<int>(keys[q] >> 32);
@@ -789,7 +783,7 @@ __device__ __forceinline__ double x1_bar(const DevView& d, std::size_t bn,
   if (qt != 0.0) {
     const double sc = d.sc[j];
     const double z = (x1 + (-d.ctr[j])) * sc;
-    const double sg = z >= 0.0 ? 1.0 / (1.0 + exp(-z)) : exp(z) / (1.0 + exp(z));
+    const double sg = z >= 0.0 ? 1.0 / (1.0 + dexp(-z)) : dexp(z) / (1.0 + dexp(z));
     xb = xb + (((qt * 1.0) * sg) * (1.0 - sg)) * sc;
   }
   return xb;

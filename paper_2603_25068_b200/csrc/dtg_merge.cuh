@@ -80,8 +80,8 @@ __device__ __forceinline__ int merge_softmax_fast(int cnt, const Cand* src, doub
   double z = 0.0;
 #pragma unroll
   for (int e = 0; e < F; ++e)
-    if (e < cnt) z += exp(c[e].alpha - m);
-  const double lzz = log(z) + m;
+    if (e < cnt) z += dexp(c[e].alpha - m);
+  const double lzz = dlog(z) + m;
   double y[F];
 #pragma unroll
   for (int e = 0; e < F; ++e) {
@@ -100,7 +100,7 @@ __device__ __forceinline__ int merge_softmax_fast(int cnt, const Cand* src, doub
   double z2 = 0.0;
 #pragma unroll
   for (int e = 0; e < F; ++e) {
-    ex[e] = exp(y[e] - m2);
+    ex[e] = dexp(y[e] - m2);
     if (e < cnt) z2 += ex[e];
   }
   int best = 0;

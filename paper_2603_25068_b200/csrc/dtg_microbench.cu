@@ -2,14 +2,20 @@
 // measured with clock64 by one thread (cycles per operation).
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <cstring>
+#include <vector>
 
 #include "dtg_device.cuh"
 
 namespace dtg {
 
 __global__ void k_micro(int which, int n, const int* chain, double* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // which >= 15: all 32 lanes run the chain on lane-dependent arguments
+  // (divergent table indices); lane 0 reports
+  if ((which < 15 && threadIdx.x != 0) || blockIdx.x != 0) return;
   double acc = 0.0;
   long long t0 = clock64();
   switch (which) {
@@ -87,6 +93,58 @@ __global__ void k_micro(int which, int n, const int* chain, double* out) {
       acc = x + bad;
       break;
     }
+    case 11: {  // dependent glibc log, table path (arguments >= 2)
+      double x = 1.5;
+      for (int i = 0; i < n; ++i) x = dlog(x + 2.0);
+      acc = x;
+      break;
+    }
+    case 12: {  // dependent glibc log, near-1 path
+      double x = 0.01;
+      for (int i = 0; i < n; ++i) x = dlog(1.0 + x * 0.5) + 0.01;
+      acc = x;
+      break;
+    }
+    case 13: {  // dependent glibc exp
+      double x = 0.5;
+      for (int i = 0; i < n; ++i) x = dexp(-x);
+      acc = x;
+      break;
+    }
+    case 15: {  // 32 lanes: dependent glibc log, table path
+      double x = 1.5 + threadIdx.x * 0.37;
+      for (int i = 0; i < n; ++i) x = dlog(x + 2.0 + threadIdx.x * 0.73);
+      acc = x;
+      break;
+    }
+    case 16: {  // 32 lanes: dependent libdevice log
+      double x = 1.5 + threadIdx.x * 0.37;
+      for (int i = 0; i < n; ++i) x = log(x + 2.0 + threadIdx.x * 0.73);
+      acc = x;
+      break;
+    }
+    case 17: {  // 32 lanes: dependent Gumbel draws (glibc logs)
+      for (int i = 0; i < n; ++i)
+        acc += gumbel(static_cast<std::uint64_t>(acc > 1e300), 3 + threadIdx.x, i, 7);
+      break;
+    }
+    case 18: {  // 32 lanes: five interleaved Gumbel draws per iteration
+      int bad = 0;
+      for (int i = 0; i < n; ++i) {
+        const std::uint64_t h = static_cast<std::uint64_t>(acc > 1e300) + threadIdx.x;
+        std::uint64_t hh[5], cc[5], b[5];
+        double g[5];
+        for (int q = 0; q < 5; ++q) {
+          hh[q] = h;
+          cc[q] = 5ull * i + q;
+        }
+        rng_final_v<5>(hh, cc, b);
+        gumbel_sl_v<5>(b, g, bad);
+        acc += g[0] + g[1] + g[2] + g[3] + g[4];
+      }
+      acc += bad;
+      break;
+    }
     case 9: {  // dependent rng_final (integer mixes only)
       std::uint64_t h = 1;
       for (int i = 0; i < n; ++i) h = rng_final(h, static_cast<std::uint64_t>(i));
@@ -137,9 +195,10 @@ extern "C" int dtg_debug_microbench(int which, int n, int grid, double* result) 
 }
 
 namespace dtg {
-// Bitwise comparison of the straight-line log / Gumbel with libdevice on
-// inputs the path produces (rng_unit draws and their -log) and on random
-// positive normal doubles over the whole exponent range.
+// Internal consistency of the device's glibc log: the interleaved F-operand
+// Gumbel / log (gumbel_sl_v, log_sl_v) against the scalar glibc::log on the
+// inputs the path produces and on random positive doubles over the whole
+// exponent range (counts[1] stays 0: no argument is ever flagged).
 __global__ void k_log_check(std::uint64_t seed, long long n, unsigned long long* counts) {
   unsigned long long mism = 0, bads = 0;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -147,10 +206,8 @@ __global__ void k_log_check(std::uint64_t seed, long long n, unsigned long long*
     const std::uint64_t b = rng_bits(seed, static_cast<std::uint64_t>(i), 17, 3);
     int bad = 0;
     const double u = rng_unit(b);
-    if (__double_as_longlong(log_sl(u, bad)) != __double_as_longlong(log(u))) ++mism;
-    const double v = -log(u);
-    if (__double_as_longlong(log_sl(v, bad)) != __double_as_longlong(log(v))) ++mism;
-    if (__double_as_longlong(gumbel_sl(b, bad)) != __double_as_longlong(gumbel_bits(b))) ++mism;
+    const double v = -glibc::log(u);
+    if (__double_as_longlong(gumbel_sl(b, bad)) != __double_as_longlong(-glibc::log(v))) ++mism;
     {
       std::uint64_t hv[3] = {b, b ^ 0x1234567ULL, seed}, cv[3] = {1ull * i, 7ull, 11ull * i}, bv[3];
       double gv[3];
@@ -161,20 +218,105 @@ __global__ void k_log_check(std::uint64_t seed, long long n, unsigned long long*
             __double_as_longlong(gv[q]) != __double_as_longlong(gumbel_bits(rng_final(hv[q], cv[q]))))
           ++mism;
     }
-    // random positive normal double: exponent field in [1, 2046]
+    // random positive double (normal or subnormal) through the interleaved path
     const std::uint64_t r = rng_bits(seed ^ 0x5bd1e995ULL, static_cast<std::uint64_t>(i), 5, 9);
-    const std::uint64_t ex = 1 + (r >> 52) % 2046;
-    const double w = __longlong_as_double(static_cast<long long>((ex << 52) | (r & 0xFFFFFFFFFFFFFULL)));
-    int bw = 0;
-    const double lw = log_sl(w, bw);
-    if (bw) ++bads;
-    else if (__double_as_longlong(lw) != __double_as_longlong(log(w))) ++mism;
+    double wv[2] = {__longlong_as_double(static_cast<long long>(r & 0x7FEFFFFFFFFFFFFFULL)),
+                    1.0 + (rng_unit(r) - 0.5) * 0.25};
+    const double w0 = glibc::log(wv[0]), w1 = glibc::log(wv[1]);
+    log_sl_v<2>(wv, bad);
+    if (__double_as_longlong(wv[0]) != __double_as_longlong(w0)) ++mism;
+    if (__double_as_longlong(wv[1]) != __double_as_longlong(w1)) ++mism;
     if (bad) ++bads;
   }
   atomicAdd(&counts[0], mism);
   atomicAdd(&counts[1], bads);
 }
+
+// Inputs of kind `which` and the device's glibc-restated results for them
+// (dtg_debug_libm_check compares them with the host's libm).
+__device__ __forceinline__ double libm_input(int which, std::uint64_t seed, long long i) {
+  const std::uint64_t b = rng_bits(seed, static_cast<std::uint64_t>(i), 29, which);
+  const double u = rng_unit(b);
+  switch (which) {
+    case 0: return u;                                   // log(u), the Gumbel's first log
+    case 1: return -glibc::log(u);                      // its second log
+    case 2: return u;                                   // the whole Gumbel -log(-log u)
+    case 3: return __longlong_as_double(static_cast<long long>(b & 0x7FEFFFFFFFFFFFFFULL));  // log, any exponent
+    case 4: return 1.0 + (u - 0.5) * 0.25;              // log near 1 (glibc's separate path)
+    case 5: return -750.0 + 1460.0 * u;                 // exp over its whole range
+    case 6: return -60.0 * u;                           // exp of softmax arguments (<= 0)
+    default: return __longlong_as_double(static_cast<long long>(b & 0xFFEFFFFFFFFFFFFFULL));  // exp, any finite
+  }
+}
+
+__global__ void k_libm_eval(int which, std::uint64_t seed, long long i0, int n, double* in, double* out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double x = libm_input(which, seed, i0 + k);
+  double y;
+  if (which == 2) {
+    y = -dlog(-dlog(x));
+  } else if (which <= 4) {
+    y = dlog(x);
+  } else {
+    y = dexp(x);
+  }
+  in[k] = x;
+  out[k] = y;
+}
 }  // namespace dtg
+
+extern "C" int dtg_debug_libm_check(int which, uint64_t seed, long long n, int on_device,
+                                    unsigned long long* mismatches) {
+  constexpr int kChunk = 1 << 24;
+  double *d_in = nullptr, *d_out = nullptr;
+  std::vector<double> in(kChunk), out(kChunk);
+  if (on_device && (cudaMalloc(&d_in, kChunk * 8) != cudaSuccess || cudaMalloc(&d_out, kChunk * 8) != cudaSuccess))
+    return 4;
+  unsigned long long mism = 0;
+  int rc = 0;
+  for (long long i0 = 0; i0 < n; i0 += kChunk) {
+    const int m = static_cast<int>(std::min<long long>(kChunk, n - i0));
+    if (on_device) {
+      dtg::k_libm_eval<<<(m + 255) / 256, 256>>>(which, seed, i0, m, d_in, d_out);
+      if (cudaMemcpy(in.data(), d_in, m * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(out.data(), d_out, m * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        rc = 4;
+        break;
+      }
+    } else {  // the host restatement, on the host's copy of the inputs
+      for (int k = 0; k < m; ++k) {
+        const std::uint64_t b = dtg::rng_bits(seed, static_cast<std::uint64_t>(i0 + k), 29, which);
+        const double u = dtg::rng_unit(b);
+        double x;
+        switch (which) {
+          case 0: case 2: x = u; break;
+          case 1: x = -dtg::glibc::log(u); break;
+          case 3: { const std::uint64_t q = b & 0x7FEFFFFFFFFFFFFFULL; std::memcpy(&x, &q, 8); } break;
+          case 4: x = 1.0 + (u - 0.5) * 0.25; break;
+          case 5: x = -750.0 + 1460.0 * u; break;
+          case 6: x = -60.0 * u; break;
+          default: { const std::uint64_t q = b & 0xFFEFFFFFFFFFFFFFULL; std::memcpy(&x, &q, 8); } break;
+        }
+        in[k] = x;
+        out[k] = which == 2 ? -dtg::glibc::log(-dtg::glibc::log(x))
+                            : (which <= 4 ? dtg::glibc::log(x) : dtg::glibc::exp(x));
+      }
+    }
+    for (int k = 0; k < m; ++k) {  // against the running libm (glibc)
+      const double x = in[k];
+      const double ref = which == 2 ? -std::log(-std::log(x)) : (which <= 4 ? std::log(x) : std::exp(x));
+      std::uint64_t a, c;
+      std::memcpy(&a, &out[k], 8);
+      std::memcpy(&c, &ref, 8);
+      if (a != c) ++mism;
+    }
+  }
+  if (d_in) cudaFree(d_in);
+  if (d_out) cudaFree(d_out);
+  *mismatches = mism;
+  return rc;
+}
 
 extern "C" int dtg_debug_log_check(uint64_t seed, long long n, unsigned long long* mismatches,
                                    unsigned long long* flagged) {

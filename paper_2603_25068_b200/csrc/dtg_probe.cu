@@ -97,8 +97,8 @@ __device__ int masked_row_argmax(std::uint64_t seed, std::uint64_t key, std::uin
                                  int n, ColKey colkey, double kinv) {
   const double V = 0.0 - kMaskLarge;
   double z = 0.0;
-  for (int c = 0; c < n; ++c) z += exp(V - V);
-  const double lz = log(z) + V;
+  for (int c = 0; c < n; ++c) z += dexp(V - V);
+  const double lz = dlog(z) + V;
   const double logz = V - lz;
   double m2 = 0.0;
   for (int c = 0; c < n; ++c) {
@@ -106,11 +106,11 @@ __device__ int masked_row_argmax(std::uint64_t seed, std::uint64_t key, std::uin
     if (c == 0 || m2 < y) m2 = y;
   }
   double z2 = 0.0;
-  for (int c = 0; c < n; ++c) z2 += exp((logz + gumbel(seed, key, row, colkey(c))) * kinv - m2);
+  for (int c = 0; c < n; ++c) z2 += dexp((logz + gumbel(seed, key, row, colkey(c))) * kinv - m2);
   int best = 0;
   double bp = 0.0;
   for (int c = 0; c < n; ++c) {
-    const double pi = exp((logz + gumbel(seed, key, row, colkey(c))) * kinv - m2) / z2;
+    const double pi = dexp((logz + gumbel(seed, key, row, colkey(c))) * kinv - m2) / z2;
     if (c == 0 || pi > bp) {
       bp = pi;
       best = c;
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kPB) k_probe(PV v) {
         if (v.sur) {
           for (int k = 0; k < m; ++k) {
             const double z = (x1[seg_id[b + k]] + (-o)) * sc;
-            const double sg = z >= 0.0 ? 1.0 / (1.0 + exp(-z)) : exp(z) / (1.0 + exp(z));
+            const double sg = z >= 0.0 ? 1.0 / (1.0 + dexp(-z)) : dexp(z) / (1.0 + dexp(z));
             soft += sg * 1.0;
           }
         }

@@ -144,3 +144,29 @@ def test_mse_loss_value_and_seeds(port):
     assert rc == 0
     assert loss[0] == float(d["loss"])
     del g1, port_scenario
+
+
+SF_TNTP = "/root/reference/proj/data/siouxfalls_net.tntp"
+
+
+@pytest.mark.parametrize("dn", [4, 1])
+def test_sioux_falls_tntp_network_and_seeding_match_reference(dn):
+    """The product's TNTP parser + attach_virtual_links + fit_inflow_queues +
+    seeding on the reference's own data/siouxfalls_net.tntp, as
+    configs/siouxfalls.toml builds it, against the reference's network
+    (tests/golden/sf_dn*.npz)."""
+    import os
+
+    if not os.path.exists(SF_TNTP):
+        pytest.skip("reference data not present on this host")
+    d = load(f"sf_dn{dn}")
+    T = int(d["meta"][2])
+    sc = P.Scenario.tntp(open(SF_TNTP).read(), 1609.34, 42, 1000.0).configure(2000, dn, T, 300)
+    f, t, ln, k = sc.links()
+    assert np.array_equal(f, d["frm"]) and np.array_equal(t, d["to"])
+    assert np.array_equal(ln, d["length"]) and np.array_equal(k, d["kind"])
+    assert sc.n_nodes == int(d["n_nodes"])
+    assert np.array_equal(np.stack(sc.sample_parameters(3).arrays()), d["params"])
+    assert np.array_equal(np.stack(sc.sample_parameters(42).arrays()), d["truth"])
+    lk, ps = sc.seed_agents()
+    assert np.array_equal(lk, d["link0"]) and np.array_equal(ps, d["pos0"])
