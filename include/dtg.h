@@ -73,6 +73,11 @@ typedef struct dtg_ctx dtg_ctx;
 int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg,
                int n_agents, int n_scenarios, int max_steps, dtg_ctx** out);
 void dtg_destroy(dtg_ctx* ctx);
+/* Optional: initialise the CUDA runtime on the current device and load the
+ * engine's default kernels now (CUDA does both lazily: context creation on
+ * the first call, each module on its kernel's first launch, ~0.2 s together),
+ * so a long-running caller does not charge them to its first request. */
+int dtg_init(void);
 /* Last error message of this context (or of the failed dtg_create when
  * ctx == NULL). */
 const char* dtg_last_error(const dtg_ctx* ctx);

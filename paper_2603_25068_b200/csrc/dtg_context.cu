@@ -37,13 +37,49 @@ struct Unsupported : std::runtime_error {
       throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));        \
   } while (0)
 
+// The stream the running C-ABI call's buffer (re)allocations are ordered on:
+// inside a call on a context (guarded), its stream.  Buffers then come from
+// the stream-ordered allocator (cudaMallocAsync / cudaFreeAsync on the
+// device's default pool, kept reserved: see reserve_pool) -- growing a
+// context for a longer horizon or more agents costs neither an implicit
+// device synchronisation (cudaFree) nor an OS round trip.  Outside a call
+// (context destruction) buffers are freed synchronously.
+thread_local cudaStream_t* tl_alloc_stream = nullptr;
+struct AllocScope {
+  cudaStream_t* prev;
+  explicit AllocScope(cudaStream_t* s) : prev(tl_alloc_stream) { tl_alloc_stream = s; }
+  ~AllocScope() { tl_alloc_stream = prev; }
+};
+
+// Keep freed pool memory reserved for reuse instead of returning it to the
+// OS at every synchronisation (the pool's default release threshold is 0).
+void reserve_pool() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    std::uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   std::size_t n = 0;
+  bool pooled = false;
   void alloc(std::size_t count) {
     release();
-    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    if (count) {
+      if (tl_alloc_stream) {
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), *tl_alloc_stream));
+        pooled = true;
+      } else {
+        CK(cudaMalloc(&p, count * sizeof(T)));
+      }
+    }
     n = count;
   }
   bool ensure(std::size_t count) {
@@ -52,9 +88,16 @@ struct DevBuf {
     return true;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      // stream-ordered after the work already queued on the context's stream
+      if (pooled && tl_alloc_stream)
+        cudaFreeAsync(p, *tl_alloc_stream);
+      else
+        cudaFree(p);
+    }
     p = nullptr;
     n = 0;
+    pooled = false;
   }
   ~DevBuf() { release(); }
 };
@@ -350,6 +393,7 @@ int fail(dtg_ctx* c, int code, const std::string& msg) {
 
 template <class F>
 int guarded(dtg_ctx* c, F&& f) {
+  AllocScope scope(c ? &c->stream : tl_alloc_stream);
   try {
     f();
     return DTG_OK;
@@ -431,6 +475,8 @@ int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
     c->cfg = *cfg;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
+    reserve_pool();
+    AllocScope scope(&c->stream);  // the context's buffers come from the pool
     // CSR + predecessor CSR with the successor position of each edge
     std::vector<int> so(net->succ_off, net->succ_off + L + 1);
     const int E = so[L];
@@ -539,7 +585,10 @@ int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
   return DTG_OK;
 }
 
-void dtg_destroy(dtg_ctx* c) { delete c; }
+void dtg_destroy(dtg_ctx* c) {
+  AllocScope sync_free(nullptr);  // outside any call: free synchronously
+  delete c;
+}
 
 const char* dtg_last_error(const dtg_ctx* c) {
   return c ? c->err.c_str() : g_create_error.c_str();
@@ -556,6 +605,31 @@ int dtg_set_stream(dtg_ctx* c, void* s) {
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->drop_graphs();
   });
+}
+
+int dtg_init(void) {
+  // CUDA creates the context and loads modules lazily, on the first API call
+  // and each kernel's first launch; a 3-link chain with two agents, forward
+  // with checkpoints and the reverse sweep, touches the default schedules.
+  if (cudaFree(nullptr) != cudaSuccess) return DTG_ERR_CUDA;
+  const int succ_off[4] = {0, 1, 2, 2};
+  const int succ[2] = {1, 2};
+  const double len[3] = {100.0, 100.0, 400.0};
+  const dtg_net_desc nd{3, succ_off, succ, len};
+  const dtg_sim_config sc{1, 1.0, 99999.0, 0.01, 1};
+  dtg_ctx* c = nullptr;
+  int rc = dtg_create(&nd, &sc, 2, 1, 4, &c);
+  if (rc != DTG_OK) return rc;
+  const double u[3] = {16, 16, 16}, k[3] = {0.2, 0.2, 0.2}, one[3] = {1, 1, 1};
+  const int link[2] = {0, 0};
+  const double pos[2] = {90.0, 50.0};
+  double g[15];
+  if ((rc = dtg_set_params(c, -1, u, k, one, one, one)) == DTG_OK &&
+      (rc = dtg_set_state(c, -1, link, pos)) == DTG_OK && (rc = dtg_set_noise(c, -1, 1, 0)) == DTG_OK &&
+      (rc = dtg_forward(c, 4, 2, 1)) == DTG_OK)
+    rc = dtg_backward(c, nullptr, nullptr, nullptr, g);
+  dtg_destroy(c);
+  return rc;
 }
 
 int dtg_get_stream(const dtg_ctx* c, void** stream, int* owned) {
