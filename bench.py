@@ -216,6 +216,18 @@ def cpu_reference_rtf(max_samples=1, use_ref=True):
     return SIM_SECONDS / w, "port", f"C3 1-h forward of the C port on 1 core ({w:.2f} s)", w / T_STEPS, 0.0
 
 
+def decision_count():
+    """Decisions the fast rules handed to the exact softmax evaluation since the
+    last call (dtg_debug_decisions; resets the device counter)."""
+    import ctypes as C
+
+    import paper_2603_25068_b200 as P
+
+    n = C.c_ulonglong()
+    P.load().dtg_debug_decisions(-1, C.byref(n))
+    return int(n.value)
+
+
 # ---- distributed helpers ---------------------------------------------------------------
 def dist_setup(n_gpus):
     import torch
@@ -279,6 +291,7 @@ def run_ours(args):
     for _ in range(max(3, args.warmup)):
         eng.forward(T_STEPS, SPI, checkpoint=False)
     eng.sync()
+    exact_decisions = decision_count()  # resets the device counter
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -302,6 +315,7 @@ def run_ours(args):
         clk.under_load(more)
     barrier(world)
     eng.sync()
+    exact_decisions = decision_count()  # during the timed and the sampler's extra runs
     launches_per_step = eng.last_launches
     dev_s = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / 1e3
     dev_s = max_over_ranks(dev_s, world)
@@ -388,6 +402,11 @@ def run_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "exact_decisions": {"count": exact_decisions,
+                                "note": "link-choice / merge decisions the fast argmax rules handed to the "
+                                        "exact two-stage softmax (near ties within 2^-40 / the merge rounding "
+                                        "bound) during the timed region; exp/log are glibc-identical on the "
+                                        "device, so choices are bit-exact either way"},
             "gradient": grad,
             "control": control,
             "batched_throughput": throughput,

@@ -159,6 +159,13 @@ int dtg_sync(dtg_ctx* ctx);
  * the first arrived agent (normally used only on near ties). */
 int dtg_debug_force_slow_path(dtg_ctx* ctx, int on);
 
+/* Decision instrumentation (process-wide, all contexts on the device): returns
+ * how many link-choice / merge decisions since the last call the fast rules
+ * handed to the exact softmax evaluation (second-stage near ties within
+ * 2^-40, merge winners inside the rounding bound) and resets the count;
+ * force_exact 1 sends every decision to the exact evaluation, 0 restores the
+ * fast rules, -1 leaves the setting.  Results are identical either way. */
+int dtg_debug_decisions(int force_exact, unsigned long long* exact_decisions);
 /* Test hook: n Gumbel draws -log(-log(u)), u = uniform(seed, key, rows[i],
  * cols[i]), computed by the device code path (libdevice log). */
 int dtg_debug_gumbel(uint64_t seed, uint64_t key, int n, const uint64_t* rows,
@@ -196,6 +203,18 @@ int dtg_read_cum(dtg_ctx* ctx, int scenario, double* cum_per_step);
 int dtg_read_cum_all(dtg_ctx* ctx, double* cum_per_step);
 int dtg_read_state(dtg_ctx* ctx, int scenario, int step, int* link,
                    double* pos);
+/* Transfer events (travel times).  With recording on, every
+ * forward stores the agent admitted to each link at each step ([T][B][L],
+ * 4 B per link-step, written by the merge).  dtg_read_transfers: [T][L]
+ * admitted agent ids (-1: none) of one scenario of the last forward;
+ * dtg_transfer_events: its link changes as rows (step, agent, from, to),
+ * step-major then ascending agent (the agent is on `to` after engine step
+ * `step`), `from` tracked from the scenario's dtg_set_state links; events
+ * NULL / cap too small: *n_events is the count only. */
+int dtg_set_record_transfers(dtg_ctx* ctx, int on);
+int dtg_read_transfers(dtg_ctx* ctx, int scenario, int* winners);
+int dtg_transfer_events(dtg_ctx* ctx, int scenario, int* events, size_t cap,
+                        size_t* n_events);
 /* Number of observation snapshots of the last forward. */
 int dtg_n_snapshots(const dtg_ctx* ctx);
 
@@ -302,6 +321,9 @@ int dtg_scenario_seed_agents(const dtg_scenario* sc, int* link, double* pos);
 /* steps_for_minutes (engine.cpp:149-154); -1 on error. */
 int dtg_steps_for_minutes(int delta_n, double tau, double minutes);
 
+/* Scenario::record_transfers: level-2 forwards record transfer events (read
+ * them with dtg_transfer_events on dtg_scenario_ctx(sc), draw d = scenario d). */
+int dtg_scenario_set_record_transfers(dtg_scenario* sc, int on);
 /* simulate_forward for n_draws noise iterations of one scenario (draw d uses
  * noise_iterations[d]; scenario-major outputs).  cum_per_step [D][T][L],
  * link_final/pos_final [D][N]; states_link/states_pos [D][T][N] optional

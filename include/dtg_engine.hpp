@@ -120,6 +120,10 @@ struct Scenario {
   /// the re-seeding and upload.  0 (default): always upload.  The level-2
   /// C-ABI assigns a fresh key whenever a scenario is created or reconfigured.
   std::uint64_t state_key = 0;
+  /// Record every transfer of a forward run (Trajectory::transfers): travel
+  /// times.  The reference has no such output; it is derived from its
+  /// per-step states (SURVEY.md §8a "Travel times").
+  bool record_transfers = false;
   int n_agents() const;
 };
 
@@ -146,6 +150,20 @@ struct CompactState {
   std::vector<double> pos;
 };
 
+/// One link change: `agent` leaves `from` and is on `to` (at position 0)
+/// after engine step `step` (0-based).  Within a step, ascending agent id.
+struct TransferEvent {
+  int step = 0, agent = 0, from = 0, to = 0;
+};
+
+/// Per-agent link entries and link traversal times from transfer events:
+/// entry step -1 is the initial link; exit -1: still on the link at the end.
+struct LinkVisit {
+  int agent = 0, link = 0, entry_step = -1, exit_step = -1;
+};
+std::vector<LinkVisit> link_visits(const std::vector<int>& initial_link,
+                                   const std::vector<TransferEvent>& transfers);
+
 struct Trajectory {
   int steps = 0;
   std::vector<std::vector<double>> cum_per_step;  // agent units, per link
@@ -154,6 +172,7 @@ struct Trajectory {
   std::vector<double> cum_final;
   double wall_seconds = 0.0;
   std::uint64_t branch_hash = 0xcbf29ce484222325ULL;  // BranchTrace::h (engine.cpp:251)
+  std::vector<TransferEvent> transfers;  // Scenario::record_transfers
 };
 
 Trajectory simulate_forward(const Scenario& s, const LinkParams& params,

@@ -22,11 +22,13 @@ from .engine import (  # noqa: F401
     Scenario,
     Trajectory,
     calibrate,
+    link_visits,
     optimize_control,
     simulate_forward,
     simulate_gradient,
     simulate_gradient_mse,
     steps_for_minutes,
+    transfer_events,
 )
 
 __version__ = "0.1.0"

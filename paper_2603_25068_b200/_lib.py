@@ -108,6 +108,10 @@ SIGNATURES = [
     ("dtg_read_cum_all", i32, [vp, _dp]),
     ("dtg_read_state", i32, [vp, i32, i32, _ip, _dp]),
     ("dtg_n_snapshots", i32, [vp]),
+    ("dtg_set_record_transfers", i32, [vp, i32]),
+    ("dtg_read_transfers", i32, [vp, i32, _ip]),
+    ("dtg_transfer_events", i32, [vp, i32, vp, C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("dtg_scenario_set_record_transfers", i32, [vp, i32]),
     ("dtg_backward", i32, [vp, vp, vp, vp, _dp]),
     ("dtg_backward_device", i32, [vp, vp, vp, vp, vp]),
     ("dtg_set_loss_mse", i32, [vp, i32, i32, _ip, _dp]),
@@ -153,6 +157,7 @@ SIGNATURES = [
     ("dtg_scenario_ctx", vp, [vp]),
     ("dtg_mse_loss", i32, [i32, i32, _dp, i32, _ip, i32, _dp, i32, _dp, _dp]),
     ("dtg_debug_gumbel", i32, [u64, u64, i32, _u64p, _u64p, _dp]),
+    ("dtg_debug_decisions", i32, [i32, C.POINTER(C.c_ulonglong)]),
     ("dtg_debug_microbench", i32, [i32, i32, i32, _dp]),
     ("dtg_debug_log_check", i32, [u64, C.c_longlong, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     ("dtg_debug_libm_check", i32, [i32, u64, C.c_longlong, i32, C.POINTER(C.c_ulonglong)]),

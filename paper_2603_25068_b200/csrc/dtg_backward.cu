@@ -985,3 +985,7 @@ cudaError_t launch_backward_persistent(const BView& V, int grid, cudaStream_t st
 }
 
 }  // namespace dtg
+
+namespace dtg {
+cudaError_t decision_stats_backward(int force, unsigned long long* count) { return decision_stats_tu(force, count); }
+}  // namespace dtg

@@ -19,6 +19,12 @@
 #include "dtg_backward.h"
 #include "dtg_loss.h"
 
+namespace dtg {
+cudaError_t decision_stats_fused(int force, unsigned long long* count);
+cudaError_t decision_stats_backward(int force, unsigned long long* count);
+cudaError_t decision_stats_kernels(int force, unsigned long long* count);
+}  // namespace dtg
+
 namespace {
 
 thread_local std::string g_create_error;
@@ -122,6 +128,12 @@ struct dtg_ctx {
   DevBuf<std::uint64_t> seeds;  // [2][B]
   std::vector<std::uint64_t> h_seeds;
   std::vector<char> have_params, have_state;
+  // transfer events (dtg_set_record_transfers): admitted agent per link and
+  // step of the last forward, and each scenario's initial link per agent
+  bool rec_transfers = false;
+  DevBuf<int> ev;
+  int ev_T = -1;
+  std::vector<std::vector<int>> h_link0;
   // initial state
   DevBuf<double> pos0, q0;
   DevBuf<int> aid0, lnk0, off0;
@@ -270,6 +282,7 @@ struct dtg_ctx {
     d.cu = cu.p;
     d.cg = cg.p;
     d.grads = grads.p;
+    d.ev = rec_transfers ? ev.p : nullptr;
     return d;
   }
 
@@ -339,6 +352,8 @@ struct dtg_ctx {
     const int s_need = ckpt ? T + 1 : 2;
     const int h_need = T + 1;
     bool realloc = false;
+    if (rec_transfers && ev.ensure(static_cast<std::size_t>(std::max(T, 1)) * B * L)) realloc = true;
+    ev_T = rec_transfers ? T : -1;
     if (s_need > S) {
       const std::size_t BN = static_cast<std::size_t>(B) * N;
       pos.alloc(BN * s_need);
@@ -534,6 +549,7 @@ int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
     c->h_seeds.assign(2 * B, 0);
     c->have_params.assign(B, 0);
     c->have_state.assign(B, 0);
+    c->h_link0.assign(B, {});
     for (int b = 0; b < c->B; ++b) {  // default noise: RngStream(0), iteration 0
       const std::uint64_t it = dtg::rng_fork(dtg::rng_fork(0, dtg::lane::kIteration), 0);
       c->h_seeds[b] = dtg::rng_fork(it, dtg::lane::kGumbelLink);
@@ -630,6 +646,70 @@ int dtg_init(void) {
     rc = dtg_backward(c, nullptr, nullptr, nullptr, g);
   dtg_destroy(c);
   return rc;
+}
+
+int dtg_debug_decisions(int force_exact, unsigned long long* exact_decisions) {
+  unsigned long long total = 0;
+  for (auto fn : {dtg::decision_stats_fused, dtg::decision_stats_backward, dtg::decision_stats_kernels}) {
+    unsigned long long n = 0;
+    if (fn(force_exact, &n) != cudaSuccess) return DTG_ERR_CUDA;
+    total += n;
+  }
+  if (exact_decisions) *exact_decisions = total;
+  return DTG_OK;
+}
+
+int dtg_set_record_transfers(dtg_ctx* c, int on) {
+  return guarded(c, [&] {
+    CK(cudaStreamSynchronize(c->stream));
+    c->rec_transfers = on != 0;
+    c->drop_graphs();  // the step graph captured the event pointer (or its absence)
+  });
+}
+
+int dtg_read_transfers(dtg_ctx* c, int scenario, int* winners) {
+  return guarded(c, [&] {
+    if (scenario < 0 || scenario >= c->B) throw std::invalid_argument("scenario index out of range");
+    if (c->ev_T < 0 || c->ev_T != c->last_T)
+      throw std::runtime_error("the last forward did not record transfers (dtg_set_record_transfers)");
+    c->sync_check();
+    const std::size_t L = c->L;
+    if (c->ev_T)
+      CK(cudaMemcpy2D(winners, L * 4, c->ev.p + scenario * L, static_cast<std::size_t>(c->B) * L * 4, L * 4,
+                      c->ev_T, cudaMemcpyDeviceToHost));
+  });
+}
+
+int dtg_transfer_events(dtg_ctx* c, int scenario, int* events, size_t cap, size_t* n_events) {
+  return guarded(c, [&] {
+    if (scenario < 0 || scenario >= c->B) throw std::invalid_argument("scenario index out of range");
+    const int T = c->ev_T, L = c->L;
+    std::vector<int> win(static_cast<std::size_t>(std::max(T, 0)) * L);
+    const int rc = dtg_read_transfers(c, scenario, win.data());
+    if (rc != DTG_OK) throw std::runtime_error(c->err);
+    std::vector<int> cur = c->h_link0[scenario];
+    std::size_t n = 0;
+    std::vector<std::pair<int, int>> step;  // (agent, to) of one step, ascending agent
+    for (int t = 0; t < T; ++t) {
+      step.clear();
+      for (int i = 0; i < L; ++i) {
+        const int a = win[static_cast<std::size_t>(t) * L + i];
+        if (a >= 0) step.emplace_back(a, i);
+      }
+      std::sort(step.begin(), step.end());
+      for (const auto& [a, to] : step) {
+        if (events && n < cap) {
+          events[4 * n] = t;
+          events[4 * n + 1] = a;
+          events[4 * n + 2] = cur[a];
+          events[4 * n + 3] = to;
+        }
+        cur[a] = to;
+        ++n;
+      }
+    }
+    *n_events = n;
+  });
 }
 
 int dtg_get_stream(const dtg_ctx* c, void** stream, int* owned) {
@@ -865,6 +945,7 @@ int dtg_set_state(dtg_ctx* c, int scenario, const int* link, const double* pos) 
                          cudaMemcpyHostToDevice, c->stream));
       CK(cudaMemcpyAsync(c->q0.p + b * L, q0.data(), L * 8, cudaMemcpyHostToDevice, c->stream));
       c->have_state[b] = 1;
+      c->h_link0[b].assign(link, link + N);
     }
     CK(cudaStreamSynchronize(c->stream));
   });

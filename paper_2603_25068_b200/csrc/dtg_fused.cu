@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_forward_fused(CView V) {
         const bool vacant = tx > jam;  // vacancy_from_state (node_model.cpp:27-41)
         V.ccnt[bl + i] = 0;
         depn[i] = 0;
-        int w = -1;
+        int w = -1, wa = -1;
         if (vacant && cnt > 0) {
           if (cnt > kClusterCandCap) {
             atomicOr(&d.err[bb], kErrCandOverflow);
@@ -828,6 +828,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_forward_fused(CView V) {
               if (e < cnt && c[e].alpha == 0.0) atomicOr(&d.err[bb], kErrZeroAlpha);
             const Cand cb = pick_cand(c, best);
             w = cb.slot;
+            wa = cb.aid;
             wonc[w] = 1;
             atomicAdd(&depc[cb.link], 1);
           } else {
@@ -850,11 +851,13 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_forward_fused(CView V) {
             }
             const int best = two_softmax<kClusterCandCap>(cnt, v, g, d.kinv, lz, pi);
             w = c[best].slot;
+            wa = c[best].aid;
             wonc[w] = 1;
             atomicAdd(&depc[c[best].link], 1);
           }
         }
         V.win[bl + i] = w;
+        if (d.ev) d.ev[(static_cast<std::size_t>(t) * d.B + bb) * L + i] = wa;
       }
       // threads without a link draw step t+1's decisions of every link's
       // first two agents while the merges run
@@ -997,4 +1000,8 @@ int fused_max_cluster(int L, bool stage_params) {
   return 0;
 }
 
+}  // namespace dtg
+
+namespace dtg {
+cudaError_t decision_stats_fused(int force, unsigned long long* count) { return decision_stats_tu(force, count); }
 }  // namespace dtg

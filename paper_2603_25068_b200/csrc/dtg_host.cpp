@@ -369,6 +369,7 @@ struct CacheEntry {
   // what the context holds, so unchanged inputs are not uploaded again
   std::uint64_t state_key = 0;
   std::vector<double> params;  // [5][L] of the last upload (all scenarios)
+  bool record_transfers = false;
 };
 
 thread_local std::vector<CacheEntry> g_cache;
@@ -469,7 +470,21 @@ Prepared prepare(const Scenario& s, const LinkParams& params, const RngStream& r
     if (e) e->state_key = s.state_key;
   }
   for (int b = 0; b < B; ++b) check(c, dtg_set_noise(c, b, rng.seed(), its[b]));
+  if (e && e->record_transfers != s.record_transfers) {
+    check(c, dtg_set_record_transfers(c, s.record_transfers ? 1 : 0));
+    e->record_transfers = s.record_transfers;
+  }
   return {c, N, L, B, s.horizon_steps, spi};
+}
+
+std::vector<TransferEvent> read_transfers(dtg_ctx* c, int b) {
+  std::size_t n = 0;
+  check(c, dtg_transfer_events(c, b, nullptr, 0, &n));
+  std::vector<int> raw(4 * n);
+  check(c, dtg_transfer_events(c, b, raw.data(), n, &n));
+  std::vector<TransferEvent> ev(n);
+  for (std::size_t k = 0; k < n; ++k) ev[k] = {raw[4 * k], raw[4 * k + 1], raw[4 * k + 2], raw[4 * k + 3]};
+  return ev;
 }
 
 CompactState read_state(dtg_ctx* c, int b, int step, int N) {
@@ -516,6 +531,7 @@ std::vector<Trajectory> simulate_forward_draws(const Scenario& s, const LinkPara
       tr.final_state.link.assign(link.begin() + b * N, link.begin() + (b + 1) * N);
       tr.final_state.pos.assign(pos.begin() + b * N, pos.begin() + (b + 1) * N);
       tr.cum_final = p.T ? tr.cum_per_step.back() : std::vector<double>(p.L, 0.0);
+      if (s.record_transfers) tr.transfers = read_transfers(p.ctx, b);
     }
     const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
     for (auto& tr : out) tr.wall_seconds = wall;
@@ -531,6 +547,7 @@ std::vector<Trajectory> simulate_forward_draws(const Scenario& s, const LinkPara
     tr.cum_final = p.T ? tr.cum_per_step.back() : std::vector<double>(p.L, 0.0);
     if (record_states)
       for (int t = 1; t <= p.T; ++t) tr.states.push_back(read_state(p.ctx, b, t, p.N));
+    if (s.record_transfers) tr.transfers = read_transfers(p.ctx, b);
   }
   const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
   for (auto& tr : out) tr.wall_seconds = wall;
@@ -630,6 +647,25 @@ GradResult simulate_gradient(const Scenario& s, const LinkParams& params, const 
   GradResult g = std::move(simulate_gradient_draws(hard, params, rng, builder, {opt.noise_iteration})[0]);
   g.branch_hash = detail::gradient_instrumentation(s, params, rng, opt, g.cum_final_values);
   return g;
+}
+
+std::vector<LinkVisit> link_visits(const std::vector<int>& initial_link,
+                                   const std::vector<TransferEvent>& transfers) {
+  std::vector<LinkVisit> out;
+  std::vector<int> open(initial_link.size(), -1);  // index into out of the agent's current visit
+  for (std::size_t a = 0; a < initial_link.size(); ++a) {
+    if (initial_link[a] < 0) continue;
+    open[a] = static_cast<int>(out.size());
+    out.push_back({static_cast<int>(a), initial_link[a], -1, -1});
+  }
+  for (const auto& e : transfers) {
+    if (e.agent < 0 || e.agent >= static_cast<int>(open.size()))
+      throw std::runtime_error("transfer event of an unknown agent");
+    if (open[e.agent] >= 0) out[open[e.agent]].exit_step = e.step;
+    open[e.agent] = static_cast<int>(out.size());
+    out.push_back({e.agent, e.to, e.step, -1});
+  }
+  return out;
 }
 
 // ---- losses (host mini-tape restated: values and seeds in the reference's op order)
@@ -1223,6 +1259,10 @@ int dtg_steps_for_minutes(int delta_n, double tau, double minutes) {
   } catch (const std::exception&) {
     return -1;
   }
+}
+
+int dtg_scenario_set_record_transfers(dtg_scenario* sc, int on) {
+  return scn_guard(sc, [&] { sc->s.record_transfers = on != 0; });
 }
 
 int dtg_simulate_forward(dtg_scenario* sc, const double* u, const double* k, const double* b,

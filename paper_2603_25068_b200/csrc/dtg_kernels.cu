@@ -245,7 +245,8 @@ __device__ __forceinline__ int merge_softmax(const DevView& d, int b, int t, int
             v2 = a;
           }
         }
-      if (small && d.kinv <= 100.0 && (nc == 1 || (v1 - v2) * d.kinv > 1e-9)) return best;
+      if (!g_force_exact && small && d.kinv <= 100.0 && (nc == 1 || (v1 - v2) * d.kinv > 1e-9)) return best;
+      if (!g_force_exact) atomicAdd(&g_exact_decisions, 1ULL);
     }
     double m = v[0];
 #pragma unroll
@@ -289,17 +290,20 @@ __global__ void __launch_bounds__(128) k_step_merge(DevView d, int t, int s_cur,
   }
   const bool vacant = tx > d.jam[bl + i];
   d.vac[bl + i] = vacant;
-  int w = -1;
+  int w = -1, wa = -1;
   if (vacant) {
     int cid[kMaxCand], cslot[kMaxCand], clink[kMaxCand];
     const int nc = gather_candidates(d, b, i, off, so, cid, cslot, clink);
     if (nc) {
       double lz[kMaxCand], pi[kMaxCand];
-      w = cslot[merge_softmax(d, b, t, i, nc, cid, clink, lz, pi, false)];
+      const int best = merge_softmax(d, b, t, i, nc, cid, clink, lz, pi, false);
+      w = cslot[best];
+      wa = cid[best];
       d.won[static_cast<std::size_t>(b) * d.N + w] = 1;
     }
   }
   d.win[bl + i] = w;
+  if (!replay && d.ev) d.ev[(static_cast<std::size_t>(t) * d.B + b) * d.L + i] = wa;
 }
 
 // Block-wide exclusive scan of one int per thread (blockDim.x == 1024).
@@ -1011,4 +1015,8 @@ void launch_derive(const DevView& d, double* jam, double* dxf, double* pref,
   k_derive<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, jam, dxf, pref);
 }
 
+}  // namespace dtg
+
+namespace dtg {
+cudaError_t decision_stats_kernels(int force, unsigned long long* count) { return decision_stats_tu(force, count); }
 }  // namespace dtg

@@ -71,7 +71,8 @@ __device__ __forceinline__ int merge_softmax_fast(int cnt, const Cand* src, doub
           v2 = v;
         }
       }
-    if (small && kinv <= 100.0 && (cnt == 1 || (v1 - v2) * kinv > kGap)) return best;
+    if (!g_force_exact && small && kinv <= 100.0 && (cnt == 1 || (v1 - v2) * kinv > kGap)) return best;
+    if (!g_force_exact) atomicAdd(&g_exact_decisions, 1ULL);
   }
   double m = c[0].alpha;
 #pragma unroll

@@ -52,6 +52,7 @@ class Trajectory:
     wall_seconds: float = 0.0
     states_link: Optional[np.ndarray] = None  # [T, N]
     states_pos: Optional[np.ndarray] = None
+    transfers: Optional[np.ndarray] = None  # [E, 4] (step, agent, from, to); record_transfers
 
     @property
     def steps(self) -> int:
@@ -200,10 +201,54 @@ def _its(noise_iteration, noise_iterations):
     return np.ascontiguousarray(its, dtype=np.uint64)
 
 
+def transfer_events(ctx, scenario: int = 0) -> np.ndarray:
+    """(step, agent, from, to) rows of the last recorded forward of a device
+    context (dtg_transfer_events)."""
+    lib = load()
+    n = C.c_size_t()
+    raise_for(lib.dtg_transfer_events(ctx, scenario, None, 0, C.byref(n)), lib.dtg_last_error(ctx).decode())
+    out = np.zeros((max(n.value, 1), 4), np.int32)
+    raise_for(lib.dtg_transfer_events(ctx, scenario, out.ctypes.data, n.value, C.byref(n)),
+              lib.dtg_last_error(ctx).decode())
+    return out[: n.value]
+
+
+def link_visits(link0, transfers) -> np.ndarray:
+    """Per-agent link visits [V, 4] = (agent, link, entry_step, exit_step) from
+    the initial links and the transfer events; entry -1 = the initial link,
+    exit -1 = still on the link at the horizon.  A completed visit's travel
+    time is (exit_step - entry_step) engine steps of dt = tau * delta_n
+    seconds."""
+    rows, open_ = [], {}
+    for a, l in enumerate(np.asarray(link0)):
+        if l >= 0:
+            open_[a] = len(rows)
+            rows.append([a, int(l), -1, -1])
+    for t, a, _frm, to in np.asarray(transfers).reshape(-1, 4):
+        if a in open_:
+            rows[open_[a]][3] = int(t)
+        open_[int(a)] = len(rows)
+        rows.append([int(a), int(to), int(t), -1])
+    return np.array(rows, np.int32).reshape(-1, 4)
+
+
 def simulate_forward(sc: Scenario, params: LinkParams, seed: int, noise_iteration: int = 0,
-                     record_states: bool = False, noise_iterations: Optional[Sequence[int]] = None):
+                     record_states: bool = False, noise_iterations: Optional[Sequence[int]] = None,
+                     record_transfers: bool = False):
     """simulate_forward (engine.cpp:227-254) on the GPU.  With noise_iterations,
-    all draws run batched in one device pass and a list is returned."""
+    all draws run batched in one device pass and a list is returned.
+    record_transfers: every link change of every agent, recorded by the
+    device merge (Trajectory.transfers; travel times via link_visits)."""
+    if record_transfers:
+        sc._check(sc._lib.dtg_scenario_set_record_transfers(sc._h, 1))
+        try:
+            out = simulate_forward(sc, params, seed, noise_iteration, record_states, noise_iterations)
+            ctx = sc.device_context()
+            for d, tr in enumerate(out if isinstance(out, list) else [out]):
+                tr.transfers = transfer_events(ctx, d)
+            return out
+        finally:
+            sc._check(sc._lib.dtg_scenario_set_record_transfers(sc._h, 0))
     its = _its(noise_iteration, noise_iterations)
     D, T, L, N = len(its), sc.horizon_steps, sc.n_links, sc.n_agents
     cum = np.empty((D, T, L))  # every entry is written by the call

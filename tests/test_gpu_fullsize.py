@@ -273,3 +273,52 @@ def test_sioux_falls_gradient_against_reference(dn):
     loss, grads = P.simulate_gradient_mse(sc, p, 42, d["obs_ids"], d["obs"], noise_iterations=[1])
     assert loss[0] == pytest.approx(float(d["loss"]), rel=LOSS_RTOL)
     grads_close(grads[0], d["grads"])
+
+
+# ---- travel times: transfer events from the device merge -----------------------------------
+def test_c1_transfer_events_against_reference():
+    """Every agent's link changes over the C1 half hour, recorded by the
+    device merge (record_transfers), against the changes in the reference's
+    record_states (tests/golden/c1_travel.npz)."""
+    d = _need("c1_travel")
+    sc = P.Scenario.grid(4, 400.0, 42, 1000.0).configure(1000, 1, 1800, 300)
+    p = sc.sample_parameters(3)
+    tr = P.simulate_forward(sc, p, seed=7, record_transfers=True)
+    assert np.array_equal(tr.transfers, d["events"])
+    lk0, _ = sc.seed_agents()
+    assert np.array_equal(lk0, d["link0"])
+    visits = P.link_visits(lk0, tr.transfers)
+    done = visits[visits[:, 3] >= 0]
+    assert len(done) == len(d["events"])  # every transfer closes one visit
+    assert (done[:, 3] > done[:, 2]).all()
+
+
+@pytest.mark.parametrize("dn", [4, 1])
+def test_sioux_falls_transfer_events_against_reference(dn):
+    d = _need(f"sf_dn{dn}")
+    sc = sf_scenario(d, int(d["meta"][2]))
+    tr = P.simulate_forward(sc, P.LinkParams(*d["params"]), seed=42, record_transfers=True)
+    assert np.array_equal(tr.transfers, d["events"])
+
+
+@pytest.mark.parametrize("mode", [0, 1, 3])
+def test_c3_transfer_events_every_schedule_against_port(port, mode):
+    """C3 (1,000,020 vehicles, dn=30, 1 h), 8 draws batched: the recorded
+    events equal the link changes of the port's per-step states, on the fused
+    grid, the cluster and the step-graph schedules."""
+    T, B = 120, 8
+    sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 30, T, 300)
+    p = sc.sample_parameters(3)
+    lk0, ps0 = sc.seed_agents()
+    e = P.Engine(sc, B, T)
+    e.set_mode(mode)
+    e.set_params(p)
+    e.set_state(lk0, ps0)
+    for b in range(B):
+        e.set_noise(7, b, b)
+    P.load().dtg_set_record_transfers(e._h, 1)
+    e.forward(T, sc.steps_per_interval)
+    pr = port_of(port, sc)
+    for b in (0, B - 1):
+        ref = pr.forward(p, 7, b, record_states=True)
+        assert np.array_equal(P.transfer_events(e._h, b), events_of(lk0, ref["states_link"]))
