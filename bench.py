@@ -163,44 +163,117 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+def ncu_traffic(kernel, key=None):
+    """Per-launch bytes of `kernel` from the committed ncu captures
+    (profiles/ncu_traffic.json): dram__bytes_read.sum + dram__bytes_write.sum
+    by default, `key` for another counter (e.g. "lts" = lts__t_bytes.sum)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(kernel)
+            return json.load(f).get(kernel if key is None else f"{kernel}:{key}")
     except Exception:
         return None
 
 
+def measured_l2_and_floor(grid):
+    """Builder-measured L2 read bandwidth (64 MiB resident buffer) and the
+    latency floor of a two-barrier persistent step on `grid` CTAs."""
+    import ctypes as C
+
+    import paper_2603_25068_b200 as P
+
+    lib = P.load()
+    bw, fl = C.c_double(), C.c_double()
+    if lib.dtg_debug_l2_bandwidth(64 << 20, 20, C.byref(bw)) != 0:
+        bw.value = float("nan")
+    if lib.dtg_debug_step_floor(grid, 2000, C.byref(fl)) != 0:
+        fl.value = float("nan")
+    return bw.value, fl.value
+
+
 # ---- CPU baseline (the reference build, or the C port) ---------------------------------
-def cpu_reference_rtf(max_samples=1, use_ref=True):
-    """Steady-state real-time factor of the reference on C3: per-step cost from
-    a horizon-0 run (setup only) and horizon-1 runs on one host core."""
-    from oracle.oracle import REF_SO, PortLib, PortScenario, RefLib, RefScenario
+PHASES = (0, 30, 60, 90)  # engine steps into the hour at which the reference's step cost is sampled
+
+
+class RefStepSampler:
+    """Per-step cost of the reference's simulate_forward across the hour.
+
+    The reference's step cost grows as the queued demand spreads over the
+    network (a full C3 hour on the GPU box: 232.8 s against 172.5 s
+    extrapolated from its first step; profiles/r02/ref_full_hour.json), so a
+    step is sampled at each phase t of PHASES: the scenario starts from the
+    compact state at step t (Scenario::custom_init, positions from the C port,
+    which is bit-exact to the reference) and runs 1 step; its setup (seeding
+    and initial counts of that state, a horizon-0 run) is timed separately and
+    subtracted.  The mean over phases is the hour's mean step cost."""
+
+    def __init__(self):
+        from oracle.oracle import PortLib, PortScenario, RefLib, RefScenario
+
+        self.R = RefLib()
+        base = RefScenario.grid(self.R, GRID_N, LINK_LEN, NET_SEED, VIRT_LEN).configure(VEHICLES, DELTA_N, 0, OBS_S)
+        self.p = base.sample_parameters(PARAM_SEED)
+        f, t_, ln, k = base.links()
+        lk, ps = base.seed_agents()
+        port = PortScenario(PortLib(), f, t_, ln, link0=lk, pos0=ps, delta_n=DELTA_N, horizon_steps=max(PHASES),
+                            obs_interval_s=OBS_S)
+        st = port.forward(self.p, SIM_SEED, 0, record_states=True)
+        states = {0: (lk, ps)}
+        for ph in PHASES[1:]:
+            states[ph] = (st["states_link"][ph - 1], st["states_pos"][ph - 1])
+        self.scn = {}
+        for ph in PHASES:
+            pair = []
+            for T in (0, 1):
+                # fitted network first (fit_inflow_queues is skipped once a custom_init is set)
+                sc = RefScenario.from_links(self.R, base.n_nodes, f, t_, ln, k).configure(
+                    VEHICLES, DELTA_N, T, OBS_S, fit=False)
+                lkp, psp = states[ph]
+                self.R.lib.ref_scenario_custom_init(sc.h, len(lkp), np.ascontiguousarray(lkp, np.int32),
+                                                    np.ascontiguousarray(psp, np.float64))
+                sc.horizon_steps = T
+                pair.append(sc)
+            self.scn[ph] = pair
+        self.setup = {}
+
+    def warm(self, ph):
+        t = time.perf_counter()
+        self.scn[ph][0].forward(self.p, SIM_SEED, 0)
+        w = time.perf_counter() - t
+        self.setup[ph] = min(w, self.setup.get(ph, w))
+
+    def step(self, ph, i):
+        """Wall time of one engine step from phase ph (setup subtracted)."""
+        if ph not in self.setup:
+            self.warm(ph)
+        t = time.perf_counter()
+        self.scn[ph][1].forward(self.p, SIM_SEED, i)
+        return time.perf_counter() - t - self.setup[ph]
+
+
+def full_hour_record():
+    """The committed full-hour reference run on a GPU box's host (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "ref_full_hour.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def cpu_reference_rtf(n_samples=4, use_ref=True):
+    """Real-time factor of the reference on C3, one host core: the mean step
+    cost over the hour (RefStepSampler, one sample per phase)."""
+    from oracle.oracle import REF_SO, PortLib, PortScenario
 
     if use_ref and os.path.exists(REF_SO):
-        R = RefLib()
-        kind = "reference"
-
-        def make(T):
-            return RefScenario.grid(R, GRID_N, LINK_LEN, NET_SEED, VIRT_LEN).configure(VEHICLES, DELTA_N, T, OBS_S)
-
-        s0 = make(0)
-        p = s0.sample_parameters(PARAM_SEED)
-        t = time.perf_counter()
-        s0.forward(p, SIM_SEED, 0)
-        setup = time.perf_counter() - t
-        s1 = make(1)
-        walls = []
-        for i in range(max_samples):
-            t = time.perf_counter()
-            s1.forward(p, SIM_SEED, i)
-            walls.append(time.perf_counter() - t)
-        step = max(1e-9, statistics.mean(walls) - setup)
-        sample = (f"C3 reference simulate_forward: horizon 0 (setup {setup:.2f} s) and {max_samples} x horizon 1 "
-                  f"on 1 core; steady per-step {step:.2f} s (30 simulated s)")
-        return DT / step, kind, sample, step, setup
+        S = RefStepSampler()
+        steps = [S.step(PHASES[i % len(PHASES)], i) for i in range(n_samples)]
+        step = max(1e-9, statistics.mean(steps))
+        setup = statistics.mean(S.setup.values())
+        sample = (f"C3 reference simulate_forward on 1 core: {n_samples} single engine steps started from the "
+                  f"states at steps {list(PHASES)} of the hour (custom_init), setup subtracted; mean step "
+                  f"{step:.2f} s per 30 simulated s")
+        return DT / step, "reference", sample, step, setup
     import paper_2603_25068_b200 as P
 
     PL = PortLib()
@@ -226,6 +299,77 @@ def decision_count():
     n = C.c_ulonglong()
     P.load().dtg_debug_decisions(-1, C.byref(n))
     return int(n.value)
+
+
+def host_info():
+    """The CPU the baselines ran on: nproc and /proc/cpuinfo's model name."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def _ref_grad_worker(horizon):
+    """One reference simulate_gradient (Checkpointed) on C4's scenario with
+    `horizon` steps (0 = setup only: seeding, initial counts, loss tape), loss
+    on cum_final (the sweep's cost does not depend on the loss); prints its
+    wall time."""
+    from oracle.oracle import RefLib, RefScenario
+
+    R = RefLib()
+    sc = RefScenario.grid(R, GRID_N, LINK_LEN, NET_SEED, VIRT_LEN).configure(VEHICLES, DELTA_N, horizon, OBS_S)
+    p = sc.sample_parameters(PARAM_SEED)
+    wc = np.ones(sc.n_links)
+    t = time.perf_counter()
+    sc.gradient(p, SIM_SEED, 1, 1, wc=wc)
+    print(json.dumps({"horizon": horizon, "wall_s": time.perf_counter() - t}), flush=True)
+
+
+def cpu_reference_gradient():
+    """The gradient half of the metric on the CPU: the
+    reference's checkpointed simulate_gradient at C4, K = min(8, nproc)
+    processes at once (one noise draw per core, the way the reference's draw
+    loop would be spread over a host): per process a 0-step run (setup) and a
+    1-step run; steady per-step cost = the difference.  One calibration
+    iteration = ceil(8 / K) rounds of (setup + 60 steps)."""
+    from oracle.oracle import REF_SO
+
+    if not os.path.exists(REF_SO):
+        return None
+    K = max(1, min(CAL_DRAWS, os.cpu_count() or 1))
+    try:  # one C4 gradient process peaks at ~7 GB (dense N x L fp64 tensors): never overcommit the host
+        with open("/proc/meminfo") as f:
+            avail = next(int(ln.split()[1]) for ln in f if ln.startswith("MemAvailable")) * 1024
+        K = max(1, min(K, int(avail // (9 * 2 ** 30))))
+    except (OSError, StopIteration):
+        K = 1
+
+    def wave(h):
+        procs = [subprocess.Popen([sys.executable, os.path.abspath(__file__), "--ref-grad-worker", str(h)],
+                                  stdout=subprocess.PIPE, text=True) for _ in range(K)]
+        walls = []
+        for pr in procs:
+            out, _ = pr.communicate()
+            walls.append(json.loads(out.strip().splitlines()[-1])["wall_s"])
+        return statistics.mean(walls)
+
+    t0 = time.perf_counter()
+    setup = wave(0)
+    one = wave(1)
+    step = max(1e-9, one - setup)
+    T = int(CAL_MIN * 60 / DT)
+    rounds = -(-CAL_DRAWS // K)
+    return {"gradient_s_per_iter": rounds * (setup + T * step), "gradient_step_s": step, "gradient_setup_s": setup,
+            "gradient_processes": K, "gradient_wall_s": time.perf_counter() - t0,
+            "gradient_sample": f"C4 reference simulate_gradient (Checkpointed), {K} processes at once, each a 0-step "
+                               f"and a 1-step run; iteration = {rounds} round(s) of setup + {T} x step for "
+                               f"{CAL_DRAWS} draws"}
 
 
 # ---- distributed helpers ---------------------------------------------------------------
@@ -333,6 +477,8 @@ def run_ours(args):
     achieved = alg_bytes / per_launch_s / 1e9
     phases, grid = eng.profile_persistent(T_STEPS, SPI)
     ker_ms, _ = eng.profile_kernels(T_STEPS, SPI)  # the 5-kernel step-graph schedule, for reference
+    l2_peak, floor_us = measured_l2_and_floor(grid)
+    l2_bytes = ncu_traffic("k_forward_fused", "lts")
     roofline = {"bound": "hbm", "kernel": "k_forward_fused", "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic("k_forward_fused"),
                 "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes,
@@ -340,6 +486,15 @@ def run_ours(args):
                 "phase_us_per_engine_step": {k: round(v, 2) for k, v in phases.items()},
                 "note": "latency-bound: the 1 MB scenario state stays in L2 (ncu dram traffic per launch "
                         "<< algorithmic bytes); per-step time = 2 grid barriers + 2 dependent phases",
+                "l2_bytes": l2_bytes,
+                "l2_peak_GBps": l2_peak,
+                "l2_peak_source": "builder-measured (dtg_debug_l2_bandwidth: 64 MiB L2-resident read)",
+                "l2_frac": (l2_bytes / per_launch_s / 1e9 / l2_peak) if l2_bytes and l2_peak == l2_peak else None,
+                "us_per_step": per_launch_s / T_STEPS * 1e6,
+                "latency_floor_us_per_step": floor_us,
+                "latency_floor_source": "builder-measured (dtg_debug_step_floor: same grid, 2 grid barriers + one "
+                                        "dependent global round trip per phase, no work)",
+                "latency_frac": (floor_us / (per_launch_s / T_STEPS * 1e6)) if floor_us == floor_us else None,
                 "step_graph_kernel_ms_per_nowcast": {k: round(v, 4) for k, v in ker_ms.items()}}
     throughput = run_throughput(P, torch, sc, p, lk0, ps0, args) if world == 1 and not args.no_throughput else None
 
@@ -372,6 +527,32 @@ def run_ours(args):
                    "while the kernel runs, dtg_forward_read); new parameters and noise every call; the scenario's initial state stays resident on the device between calls "
                    "(unchanged scenario)"}
 
+    # the same request with a FRESH scenario every call, as the reference's
+    # simulate_forward rebuilds its state each time: network generation and
+    # queue fitting (host), agent seeding and the initial-state upload are
+    # inside the timed call (the device context for the network is reused)
+    def e2e_fresh_call():
+        nonlocal calls
+        scf = build_scenario(P)
+        its = [(calls + 1) * 1000 + rank * B + b for b in range(B)]
+        P.simulate_forward(scf, p if calls % 2 == 0 else p_alt, seed=SIM_SEED, noise_iterations=its)
+        calls += 1
+
+    e2e_fresh_call()
+    fresh_times = []
+    for _ in range(max(4, args.steps)):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        e2e_fresh_call()
+        fresh_times.append(time.perf_counter() - t)
+    fresh_s = max_over_ranks(statistics.mean(fresh_times), world)
+    e2e["fresh_scenario"] = {
+        "value": world * B * SIM_SECONDS / fresh_s, "unit": UNIT, "s_per_call": fresh_s,
+        "h2d_bytes_per_step": h2d + N * (4 + 8) + (L + 1) * 4 + L * 8,
+        "d2h_bytes_per_step": d2h,
+        "path": "Scenario.grid + configure (host network build, fit_inflow_queues) + simulate_forward: seeding "
+                "and initial-state upload inside every call"}
+
     grad = run_gradient(P, torch, world, rank, args)
     control = run_control(P, torch, world, rank, args)
 
@@ -381,7 +562,13 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             v, kind, sample, step_s, setup = cpu_reference_rtf()
             cpu = {"value": v, "unit": "x real time (1 scenario, 1 core)", "cores": 1, "kind": kind,
-                   "sample": sample, "est_full_hour_s": setup + T_STEPS * step_s}
+                   "sample": sample, "est_full_hour_s": setup + T_STEPS * step_s, **host_info(),
+                   "full_hour_measured": full_hour_record()}
+            g = cpu_reference_gradient()
+            if g:
+                cpu.update(g)
+                if grad:
+                    cpu["gradient_speedup_vs_cpu"] = g["gradient_s_per_iter"] / grad["s_per_iter"]
         out = {
             "metric": METRIC,
             "value": value,
@@ -646,32 +833,18 @@ def run_reference(args):
 
     if not os.path.exists(REF_SO):
         v, kind, sample, step_s, setup = cpu_reference_rtf(use_ref=False)
-        walls = []
     else:
-        R = RefLib()
         kind = "reference"
-
-        def make(T):
-            return RefScenario.grid(R, GRID_N, LINK_LEN, NET_SEED, VIRT_LEN).configure(VEHICLES, DELTA_N, T, OBS_S)
-
-        s0, s1 = make(0), make(1)
-        p = s0.sample_parameters(PARAM_SEED)
-        setups = []
-        for _ in range(max(3, args.warmup)):  # warm-up: setup-only runs (horizon 0)
-            t = time.perf_counter()
-            s0.forward(p, SIM_SEED, 0)
-            setups.append(time.perf_counter() - t)
-        setup = min(setups)
-        walls = []
-        for i in range(args.steps):  # timed: one 30-s engine step each (horizon 1)
-            t = time.perf_counter()
-            s1.forward(p, SIM_SEED, i)
-            walls.append(time.perf_counter() - t)
-        step_s = max(1e-9, statistics.mean(walls) - setup)
+        S = RefStepSampler()
+        for i in range(max(3, args.warmup)):  # warm-up: the phases' setup-only runs (horizon 0)
+            S.warm(PHASES[i % len(PHASES)])
+        walls = [S.step(PHASES[i % len(PHASES)], i) for i in range(args.steps)]  # timed: one engine step each
+        step_s = max(1e-9, statistics.mean(walls))
+        setup = statistics.mean(S.setup.values())
         v = DT / step_s
-        sample = (f"C3 reference simulate_forward, {args.steps} x horizon-1 runs minus the horizon-0 setup "
-                  f"({setup:.2f} s): steady per-step {step_s:.2f} s per 30 simulated s, 1 core "
-                  f"(the reference is single-threaded)")
+        sample = (f"C3 reference simulate_forward, {args.steps} single engine steps started from the states at "
+                  f"steps {list(PHASES)} of the hour in turn (custom_init), each minus that state's horizon-0 "
+                  f"setup: mean step {step_s:.2f} s per 30 simulated s, 1 core (the reference is single-threaded)")
     out = {
         "impl": "reference",
         "metric": METRIC,
@@ -687,10 +860,18 @@ def run_reference(args):
         "dtype": "f64",
         "data": "synthetic (SURVEY §8d grid generator, sampled parameters, seeded demand)",
         "config": config_dict(1, world),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample, **host_info()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "est_full_hour_s": setup + T_STEPS * step_s,
+        "full_hour_measured": full_hour_record(),
     }
+    if not args.no_gradient:
+        g = cpu_reference_gradient()
+        if g:
+            out["cpu_baseline"].update(g)
+            out["gradient"] = {"s_per_iter": g["gradient_s_per_iter"], "draws": CAL_DRAWS,
+                               "steps": int(CAL_MIN * 60 / DT), "processes": g["gradient_processes"],
+                               "projected_200_iter_s": 200 * g["gradient_s_per_iter"]}
     print(json.dumps(out), flush=True)
 
 
@@ -723,7 +904,11 @@ def main():
     ap.add_argument("--no-gradient", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-throughput", action="store_true")
+    ap.add_argument("--ref-grad-worker", type=int, default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.ref_grad_worker is not None:
+        _ref_grad_worker(args.ref_grad_worker)
+        return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         relaunch_under_torchrun(args.gpus)
     if args.impl == "reference":

@@ -175,6 +175,12 @@ int dtg_debug_gumbel(uint64_t seed, uint64_t key, int n, const uint64_t* rows,
  * (which: 0 Gumbel draw, 1 log, 2 exp, 3 division, 4 L2 pointer chase,
  * 5 counter-RNG uniform; 100 = empty grid.sync with `grid` CTAs of 512). */
 int dtg_debug_microbench(int which, int n, int grid, double* result);
+/* Measurement hooks for the roofline (builder-measured, not NVIDIA figures):
+ * L2 read bandwidth over an L2-resident `bytes` buffer, and the time per step
+ * of a persistent grid of `grid` CTAs x 512 doing only the fused forward's two
+ * grid barriers and one dependent global round trip per phase. */
+int dtg_debug_l2_bandwidth(long long bytes, int reps, double* gbps);
+int dtg_debug_step_floor(int grid, int n_steps, double* us_per_step);
 /* Test hook: the device's interleaved glibc log / Gumbel (several draws per
  * chain) against its scalar glibc log on n inputs per kind; mismatches must
  * be 0 and flagged stays 0. */

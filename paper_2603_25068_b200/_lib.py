@@ -159,6 +159,8 @@ SIGNATURES = [
     ("dtg_debug_gumbel", i32, [u64, u64, i32, _u64p, _u64p, _dp]),
     ("dtg_debug_decisions", i32, [i32, C.POINTER(C.c_ulonglong)]),
     ("dtg_debug_microbench", i32, [i32, i32, i32, _dp]),
+    ("dtg_debug_l2_bandwidth", i32, [C.c_longlong, i32, C.POINTER(C.c_double)]),
+    ("dtg_debug_step_floor", i32, [i32, i32, C.POINTER(C.c_double)]),
     ("dtg_debug_log_check", i32, [u64, C.c_longlong, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     ("dtg_debug_libm_check", i32, [i32, u64, C.c_longlong, i32, C.POINTER(C.c_ulonglong)]),
     ("dtg_debug_warp_records", i32, [vp, i32, i32, vp, C.POINTER(C.c_int)]),
@@ -196,6 +198,20 @@ def load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def load_other(path: str) -> C.CDLL:
+    """Measurement only (A/B against another build, scripts/): load `path` in
+    place of the in-tree library; symbols it lacks stay unbound."""
+    global _lib
+    lib = C.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name, None)
+        if fn is not None:
+            fn.restype = res
+            fn.argtypes = args
     _lib = lib
     return lib
 

@@ -165,7 +165,124 @@ __global__ void k_micro_barrier(int n, double* out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = static_cast<double>(t1 - t0) / n;
 }
 
+// L2 read bandwidth: every CTA streams its share of a buffer that fits in L2
+// (16-byte loads, 4 in flight per thread), `reps` passes; the first pass
+// (cold) is excluded by the caller running it twice.
+__global__ void __launch_bounds__(512) k_l2_read(const double2* __restrict__ buf, std::size_t n2, int reps,
+                                                 double* sink) {
+  double acc = 0.0;
+  const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+  for (int r = 0; r < reps; ++r)
+    for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n2; i += 4 * stride) {
+      double2 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = i + q * stride < n2 ? __ldcg(buf + i + q * stride) : make_double2(0, 0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc += v[q].x + v[q].y;
+    }
+  if (acc == 12345.678) *sink = acc;  // keeps the loads
+}
+
+// Latency floor of one persistent engine step: the same grid and barrier as
+// k_forward_fused (release/acquire counter), two barriers per step, and in each
+// phase one dependent global round trip per CTA (thread 0 reads what another
+// CTA wrote in the previous phase) -- a step with no work at all.
+__global__ void __launch_bounds__(512) k_step_floor(unsigned int* ctr, int* cell, int T, unsigned long long* ns) {
+  unsigned int epoch = 0;
+  auto barrier = [&]() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ++epoch;
+      const unsigned int target = epoch * gridDim.x;
+      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
+      unsigned int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      } while (v < target);
+    }
+    __syncthreads();
+  };
+  unsigned long long t0 = 0;
+  if (threadIdx.x == 0 && blockIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  int v = 0;
+  for (int t = 0; t < T; ++t) {
+    if (threadIdx.x == 0) {
+      v += cell[(blockIdx.x + 1 + t) % gridDim.x];
+      cell[blockIdx.x] = v + t;
+    }
+    barrier();
+    if (threadIdx.x == 0) {
+      v += cell[(blockIdx.x + 3 + t) % gridDim.x];
+      cell[gridDim.x + blockIdx.x] = v;
+    }
+    barrier();
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    *ns = t1 - t0;
+  }
+  if (v == 0x7fffffff) cell[0] = v;
+}
+
 }  // namespace dtg
+
+// Builder-measured L2 read bandwidth (GB/s) over a `bytes` buffer resident in
+// L2 (second of two timed launches, CUDA events).
+extern "C" int dtg_debug_l2_bandwidth(long long bytes, int reps, double* gbps) {
+  double2* buf = nullptr;
+  double* sink = nullptr;
+  if (cudaMalloc(&buf, bytes) != cudaSuccess || cudaMalloc(&sink, 8) != cudaSuccess) return 4;
+  cudaMemset(buf, 0, bytes);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const std::size_t n2 = static_cast<std::size_t>(bytes) / 16;
+  float ms = 0.f;
+  for (int pass = 0; pass < 2; ++pass) {
+    cudaEventRecord(e0);
+    dtg::k_l2_read<<<sms * 4, 512>>>(buf, n2, reps, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+  }
+  const cudaError_t e = cudaGetLastError();
+  *gbps = static_cast<double>(bytes) * reps / (ms * 1e-3) / 1e9;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  cudaFree(sink);
+  return e == cudaSuccess ? 0 : 4;
+}
+
+// Builder-measured latency floor of a two-barrier persistent step (us) on
+// `grid` CTAs of 512 threads.
+extern "C" int dtg_debug_step_floor(int grid, int T, double* us_per_step) {
+  unsigned int* ctr = nullptr;
+  int* cell = nullptr;
+  unsigned long long* ns = nullptr;
+  if (cudaMalloc(&ctr, 4) != cudaSuccess || cudaMalloc(&cell, 8 * grid) != cudaSuccess ||
+      cudaMalloc(&ns, 8) != cudaSuccess)
+    return 4;
+  unsigned long long h = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    cudaMemset(ctr, 0, 4);
+    cudaMemset(cell, 0, 8 * grid);
+    void* args[] = {&ctr, &cell, &T, &ns};
+    cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dtg::k_step_floor), dim3(grid), dim3(512), args, 0,
+                                nullptr);
+    cudaMemcpy(&h, ns, 8, cudaMemcpyDeviceToHost);
+  }
+  const cudaError_t e = cudaGetLastError();
+  *us_per_step = static_cast<double>(h) / 1e3 / T;
+  cudaFree(ctr);
+  cudaFree(cell);
+  cudaFree(ns);
+  return e == cudaSuccess ? 0 : 4;
+}
 
 extern "C" int dtg_debug_microbench(int which, int n, int grid, double* result) {
   double* d_out = nullptr;
