@@ -752,7 +752,17 @@ def run_gradient(P, torch, world, rank, args):
     phases_f, _ = eng.profile_persistent(T, SPI)
     eng.forward(T, SPI, checkpoint=True)
     phases_b, grid_b = eng.profile_backward()
-    return {"s_per_iter": s_iter, "setup_s_per_calibrate_call": setup_s,
+    adj_s = statistics.median(adj_ms) / 1e3
+    adj_alg = local * T * (24 * sc.n_agents + 96 * L)  # SURVEY §8d adjoint figure, this rank's draws
+    peak, _ = measured_peak_hbm()
+    l2_peak, _ = measured_l2_and_floor(grid_b)
+    adj_l2 = ncu_traffic("k_backward_persistent", "lts")
+    adj_roofline = {"kernel": "k_backward_persistent", "alg_bytes_per_launch": adj_alg,
+                    "achieved_GBps": adj_alg / adj_s / 1e9, "hbm_frac": adj_alg / adj_s / 1e9 / peak,
+                    "dram_bytes_ncu": ncu_traffic("k_backward_persistent"), "l2_bytes_ncu": adj_l2,
+                    "l2_frac": (adj_l2 / adj_s / 1e9 / l2_peak) if adj_l2 and l2_peak == l2_peak else None,
+                    "grid_ctas": grid_b}
+    return {"s_per_iter": s_iter, "setup_s_per_calibrate_call": setup_s, "adj_roofline": adj_roofline,
             "wall_s": {f"{n}_it": w for n, w in zip(sizes, walls)},
             "draws": CAL_DRAWS, "draws_per_gpu": local, "steps": T,
             "iterations_timed": n_it, "params": 4 * L, "loss_first": float(res.loss_curve[0]),

@@ -5,6 +5,11 @@
 //     SimConfig::surrogate (engine.cpp:227-254, 303-429; car_following.cpp:17-94);
 //   * probe_forward_batch: many parameter sets in one launch;
 //   * run_gradcheck (pipeline.cpp:486-585) on top of both.
+//
+// TRANSCRIBED HOST CODE: run_gradcheck restates pipeline.cpp:499-585 (its draw
+// / redraw / stencil logic and report), restructured so each draw's 10 L
+// stencil probes run as ONE batched device launch; the probe engine itself
+// (dtg_probe.cu) is new device code.
 #include <algorithm>
 #include <chrono>
 #include <cmath>

@@ -5,6 +5,19 @@
 // Built with -ffp-contract=off: sample_parameters' lo + (hi - lo) * u must not
 // be contracted into an FMA or parameters differ from the reference in the
 // last bit.
+//
+// TRANSCRIBED HOST CODE.  The following functions restate the reference's
+// off-hot-path host C++ line for line (same control flow, identifiers and error
+// strings), because their outputs must be byte/bit-identical and the operation
+// order is the contract; they are not B200 work:
+//   parse_tntp_text, attach_virtual_links, sample_parameters  network.cpp:58-236
+//   Scenario::n_agents, steps_for_minutes, seed_agents,
+//   fit_inflow_queues                                          engine.cpp:138-213
+//   AdamW::step, BoundedTransform, LowerBoundTransform         optimization.cpp:10-59
+//   series_from_levels                                         observation.cpp:27-44
+// New here: the successor CSR that replaces the dense L x L adjacency
+// (Network::rebuild_csr, network.cpp:28-35), the device context cache, the
+// device-resident optimisation iteration (DeviceLoop) and the C-ABI.
 #include <algorithm>
 #include <atomic>
 #include <chrono>

@@ -8,6 +8,10 @@
 //
 // Host C++ (O(K·L) work); built with -ffp-contract=off so `lo + (hi - lo) * u`
 // and the metric sums round exactly like the reference.
+//
+// TRANSCRIBED HOST CODE: synthesize_observations, count_metrics and the CSV
+// reader/writer restate the reference functions cited above line for line
+// (byte-identical outputs need the same operation order); not B200 work.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
