@@ -143,12 +143,17 @@ __global__ void __launch_bounds__(128) k_step_choice(DevView d, int t, int s_cur
         const std::uint64_t h2 = rng_prefix2(rng_prefix1(d.seed_link[b], static_cast<std::uint64_t>(t)),
                                              static_cast<std::uint64_t>(agent));
         int sj[kFastSucc];
-        double y[kFastSucc], ex[kFastSucc], gg[kFastSucc];
+        double y[kFastSucc], ex[kFastSucc];
 #pragma unroll
         for (int e = 0; e < kFastSucc; ++e) sj[e] = d.succ[s0 + (e < deg ? e : 0)];
-        gumbel_draws<kFastSucc>(h2, sj, gg);  // the draw chains batched
+        // one scalar draw per successor: this kernel is occupancy-bound (one
+        // thread per link, few of them drawing), which the batched draws'
+        // registers would cost
+        int bad = 0;
 #pragma unroll
-        for (int e = 0; e < kFastSucc; ++e) y[e] = (lz[e < deg ? e : 0] + gg[e]) * d.kinv;
+        for (int e = 0; e < kFastSucc; ++e)
+          y[e] = e < deg ? (lz[e] + gumbel_sl(rng_final(h2, static_cast<std::uint64_t>(sj[e])), bad)) * d.kinv
+                         : 0.0;
         const int best = softmax_first_argmax<kFastSucc>(deg, y, ex);
         c = sj[0];
 #pragma unroll
@@ -216,12 +221,12 @@ __device__ __forceinline__ int merge_softmax(const DevView& d, int b, int t, int
     const std::uint64_t h2 = rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
                                          static_cast<std::uint64_t>(i));
     double v[kFastSucc], y[kFastSucc], ex[kFastSucc];
-    {
-      int key[kFastSucc];
+    // one draw per candidate (most rows have one or two): the scalar chain
+    // keeps this latency-bound kernel's register count, and so its occupancy
+    int bad = 0;
 #pragma unroll
-      for (int e = 0; e < kFastSucc; ++e) key[e] = e < nc ? cid[e] : 0;
-      gumbel_draws<kFastSucc>(h2, key, y);  // the draw chains batched
-    }
+    for (int e = 0; e < kFastSucc; ++e)
+      y[e] = e < nc ? gumbel_sl(rng_final(h2, static_cast<std::uint64_t>(cid[e])), bad) : 0.0;
 #pragma unroll
     for (int e = 0; e < kFastSucc; ++e) {
       v[e] = e < nc ? d.alpha[bl + clink[e]] : 0.0;
