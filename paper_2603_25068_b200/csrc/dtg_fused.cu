@@ -30,6 +30,10 @@
 #include "dtg_device.cuh"
 #include "dtg_merge.cuh"
 
+#ifndef DTG_SCALAR_HEAD_DRAWS
+#define DTG_SCALAR_HEAD_DRAWS 0
+#endif
+
 namespace cg = cooperative_groups;
 
 namespace dtg {
@@ -68,11 +72,18 @@ __device__ __forceinline__ void head_draw(const CView& V, std::uint64_t h1l, std
     double y[kFastDeg], ex[kFastDeg];
 #pragma unroll
     for (int e = 0; e < kFastDeg; ++e) sj[e] = d.succ[sb + (e < deg ? e : 0)];
+#if DTG_SCALAR_HEAD_DRAWS
+    int bad = 0;
+#pragma unroll
+    for (int e = 0; e < kFastDeg; ++e)
+      y[e] = (lz[e < deg ? e : 0] + gumbel_sl(rng_final(h2l, static_cast<std::uint64_t>(sj[e])), bad)) * d.kinv;
+#else
     // the five draw chains batched (dtg_device.cuh gumbel_draws)
     double gg[kFastDeg];
     gumbel_draws<kFastDeg>(h2l, sj, gg);
 #pragma unroll
     for (int e = 0; e < kFastDeg; ++e) y[e] = (lz[e < deg ? e : 0] + gg[e]) * d.kinv;
+#endif
     const int best = softmax_first_argmax<kFastDeg>(deg, y, ex);
     c = sj[best];
   } else {
@@ -142,7 +153,12 @@ __device__ __forceinline__ void spec_segment(const CView& V, std::uint64_t h1l, 
       bb[2 + h] = rng_final(rng_prefix2(h1m, sj), static_cast<std::uint64_t>(a));
     }
     int bad = 0;
+#if DTG_SCALAR_HEAD_DRAWS
+#pragma unroll
+    for (int q = 0; q < 4; ++q) gg[q] = gumbel_sl(bb[q], bad);
+#else
     gumbel_sl_v<4>(bb, gg, bad);
+#endif
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       gm[h] = gg[2 + h];
