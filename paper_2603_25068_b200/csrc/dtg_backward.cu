@@ -35,7 +35,10 @@ namespace dtg {
 
 namespace {
 
-constexpr int kBT = 512;  // threads per CTA
+#ifndef DTG_BWD_THREADS
+#define DTG_BWD_THREADS 512
+#endif
+constexpr int kBT = DTG_BWD_THREADS;  // threads per CTA
 constexpr int kFastDeg = 5;  // successor counts up to this take unrolled register paths
 constexpr int kHeadCap = 1024;  // deferred arrived heads per CTA (overflow runs inline)
 constexpr int kB3 = 2;  // R3 slots per thread in flight
@@ -964,6 +967,8 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
 int backward_smem_bytes(int L, int maxdeg) {
   return (2 * (L + 1) + 2) * 4 + (kBT / 32) * maxdeg * static_cast<int>(sizeof(T2)) + 16 + (4 + 3 * kHeadCap) * 4;
 }
+
+int backward_threads() { return kBT; }
 
 int backward_max_grid(int L, int maxdeg) {
   int dev = 0, sms = 0, occ = 0;

@@ -54,6 +54,7 @@ struct BView {
 };
 
 int backward_smem_bytes(int L, int maxdeg);
+int backward_threads();  // threads per CTA of k_backward_persistent
 int backward_max_grid(int L, int maxdeg);
 cudaError_t launch_backward_persistent(const BView& V, int grid, cudaStream_t st);
 

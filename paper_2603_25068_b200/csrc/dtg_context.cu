@@ -1290,7 +1290,8 @@ int64_t dtg_last_launches(const dtg_ctx* c) { return c->launches; }
 static void run_backward_persistent(dtg_ctx* c, cudaStream_t st) {
   const int T = c->last_T, K = c->last_K, spi = c->last_spi;
   const std::size_t B = c->B, L = c->L, N = c->N, BL = B * L, BN = B * N, MD = c->maxdeg;
-  const int want = (std::max(c->N, c->L) + 511) / 512;
+  const int bt = dtg::backward_threads();
+  const int want = (std::max(c->N, c->L) + bt - 1) / bt;
   int bps, grid;
   if (static_cast<long long>(c->B) * want <= c->bgrid_max) {
     bps = want;

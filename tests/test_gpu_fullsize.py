@@ -322,3 +322,34 @@ def test_c3_transfer_events_every_schedule_against_port(port, mode):
     for b in (0, B - 1):
         ref = pr.forward(p, 7, b, record_states=True)
         assert np.array_equal(P.transfer_events(e._h, b), events_of(lk0, ref["states_link"]))
+
+
+# ---- C3 at the stress sizes ------------------------------------------------------------------
+def test_c3_dn1_300_steps_against_port(port):
+    """C3 at dn=1 (1,000,020 agents), 300 steps (5 min) of every step's counts
+    and the final state against the port (the reference cannot hold N x L =
+    2.55e9 cells)."""
+    from oracle.oracle import fnv1a64_c
+
+    T = 300
+    sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 1, T, 300)
+    p = sc.sample_parameters(3)
+    tr = P.simulate_forward(sc, p, seed=7)
+    ref = port_of(port, sc).forward(p, 7, 0)
+    assert fnv1a64_c(tr.cum_per_step) == fnv1a64_c(ref["cum_per_step"])
+    assert np.array_equal(tr.link_final, ref["link"]) and np.array_equal(tr.pos_final, ref["pos"])
+
+
+@pytest.mark.parametrize("B", [64, 256])
+def test_c3_batched_nowcast_draws_against_port(port, B):
+    """The batched throughput configuration (B independent C3 nowcasts in one
+    pass: the step graph) — first, middle and last draw against the port."""
+    sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 30, 120, 300)
+    p = sc.sample_parameters(3)
+    its = [1000 + b for b in range(B)]
+    trs = P.simulate_forward(sc, p, seed=7, noise_iterations=its)
+    pr = port_of(port, sc)
+    for b in (0, B // 2, B - 1):
+        ref = pr.forward(p, 7, its[b])
+        assert np.array_equal(trs[b].cum_per_step, ref["cum_per_step"]), b
+        assert np.array_equal(trs[b].link_final, ref["link"]) and np.array_equal(trs[b].pos_final, ref["pos"]), b
