@@ -53,10 +53,17 @@ constexpr int kFastSucc = 5;  // successor / candidate counts up to this use reg
 constexpr int kCfPer = DTG_CF_PER;
 constexpr int kCfThreads = 256;
 
+// kVec (even N, kCfPer == 2): a thread's two slots are ADJACENT and their
+// link ids and positions are read with one 8-byte / one 16-byte load (int2,
+// double2; still fully coalesced), the pair's outer neighbours with two scalar
+// loads -- half the load instructions of the strided mapping.
+template <bool kVec>
 __global__ void __launch_bounds__(kCfThreads, DTG_CF_MINB) k_step_cf(DevView d, int t, int s_cur) {
   (void)t;
   const int b = d.b0 + blockIdx.y;
-  const int k0 = blockIdx.x * (kCfThreads * kCfPer) + threadIdx.x;
+  const int blk0 = blockIdx.x * (kCfThreads * kCfPer);
+  const int k0 = kVec ? blk0 + 2 * static_cast<int>(threadIdx.x) : blk0 + static_cast<int>(threadIdx.x);
+  const int kstep = kVec ? 1 : kCfThreads;
   const std::size_t so = sidx(d, s_cur, b);
   const double* pos = d.pos + so;
   const int* off = d.off + oidx(d, s_cur, b);
@@ -64,14 +71,28 @@ __global__ void __launch_bounds__(kCfThreads, DTG_CF_MINB) k_step_cf(DevView d, 
   const std::size_t bl = static_cast<std::size_t>(b) * d.L;
   int j[kCfPer];
   double xm[kCfPer], x[kCfPer], xp[kCfPer];
+  if (kVec) {
+    const int kk = k0 < d.N ? k0 : d.N - 2;  // even N: pairs never straddle the end
+    const int2 j2 = *reinterpret_cast<const int2*>(d.lnk + so + kk);
+    const double2 x2 = *reinterpret_cast<const double2*>(pos + kk);
+    j[0] = j2.x;
+    j[1] = j2.y;
+    x[0] = x2.x;
+    x[1] = x2.y;
+    xm[0] = pos[kk > 0 ? kk - 1 : 0];
+    xm[1] = x2.x;
+    xp[0] = x2.y;
+    xp[1] = pos[kk + 2 < d.N ? kk + 2 : kk + 1];
+  } else {
 #pragma unroll
-  for (int i = 0; i < kCfPer; ++i) {
-    const int k = k0 + i * kCfThreads;
-    const int kk = k < d.N ? k : d.N - 1;
-    j[i] = d.lnk[so + kk];
-    x[i] = pos[kk];
-    xm[i] = pos[kk > 0 ? kk - 1 : 0];
-    xp[i] = pos[kk + 1 < d.N ? kk + 1 : kk];
+    for (int i = 0; i < kCfPer; ++i) {
+      const int k = k0 + i * kCfThreads;
+      const int kk = k < d.N ? k : d.N - 1;
+      j[i] = d.lnk[so + kk];
+      x[i] = pos[kk];
+      xm[i] = pos[kk > 0 ? kk - 1 : 0];
+      xp[i] = pos[kk + 1 < d.N ? kk + 1 : kk];
+    }
   }
   int base[kCfPer], n[kCfPer];
   double jam[kCfPer], dxf[kCfPer], len[kCfPer], ctr[kCfPer], thr[kCfPer];
@@ -89,7 +110,7 @@ __global__ void __launch_bounds__(kCfThreads, DTG_CF_MINB) k_step_cf(DevView d, 
   int* nA = d.nA + bl;
 #pragma unroll
   for (int i = 0; i < kCfPer; ++i) {
-    const int k = k0 + i * kCfThreads;
+    const int k = k0 + i * kstep;
     if (k >= d.N) break;
     const int r = k - base[i];
     // headway: leader gets M (car_following.cpp:547-553)
@@ -427,10 +448,14 @@ __device__ __forceinline__ int next_slot(const DevView& d, std::size_t bn,
 constexpr int kTransferPer = DTG_TR_PER;
 constexpr int kTransferThreads = 256;
 
+// kVec: adjacent slot pairs with int2 / double2 loads, as in k_step_cf.
+template <bool kVec>
 __global__ void __launch_bounds__(kTransferThreads) k_step_transfer(DevView d, int s_cur,
                                                                      int s_next) {
   const int b = d.b0 + blockIdx.y;
-  const int k0 = blockIdx.x * (kTransferThreads * kTransferPer) + threadIdx.x;
+  const int blk0 = blockIdx.x * (kTransferThreads * kTransferPer);
+  const int k0 = kVec ? blk0 + 2 * static_cast<int>(threadIdx.x) : blk0 + static_cast<int>(threadIdx.x);
+  const int kstep = kVec ? 1 : kTransferThreads;
   const std::size_t so = sidx(d, s_cur, b), sn = sidx(d, s_next, b);
   const std::size_t bl = static_cast<std::size_t>(b) * d.L;
   const std::size_t bn = static_cast<std::size_t>(b) * d.N;
@@ -438,13 +463,26 @@ __global__ void __launch_bounds__(kTransferThreads) k_step_transfer(DevView d, i
   const int* offn = d.off + oidx(d, s_next, b);
   int j[kTransferPer], id[kTransferPer], base[kTransferPer], na[kTransferPer], sh[kTransferPer];
   double x[kTransferPer];
+  if (kVec) {
+    const int kk = k0 < d.N ? k0 : d.N - 2;
+    const int2 j2 = *reinterpret_cast<const int2*>(d.lnk + so + kk);
+    const double2 x2 = *reinterpret_cast<const double2*>(d.x1 + bn + kk);
+    const int2 i2 = *reinterpret_cast<const int2*>(d.aid + so + kk);
+    j[0] = j2.x;
+    j[1] = j2.y;
+    x[0] = x2.x;
+    x[1] = x2.y;
+    id[0] = i2.x;
+    id[1] = i2.y;
+  } else {
 #pragma unroll
-  for (int i = 0; i < kTransferPer; ++i) {
-    const int k = k0 + i * kTransferThreads;
-    const int kk = k < d.N ? k : d.N - 1;
-    j[i] = d.lnk[so + kk];
-    x[i] = d.x1[bn + kk];
-    id[i] = d.aid[so + kk];
+    for (int i = 0; i < kTransferPer; ++i) {
+      const int k = k0 + i * kTransferThreads;
+      const int kk = k < d.N ? k : d.N - 1;
+      j[i] = d.lnk[so + kk];
+      x[i] = d.x1[bn + kk];
+      id[i] = d.aid[so + kk];
+    }
   }
 #pragma unroll
   for (int i = 0; i < kTransferPer; ++i) {
@@ -454,7 +492,7 @@ __global__ void __launch_bounds__(kTransferThreads) k_step_transfer(DevView d, i
   }
 #pragma unroll
   for (int i = 0; i < kTransferPer; ++i) {
-    const int k = k0 + i * kTransferThreads;
+    const int k = k0 + i * kstep;
     if (k >= d.N) break;
     const int r = k - base[i];
     int ns = sh[i] + r, lk = j[i];
@@ -923,6 +961,16 @@ __global__ void k_derive(DevView d, double* jam, double* dxf, double* pref) {
 // launch wrappers
 // ---------------------------------------------------------------------------------
 static inline dim3 grid_n(int n, int bs, int B) { return dim3((n + bs - 1) / bs, B); }
+
+// The paired (vector-load) slot mapping needs an even agent count (pairs
+// never straddle a scenario) and two slots per thread.
+static inline bool slot_vec(const DevView& d) {
+#ifdef DTG_NO_SLOT_VEC
+  return false;
+#else
+  return d.N % 2 == 0 && kCfPer == 2 && kTransferPer == 2;
+#endif
+}
 // scenarios of one forward launch: [b0, b0 + nb) (nb 0: all B)
 static inline int nbl(const DevView& d) { return d.nb ? d.nb : d.B; }
 
@@ -936,7 +984,10 @@ void launch_fwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
                        cudaStream_t st) {
   switch (which) {
     case 0:
-      k_step_cf<<<grid_n(d.N, kCfThreads * kCfPer, nbl(d)), kCfThreads, 0, st>>>(d, t, s_cur);
+      if (slot_vec(d))
+        k_step_cf<true><<<grid_n(d.N, kCfThreads * kCfPer, nbl(d)), kCfThreads, 0, st>>>(d, t, s_cur);
+      else
+        k_step_cf<false><<<grid_n(d.N, kCfThreads * kCfPer, nbl(d)), kCfThreads, 0, st>>>(d, t, s_cur);
       break;
     case 1:
       k_step_choice<<<grid_n(d.L, 128, nbl(d)), 128, 0, st>>>(d, t, s_cur);
@@ -948,8 +999,12 @@ void launch_fwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
       k_step_scan<<<nbl(d), 1024, 0, st>>>(d, s_cur, s_next, 0);
       break;
     default:
-      k_step_transfer<<<grid_n(d.N, kTransferThreads * kTransferPer, nbl(d)), kTransferThreads, 0, st>>>(
-          d, s_cur, s_next);
+      if (slot_vec(d))
+        k_step_transfer<true><<<grid_n(d.N, kTransferThreads * kTransferPer, nbl(d)), kTransferThreads, 0, st>>>(
+            d, s_cur, s_next);
+      else
+        k_step_transfer<false><<<grid_n(d.N, kTransferThreads * kTransferPer, nbl(d)), kTransferThreads, 0, st>>>(
+            d, s_cur, s_next);
   }
 }
 
@@ -965,7 +1020,10 @@ void launch_bwd_kernel(int which, const DevView& d, int t, int s_cur, int s_next
                        cudaStream_t st) {
   switch (which) {
     case 0:
-      k_step_cf<<<grid_n(d.N, kCfThreads * kCfPer, d.B), kCfThreads, 0, st>>>(d, t, s_cur);
+      if (slot_vec(d))
+        k_step_cf<true><<<grid_n(d.N, kCfThreads * kCfPer, d.B), kCfThreads, 0, st>>>(d, t, s_cur);
+      else
+        k_step_cf<false><<<grid_n(d.N, kCfThreads * kCfPer, d.B), kCfThreads, 0, st>>>(d, t, s_cur);
       break;
     case 1:
       k_step_choice<<<grid_n(d.L, 128, d.B), 128, 0, st>>>(d, t, s_cur);
