@@ -504,11 +504,14 @@ def run_ours(args):
     # back into host arrays (every step's counts + the final state)
     p_alt = P.LinkParams(p.u * (1.0 + 1e-3), p.kappa, p.beta, p.alpha, p.cost)
     calls = 0
+    # the caller's result buffers: page-locked and reused across requests, so
+    # the counts and the final state arrive by DMA without staging copies
+    outs = (P.pinned_empty((B, T_STEPS, L)), P.pinned_empty((B, N), np.int32), P.pinned_empty((B, N)))
 
     def e2e_call():
         nonlocal calls
         its = [(calls + 1) * 1000 + rank * B + b for b in range(B)]
-        P.simulate_forward(sc, p if calls % 2 == 0 else p_alt, seed=SIM_SEED, noise_iterations=its)
+        P.simulate_forward(sc, p if calls % 2 == 0 else p_alt, seed=SIM_SEED, noise_iterations=its, out=outs)
         calls += 1
 
     e2e_call()  # warm (context, graphs)
@@ -524,8 +527,9 @@ def run_ours(args):
     e2e = {"value": world * B * SIM_SECONDS / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "s_per_call": e2e_s,
            "path": "dtg_simulate_forward (C-ABI, host buffers, synchronous; count rows are copied back "
-                   "while the kernel runs, dtg_forward_read); new parameters and noise every call; the scenario's initial state stays resident on the device between calls "
-                   "(unchanged scenario)"}
+                   "while the kernel runs, dtg_forward_read, by DMA into the caller's page-locked result "
+                   "buffers (pinned_empty, reused across calls)); new parameters and noise every call; the "
+                   "scenario's initial state stays resident on the device between calls (unchanged scenario)"}
 
     # the same request with a FRESH scenario every call, as the reference's
     # simulate_forward rebuilds its state each time: network generation and

@@ -152,6 +152,12 @@ int dtg_forward_read(dtg_ctx* ctx, int n_steps, int steps_per_interval,
                      int checkpoint, double* cum_per_step, int* link_final,
                      double* pos_final);
 
+/* Page-locked host memory for result buffers: dtg_forward_read (and the
+ * level-2 dtg_simulate_forward) DMA their results straight into such buffers
+ * instead of staging them.  NULL on failure. */
+void* dtg_host_alloc(size_t bytes);
+void dtg_host_free(void* ptr);
+
 /* Wait for the context's stream and report device-side errors of the last
  * forward / backward (reads below do this implicitly). */
 int dtg_sync(dtg_ctx* ctx);

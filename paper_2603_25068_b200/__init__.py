@@ -24,6 +24,7 @@ from .engine import (  # noqa: F401
     calibrate,
     link_visits,
     optimize_control,
+    pinned_empty,
     simulate_forward,
     simulate_gradient,
     simulate_gradient_mse,

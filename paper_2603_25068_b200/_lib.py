@@ -87,6 +87,8 @@ SIGNATURES = [
     ("dtg_create", i32, [C.POINTER(NetDesc), C.POINTER(SimConfig), i32, i32, i32, C.POINTER(vp)]),
     ("dtg_destroy", None, [vp]),
     ("dtg_init", i32, []),
+    ("dtg_host_alloc", vp, [C.c_size_t]),
+    ("dtg_host_free", None, [vp]),
     ("dtg_last_error", C.c_char_p, [vp]),
     ("dtg_set_stream", i32, [vp, vp]),
     ("dtg_get_stream", i32, [vp, C.POINTER(vp), C.POINTER(C.c_int)]),

@@ -71,6 +71,18 @@ void reserve_pool() {
   done[dev] = true;
 }
 
+// Page-locked host memory (cudaHostAlloc / cudaHostRegister): copies into it
+// can be DMA'd directly, without pinned staging.
+bool pinned_host(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -1216,12 +1228,15 @@ int dtg_forward_read(dtg_ctx* c, int T, int spi, int checkpoint, double* cum, in
     int* hl = he + B;
     double* hp = reinterpret_cast<double*>(
         static_cast<char*>(c->h_fin) + ((B * 4 + B * N * 4 + 7) / 8) * 8);
+    const bool link_direct = link && pinned_host(link), pos_direct = pos && pinned_host(pos);
     if (link || pos) {
       const dtg::DevView d = c->view();
       dtg::launch_gather_state(d, T % c->S, c->tmp_link.p, c->tmp_pos.p, c->stream);
       CK(cudaGetLastError());
-      if (link) CK(cudaMemcpyAsync(hl, c->tmp_link.p, B * N * 4, cudaMemcpyDeviceToHost, c->stream));
-      if (pos) CK(cudaMemcpyAsync(hp, c->tmp_pos.p, B * N * 8, cudaMemcpyDeviceToHost, c->stream));
+      if (link)
+        CK(cudaMemcpyAsync(link_direct ? link : hl, c->tmp_link.p, B * N * 4, cudaMemcpyDeviceToHost, c->stream));
+      if (pos)
+        CK(cudaMemcpyAsync(pos_direct ? pos : hp, c->tmp_pos.p, B * N * 8, cudaMemcpyDeviceToHost, c->stream));
     }
     CK(cudaMemcpyAsync(he, c->errf.p, B * 4, cudaMemcpyDeviceToHost, c->stream));
     if (cum && T > 0) {
@@ -1235,7 +1250,11 @@ int dtg_forward_read(dtg_ctx* c, int T, int spi, int checkpoint, double* cum, in
       }
       // copy finished count rows while the kernel runs: each chunk is issued
       // once the kernel has published that its steps are final (or once the
-      // stream is idle: schedules without a progress counter, errors)
+      // stream is idle: schedules without a progress counter, errors).  A
+      // caller buffer in page-locked memory (dtg_host_alloc) takes the rows by
+      // DMA directly ([t][b] rows on the device -> [b][t] rows: one strided
+      // 2-D copy per scenario); pageable memory goes through pinned staging.
+      const bool direct = pinned_host(cum);
       const volatile unsigned int* prog = c->prog_h;
       int done = 0;
       while (done < T) {
@@ -1243,23 +1262,40 @@ int dtg_forward_read(dtg_ctx* c, int T, int spi, int checkpoint, double* cum, in
         while (static_cast<int>(*prog) < end) {
           if (cudaStreamQuery(c->stream) != cudaErrorNotReady) break;
         }
-        CK(cudaMemcpyAsync(c->h_stage + static_cast<std::size_t>(done) * BL,
-                           c->cumh.p + static_cast<std::size_t>(done + 1) * BL,
-                           static_cast<std::size_t>(end - done) * BL * 8, cudaMemcpyDeviceToHost,
-                           c->copy_stream));
-        CK(cudaStreamSynchronize(c->copy_stream));
-        for (std::size_t b = 0; b < B; ++b)
-          for (int t = done; t < end; ++t)
-            std::memcpy(cum + (b * T + t) * L, c->h_stage + (t * B + b) * L, L * 8);
+        const double* src = c->cumh.p + static_cast<std::size_t>(done + 1) * BL;
+        if (direct) {
+          for (std::size_t b = 0; b < B; ++b)
+            CK(cudaMemcpy2DAsync(cum + (b * T + done) * L, L * 8, src + b * L, BL * 8, L * 8, end - done,
+                                 cudaMemcpyDeviceToHost, c->copy_stream));
+        } else {
+          CK(cudaMemcpyAsync(c->h_stage + static_cast<std::size_t>(done) * BL, src,
+                             static_cast<std::size_t>(end - done) * BL * 8, cudaMemcpyDeviceToHost,
+                             c->copy_stream));
+          CK(cudaStreamSynchronize(c->copy_stream));
+          for (std::size_t b = 0; b < B; ++b)
+            for (int t = done; t < end; ++t)
+              std::memcpy(cum + (b * T + t) * L, c->h_stage + (t * B + b) * L, L * 8);
+        }
         done = end;
       }
+      if (direct) CK(cudaStreamSynchronize(c->copy_stream));
     }
     CK(cudaStreamSynchronize(c->stream));
     c->pending = false;
     c->check_flags(he);
-    if (link) std::memcpy(link, hl, B * N * 4);
-    if (pos) std::memcpy(pos, hp, B * N * 8);
+    if (link && !link_direct) std::memcpy(link, hl, B * N * 4);
+    if (pos && !pos_direct) std::memcpy(pos, hp, B * N * 8);
   });
+}
+
+void* dtg_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void dtg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 int dtg_read_state(dtg_ctx* c, int scenario, int step, int* link, double* pos) {

@@ -232,17 +232,37 @@ def link_visits(link0, transfers) -> np.ndarray:
     return np.array(rows, np.int32).reshape(-1, 4)
 
 
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """A numpy array in page-locked host memory (dtg_host_alloc), freed with
+    the array.  Results written into such arrays (simulate_forward's `out`)
+    are DMA'd from the device directly, without staging copies."""
+    import weakref
+
+    lib = load()
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape)) * dt.itemsize
+    p = lib.dtg_host_alloc(max(n, 1))
+    if not p:
+        raise MemoryError(f"dtg_host_alloc({n}) failed")
+    arr = np.frombuffer((C.c_char * max(n, 1)).from_address(p), dtype=dt, count=int(np.prod(shape))).reshape(shape)
+    weakref.finalize(arr, lib.dtg_host_free, p)
+    return arr
+
+
 def simulate_forward(sc: Scenario, params: LinkParams, seed: int, noise_iteration: int = 0,
                      record_states: bool = False, noise_iterations: Optional[Sequence[int]] = None,
-                     record_transfers: bool = False):
+                     record_transfers: bool = False, out=None):
     """simulate_forward (engine.cpp:227-254) on the GPU.  With noise_iterations,
     all draws run batched in one device pass and a list is returned.
     record_transfers: every link change of every agent, recorded by the
-    device merge (Trajectory.transfers; travel times via link_visits)."""
+    device merge (Trajectory.transfers; travel times via link_visits).
+    out: optional (cum_per_step [D, T, L] float64, link_final [D, N] int32,
+    pos_final [D, N] float64) arrays to write the results into, e.g. reused
+    page-locked buffers from pinned_empty (the results then arrive by DMA)."""
     if record_transfers:
         sc._check(sc._lib.dtg_scenario_set_record_transfers(sc._h, 1))
         try:
-            out = simulate_forward(sc, params, seed, noise_iteration, record_states, noise_iterations)
+            out = simulate_forward(sc, params, seed, noise_iteration, record_states, noise_iterations, out=out)
             ctx = sc.device_context()
             for d, tr in enumerate(out if isinstance(out, list) else [out]):
                 tr.transfers = transfer_events(ctx, d)
@@ -251,8 +271,14 @@ def simulate_forward(sc: Scenario, params: LinkParams, seed: int, noise_iteratio
             sc._check(sc._lib.dtg_scenario_set_record_transfers(sc._h, 0))
     its = _its(noise_iteration, noise_iterations)
     D, T, L, N = len(its), sc.horizon_steps, sc.n_links, sc.n_agents
-    cum = np.empty((D, T, L))  # every entry is written by the call
-    lk, ps = np.empty((D, N), np.int32), np.empty((D, N))
+    if out is not None:
+        cum, lk, ps = out
+        for a, shp, dt in ((cum, (D, T, L), np.float64), (lk, (D, N), np.int32), (ps, (D, N), np.float64)):
+            if a.shape != shp or a.dtype != dt or not a.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"out array must be a C-contiguous {np.dtype(dt).name} array of shape {shp}")
+    else:
+        cum = np.empty((D, T, L))  # every entry is written by the call
+        lk, ps = np.empty((D, N), np.int32), np.empty((D, N))
     sl = np.zeros((D, T, N), np.int32) if record_states else None
     sp = np.zeros((D, T, N)) if record_states else None
     wall = np.zeros(1)

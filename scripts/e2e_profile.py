@@ -24,6 +24,12 @@ def l2(i):
     its[0] = i; q = p if i % 2 else p2
     sc._check(lib.dtg_simulate_forward(sc._h, *q.arrays(), 7, 1, its, ptr(cum), ptr(lk), ptr(ps), None, None, ptr(wall)))
 print(f"level-2 C call, reused arrays: {tm(l2):.3f} ms")
+outs = (P.pinned_empty((1, T, L)), P.pinned_empty((1, N), np.int32), P.pinned_empty((1, N)))
+print(f"level-2 simulate_forward, pinned out=: {tm(lambda i: P.simulate_forward(sc, p if i % 2 else p2, seed=7, noise_iterations=[i], out=outs)):.3f} ms")
+def l2p(i):
+    its[0] = i; q = p if i % 2 else p2
+    sc._check(lib.dtg_simulate_forward(sc._h, *q.arrays(), 7, 1, its, ptr(outs[0]), ptr(outs[1]), ptr(outs[2]), None, None, ptr(wall)))
+print(f"level-2 C call, pinned arrays: {tm(l2p):.3f} ms")
 ctx = sc.device_context()
 pa = [a.copy() for a in p.arrays()]; pb = [a.copy() for a in p2.arrays()]
 def l1_params(i):

@@ -169,3 +169,25 @@ def test_mode_toggles_on_one_engine_keep_backward_exact():
         got.append(e.backward(snap_seeds=snap, x_seeds=xs))
     for g in got[1:]:
         assert np.array_equal(g, got[0])
+
+
+@pytest.mark.parametrize("B", [1, 3])
+def test_pinned_result_buffers_equal_pageable(B):
+    """simulate_forward(out=pinned_empty(...)): results DMA'd straight into
+    page-locked buffers equal the pageable (staged) read-back, call after call
+    with the buffers reused."""
+    sc = P.Scenario.grid(6, 800.0, 42, 1000.0).configure(18000, 30, 60, 300)
+    p = sc.sample_parameters(3)
+    T, L, N = sc.horizon_steps, sc.n_links, sc.n_agents
+    outs = (P.pinned_empty((B, T, L)), P.pinned_empty((B, N), np.int32), P.pinned_empty((B, N)))
+    for call in range(3):
+        its = [call * 10 + b for b in range(B)]
+        want = P.simulate_forward(sc, p, seed=7, noise_iterations=its)
+        got = P.simulate_forward(sc, p, seed=7, noise_iterations=its, out=outs)
+        for b in range(B):
+            assert np.shares_memory(got[b].cum_per_step, outs[0])  # views of the caller's buffers
+            assert np.array_equal(got[b].cum_per_step, want[b].cum_per_step)
+            assert np.array_equal(got[b].link_final, want[b].link_final)
+            assert np.array_equal(got[b].pos_final, want[b].pos_final)
+    with pytest.raises(ValueError):
+        P.simulate_forward(sc, p, seed=7, noise_iterations=list(range(B + 1)), out=outs)
