@@ -91,13 +91,21 @@ int dtg_get_stream(const dtg_ctx* ctx, void** cuda_stream, int* owned);
 int dtg_set_persistent(dtg_ctx* ctx, int enabled);
 /* Forward schedule: 0 auto (default), 1 one thread-block cluster per
  * scenario, 2 one persistent cooperative grid, 3 CUDA graph of 5 kernels per
- * step.  All produce identical results.  dtg_last_mode returns
- * 1000 * mode + CTAs per scenario of the last forward (0 for the graph). */
+ * step, 4 one CTA per scenario looping over all steps (scenarios independent,
+ * CTA barriers only).  All produce identical results.  dtg_last_mode returns
+ * 1000 * mode + CTAs per scenario of the last forward (1 for mode 4, 0 for
+ * the graph). */
 int dtg_set_mode(dtg_ctx* ctx, int mode);
 /* Measurement hook: one persistent reverse sweep (zero seeds) with
  * %globaltimer stamps; phase_us[8] = mean per-step span (us) of R1, barrier,
  * R2, barrier, R3, barrier, R4 (and 0). */
 int dtg_profile_backward(dtg_ctx* ctx, double* phase_us, int* grid_out);
+/* Measurement hook: one scenario-resident forward (mode 4) with %globaltimer
+ * stamps; phase_us[9] = mean per-step span (us) of the links, choice, merge,
+ * scan and slots phases and the whole step, then the mean number of links
+ * with arrived heads, the most heads on one link and the mean number of
+ * chosen links per step. */
+int dtg_profile_scn(dtg_ctx* ctx, int T, int steps_per_interval, double* phase_us);
 /* Measurement hook: raw per-CTA stamps [T][grid][8] (ns) of that run. */
 int dtg_debug_bwd_stamps(dtg_ctx* ctx, unsigned long long* out, int* grid);
 int dtg_last_mode(const dtg_ctx* ctx);

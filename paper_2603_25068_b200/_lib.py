@@ -97,6 +97,7 @@ SIGNATURES = [
     ("dtg_set_mode", i32, [vp, i32]),
     ("dtg_set_flag", i32, [vp, i32, i32]),
     ("dtg_profile_backward", i32, [vp, _dp, C.POINTER(C.c_int)]),
+    ("dtg_profile_scn", i32, [vp, i32, i32, _dp]),
     ("dtg_last_mode", i32, [vp]),
     ("dtg_profile_persistent", i32, [vp, i32, i32, _dp, C.POINTER(C.c_int)]),
     ("dtg_set_params", i32, [vp, i32, _dp, _dp, _dp, _dp, _dp]),

@@ -23,6 +23,7 @@ namespace dtg {
 cudaError_t decision_stats_fused(int force, unsigned long long* count);
 cudaError_t decision_stats_backward(int force, unsigned long long* count);
 cudaError_t decision_stats_kernels(int force, unsigned long long* count);
+cudaError_t decision_stats_scn(int force, unsigned long long* count);
 }  // namespace dtg
 
 namespace {
@@ -182,6 +183,8 @@ struct dtg_ctx {
   // persistent forward
   bool persistent = true;
   int pgrid_max = 0;
+  bool scn_ok = false;  // scenario-resident forward (mode 4) fits shared memory
+  int n_sm = 0;
   DevBuf<double> x1b, tailb;
   DevBuf<int> wonb, nAb, qnb, depb, winp, ccnt, clist;
   int last_grid = 0;
@@ -199,7 +202,7 @@ struct dtg_ctx {
   cudaEvent_t seed_ev = nullptr;
   void* h_fin = nullptr;         // pinned final state: int link[B*N] | double pos[B*N]
   std::size_t h_fin_n = 0;
-  int mode = 0;          // 0 auto, 1 cluster, 2 grid-persistent, 3 step graph
+  int mode = 0;          // 0 auto, 1 cluster, 2 grid-persistent, 3 step graph, 4 scenario CTAs
   int cluster_cs_max = 0;
   bool stage_params = false;
   int last_mode = 0, last_cs = 0;
@@ -599,6 +602,12 @@ int dtg_create(const dtg_net_desc* net, const dtg_sim_config* cfg, int n_agents,
     c->pgrid_max = dtg::fused_max_grid(L, c->stage_params);
     c->bgrid_max = dtg::backward_max_grid(L, c->maxdeg);
     c->cluster_cs_max = dtg::fused_max_cluster(L, c->stage_params);
+    c->scn_ok = dtg::forward_scn_ok(L);
+    {
+      int dev = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
     c->gbar.alloc(1);
     c->srec.alloc(BL * c->maxdeg);
     c->cands.alloc(BL * dtg::kClusterCandCap);
@@ -662,7 +671,8 @@ int dtg_init(void) {
 
 int dtg_debug_decisions(int force_exact, unsigned long long* exact_decisions) {
   unsigned long long total = 0;
-  for (auto fn : {dtg::decision_stats_fused, dtg::decision_stats_backward, dtg::decision_stats_kernels}) {
+  for (auto fn : {dtg::decision_stats_fused, dtg::decision_stats_backward, dtg::decision_stats_kernels,
+                  dtg::decision_stats_scn}) {
     unsigned long long n = 0;
     if (fn(force_exact, &n) != cudaSuccess) return DTG_ERR_CUDA;
     total += n;
@@ -768,6 +778,40 @@ int dtg_profile_persistent(dtg_ctx* c, int T, int spi, double* phase_us, int* gr
   });
 }
 
+// Measurement hook: one scenario-resident forward (mode 4) with %globaltimer
+// stamps; phase_us[6] = per-step span (us) of cf, choice, merge, scan,
+// transfer and the whole step, averaged over the CTAs and steps.
+int dtg_profile_scn(dtg_ctx* c, int T, int spi, double* phase_us) {
+  return guarded(c, [&] {
+    const int m = c->mode;
+    c->mode = 4;
+    c->want_stamps = true;
+    const int rc = dtg_forward(c, T, spi, 0);
+    c->want_stamps = false;
+    c->mode = m;
+    if (rc) throw std::runtime_error(c->err);
+    c->sync_check();
+    std::vector<unsigned long long> s(static_cast<std::size_t>(T) * c->B * 8);
+    CK(cudaMemcpy(s.data(), c->stamps.p, s.size() * 8, cudaMemcpyDeviceToHost));
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    for (std::size_t r = 0; r < static_cast<std::size_t>(T) * c->B; ++r) {
+      for (int w = 0; w < 5; ++w) acc[w] += double(s[r * 8 + w + 1] - s[r * 8 + w]);
+      acc[5] += double(s[r * 8 + 5] - s[r * 8]);
+    }
+    for (int w = 0; w < 6; ++w) phase_us[w] = acc[w] / (double(T) * c->B) / 1e3;
+    // work lists: mean links with arrived heads, max heads on one link, mean chosen links
+    double nact = 0, mxh = 0, ntg = 0;
+    for (std::size_t r = 0; r < static_cast<std::size_t>(T) * c->B; ++r) {
+      nact += double(s[r * 8 + 6] >> 32);
+      mxh = std::max(mxh, double(s[r * 8 + 6] & 0xffffffffull));
+      ntg += double(s[r * 8 + 7]);
+    }
+    phase_us[6] = nact / (double(T) * c->B);
+    phase_us[7] = mxh;
+    phase_us[8] = ntg / (double(T) * c->B);
+  });
+}
+
 // Measurement hook: per-warp slot-phase records [T][warps][4] (start, after
 // offsets, after slot loop, arrived agents in the warp).
 int dtg_debug_warp_records(dtg_ctx* c, int T, int spi, unsigned long long* out, int* n_warps) {
@@ -815,12 +859,14 @@ int dtg_set_flag(dtg_ctx* c, int flag, int value) {
 }
 
 int dtg_set_mode(dtg_ctx* c, int mode) {
-  if (mode < 0 || mode > 3) return fail(c, DTG_ERR_CONFIG, "mode must be 0..3");
+  if (mode < 0 || mode > 4) return fail(c, DTG_ERR_CONFIG, "mode must be 0..4");
   c->mode = mode;
   return DTG_OK;
 }
 
-int dtg_last_mode(const dtg_ctx* c) { return c->last_mode * 1000 + (c->last_mode == 3 ? 0 : c->last_cs); }
+int dtg_last_mode(const dtg_ctx* c) {
+  return c->last_mode * 1000 + (c->last_mode == 3 ? 0 : c->last_mode == 4 ? 1 : c->last_cs);
+}
 
 static void run_backward(dtg_ctx* c, const double* snap, const double* cum, const double* xs,
                          cudaMemcpyKind kind, bool seeds_ready = false);
@@ -1004,6 +1050,7 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
     const std::size_t BN = static_cast<std::size_t>(c->B) * c->N;
     const std::size_t BL = static_cast<std::size_t>(c->B) * c->L;
     const int nsp = c->graph_branches();
+    bool scn = false;  // mode 4: scenario-resident CTAs (decided below, before body() runs)
     auto body = [&] {
       dtg::launch_derive(d, c->derived.p, c->derived.p + BL, c->derived.p + 2 * BL, st);
       dtg::launch_pack_succ(d, c->srec.p, st);
@@ -1015,6 +1062,15 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       CK(cudaMemcpyAsync(c->qh.p, c->q0.p, BL * 8, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemsetAsync(c->cumh.p, 0, BL * 8, st));
       CK(cudaMemsetAsync(c->errf.p, 0, sizeof(int) * c->B, st));
+      if (scn) {
+        unsigned long long* stp = nullptr;
+        if (c->want_stamps) {
+          c->stamps.ensure(static_cast<std::size_t>(T) * c->B * 8);
+          stp = c->stamps.p;
+        }
+        CK(dtg::launch_forward_scn(d, T, stp, st));
+        return;
+      }
       c->fork_branches(nsp, st, [&](int b0, int nb, cudaStream_t sq) {
         dtg::DevView dq = d;
         dq.b0 = b0;
@@ -1038,7 +1094,13 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
     // 9.91 vs 7.41; scripts/graph_time.py)
     if (c->mode == 0 && mode == 2 && c->N > dtg::kClusterThreads && 5 * c->B > c->pgrid_max) mode = 3;
     if (!c->persistent && c->mode == 0) mode = 3;
+    // auto: beyond ~1.2 scenarios per SM, one CTA per scenario beats the step
+    // graph (C3 ms/nowcast graph vs mode 4: B=160 17.2 vs 18.6, B=192 21.1 vs
+    // 19.4, B=256 27.9 vs 20.6; scripts/scn_time.py)
+    if (c->mode == 0 && c->persistent && mode == 3 && 5 * c->B > 6 * c->n_sm) mode = 4;
+    if (mode == 4 && !c->scn_ok) mode = 3;  // per-link state exceeds shared memory
     c->last_mode = mode;
+    scn = mode == 4;
     if ((mode == 1 || mode == 2) && T > 0) {
       {  // one launch for the per-link constants, the initial layout and the counters
         dtg::ForwardInit in{};
@@ -1130,6 +1192,17 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
       return;
     }
     const long long key = (static_cast<long long>(T) << 20) ^ (c->S << 1) ^ 1 ^ (static_cast<long long>(nsp) << 50);
+    if (scn && T > 0) {  // six launches: no graph needed
+      body();
+      CK(cudaGetLastError());
+      c->launches = 2 + 1;  // k_derive, k_pack_succ, k_forward_scn
+      c->last_T = T;
+      c->last_spi = spi;
+      c->last_ckpt = checkpoint;
+      c->last_K = T / spi;
+      c->pending = true;
+      return;
+    }
     if (c->graphs && T > 0) {
       if (c->fwd_key != key || !c->fwd_exec) {
         if (c->fwd_exec) cudaGraphExecDestroy(c->fwd_exec);

@@ -6,6 +6,12 @@
 
 namespace dtg {
 
+// scenario-resident forward: one CTA per scenario runs all T steps
+// scenario-resident forward (dtg_scn.cu): one CTA per scenario runs all T
+// steps; forward_scn_ok: the per-link shared-memory state fits this device
+std::size_t forward_scn_smem(int L);
+bool forward_scn_ok(int L);
+cudaError_t launch_forward_scn(const DevView& d, int T, unsigned long long* stamps, cudaStream_t st);
 void launch_step_forward(const DevView& d, int t, int s_cur, int s_next,
                          cudaStream_t st);
 void launch_step_backward(const DevView& d, int t, int s_cur, int s_next,

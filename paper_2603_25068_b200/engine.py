@@ -480,18 +480,26 @@ class Engine:
 
     @property
     def last_mode(self) -> int:
-        """1000 * schedule (1 cluster, 2 persistent grid, 3 step graph) + CTAs
-        per scenario of the last forward."""
+        """1000 * schedule (1 cluster, 2 persistent grid, 3 step graph,
+        4 scenario-resident CTAs) + CTAs per scenario of the last forward."""
         return int(self._lib.dtg_last_mode(self._h))
 
     @property
     def last_schedule(self) -> dict:
         m = self.last_mode
-        names = {1: "cluster per scenario", 2: "fused persistent grid", 3: "5-kernel step graph"}
+        names = {1: "cluster per scenario", 2: "fused persistent grid", 3: "5-kernel step graph",
+                 4: "scenario-resident CTAs"}
         return {"schedule": names.get(m // 1000, str(m)), "ctas_per_scenario": m % 1000 or None}
 
     def set_persistent(self, on: bool):
         self._check(self._lib.dtg_set_persistent(self._h, int(on)))
+
+    def profile_scn(self, T: int, steps_per_interval: int) -> dict:
+        """Mean per-step span (us) of the scenario-resident forward's phases."""
+        ph = np.zeros(9)
+        self._check(self._lib.dtg_profile_scn(self._h, T, steps_per_interval, ph))
+        return dict(zip(("links", "choice", "merge", "scan", "slots", "step", "head_links", "max_heads",
+                         "chosen_links"), ph.tolist()))
 
     def profile_persistent(self, T: int, steps_per_interval: int):
         """Mean per-step span (us) of the persistent kernel's phases."""

@@ -39,13 +39,14 @@ def run(sc, p, B, mode, T, spi, ckpt=True):
     (4, 400.0, 1000, 1, 200, 300),  # more scenarios than resident CTAs -> scenario loop
     (4, 400.0, 1000, 1, 100, 37),   # step graph in 4 uneven scenario branches (9, 9, 9, 10)
     (50, 400.0, 100000, 1, 60, 1),  # C2: 12,300 links -> lean layout (per-link arrays in global memory)
+    (4, 400.0, 1001, 1, 200, 3),    # odd agent count: scalar slot mapping
 ])
 def test_persistent_equals_step_graph(n, length, veh, dn, T, B):
     sc = P.Scenario.grid(n, length, 42, 1000.0).configure(veh, dn, T, 300 if dn <= 2 else 30 * dn * 10)
     p = sc.sample_parameters(3)
     spi = sc.steps_per_interval
     ref = run(sc, p, B, 3, T, spi)  # 5-kernel step graph
-    for mode in (1, 2):           # cluster per scenario, persistent grid
+    for mode in (1, 2, 4):        # cluster per scenario, persistent grid, scenario-resident CTAs
         a = run(sc, p, B, mode, T, spi)
         assert np.array_equal(a[0], ref[0]), mode
         for x, y in zip(a[1], ref[1]):
