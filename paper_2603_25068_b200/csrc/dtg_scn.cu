@@ -122,7 +122,7 @@ __device__ __forceinline__ void scn_move(const DevView& d, std::size_t bn, std::
 // A merge row with more than kFastSucc candidates (rare): local arrays, out
 // of line so the common path keeps its candidates in registers.
 __device__ __noinline__ void scn_merge_wide(const DevView& d, int b, int t, int i, const int* off, const int* nA,
-                                            std::size_t so, int* w, int* wa) {
+                                            std::size_t so, int* w, int* wa, int* wl) {
   int cid[kMaxCand], cslot[kMaxCand], clink[kMaxCand];
   const int nc = gather_candidates(d, b, i, off, nA, so, cid, cslot, clink);
   if (nc) {
@@ -130,13 +130,14 @@ __device__ __noinline__ void scn_merge_wide(const DevView& d, int b, int t, int 
     const int best = merge_softmax(d, b, t, i, nc, cid, clink, lz, pi, false);
     *w = cslot[best];
     *wa = cid[best];
+    *wl = clink[best];
   }
 }
 
 __global__ void __launch_bounds__(kScnThreads, 2) k_forward_scn(DevView d, int T, unsigned long long* stamps) {
   __shared__ int sm[32];
   __shared__ unsigned long long smin[32];
-  __shared__ int cnt[2];  // [0] links with arrived heads, [1] chosen links
+  __shared__ int cnt[3];  // [0] links with arrived heads, [1] chosen links, [2] most heads on a link (stamps)
   extern __shared__ int scn_smem[];
   const int L = d.L, W = (L + 31) >> 5;
   int* offs[2] = {scn_smem, scn_smem + (L + 1)};
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kScnThreads, 2) k_forward_scn(DevView d, int T
     const int* off0 = d.off + oidx(d, 0, b);
     for (int j = tid; j <= L; j += kScnThreads) offs[0][j] = off0[j];
     for (int w = tid; w < W; w += kScnThreads) tbits[w] = 0;
-    if (tid == 0) cnt[0] = cnt[1] = 0;
+    if (tid == 0) cnt[0] = cnt[1] = cnt[2] = 0;
   }
   __syncthreads();
   for (int t = 0; t < T; ++t) {
@@ -178,13 +179,17 @@ __global__ void __launch_bounds__(kScnThreads, 2) k_forward_scn(DevView d, int T
       const int na = scn_link(d, b, t, pos, off, j, &vacant);
       nA[j] = na;
       win[j] = -1;
+      sh[j] = 0;  // departures, counted by the merge phase
       const unsigned m = 1u << (j & 31);
       if (vacant)
         atomicOr(&vbits[j >> 5], m);
       else
         atomicAnd(&vbits[j >> 5], ~m);
       if (d.ev) d.ev[(static_cast<std::size_t>(t) * d.B + b) * L + j] = -1;
-      if (na) act[atomicAdd(&cnt[0], 1)] = static_cast<unsigned short>(j);
+      if (na) {
+        act[atomicAdd(&cnt[0], 1)] = static_cast<unsigned short>(j);
+        if (stamps != nullptr) atomicMax(&cnt[2], na);
+      }
     }
     __syncthreads();
     scn_stamp(stamps, T, t, 1);
@@ -202,10 +207,8 @@ __global__ void __launch_bounds__(kScnThreads, 2) k_forward_scn(DevView d, int T
     __syncthreads();
     scn_stamp(stamps, T, t, 2);
     if (stamps != nullptr && tid == 0) {  // measurement: work-list sizes of this step
-      int heads = 0;
-      for (int q = 0; q < cnt[0]; ++q) heads = max(heads, nA[act[q]]);
       stamps[((static_cast<std::size_t>(blockIdx.x) * T + t) << 3) + 6] =
-          (static_cast<unsigned long long>(cnt[0]) << 32) | static_cast<unsigned>(heads);
+          (static_cast<unsigned long long>(cnt[0]) << 32) | static_cast<unsigned>(cnt[2]);
       stamps[((static_cast<std::size_t>(blockIdx.x) * T + t) << 3) + 7] = cnt[1];
     }
     if (tid == 0) cnt[0] = 0;  // next read after phase 1 of t + 1
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(kScnThreads, 2) k_forward_scn(DevView d, int T
       if (!((vbits[i >> 5] >> (i & 31)) & 1u)) continue;
       int cid[kFastSucc], cslot[kFastSucc], clink[kFastSucc];
       const int nc = gather_candidates_fast(d, b, i, off, nA, so, cid, cslot, clink);
-      int w = -1, wa = -1;
+      int w = -1, wa = -1, wl = 0;
       if (nc > 0) {
         const int best = merge_softmax_fast(d, b, t, i, nc, cid, clink);
 #pragma unroll
@@ -224,12 +227,14 @@ __global__ void __launch_bounds__(kScnThreads, 2) k_forward_scn(DevView d, int T
           if (e == best) {
             w = cslot[e];
             wa = cid[e];
+            wl = clink[e];
           }
       } else if (nc < 0) {
-        scn_merge_wide(d, b, t, i, off, nA, so, &w, &wa);
+        scn_merge_wide(d, b, t, i, off, nA, so, &w, &wa, &wl);
       }
       if (w >= 0) {
         win[i] = w;
+        atomicAdd(&sh[wl], 1);
         d.won[bn + w] = 1;
         if (d.ev) d.ev[(static_cast<std::size_t>(t) * d.B + b) * L + i] = wa;
       }
@@ -247,11 +252,8 @@ __global__ void __launch_bounds__(kScnThreads, 2) k_forward_scn(DevView d, int T
       const int j0 = min(L, tid * per), j1 = min(L, j0 + per);
       int sum = 0;
       for (int j = j0; j < j1; ++j) {
-        const int base = off[j], n = off[j + 1] - base, na = nA[j];
-        int dep = 0;
-        for (int r = 0; r < na; ++r) dep += d.won[bn + base + r];
+        const int n = off[j + 1] - off[j], dep = sh[j];  // sh: departures until the offsets are known
         const int nc = n - dep + (win[j] >= 0 ? 1 : 0);
-        sh[j] = dep;  // staged until the offsets are known
         msl[j] = nc;
         sum += nc;
       }
