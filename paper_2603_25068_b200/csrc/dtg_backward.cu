@@ -1,5 +1,6 @@
 // Persistent cooperative reverse sweep: all T reverse steps of all B scenarios
-// in one launch, four grid barriers per step (the checkpointed per-step VJP of
+// in one launch, three grid barriers per step (R4 of step t + 1 runs in the
+// same phase as R1 of step t) (the checkpointed per-step VJP of
 // src/engine.cpp:388-415, i.e. Tape::vjp of src/tensor.cpp:715-996 applied to
 // engine_step / node_step / car_following_step / midpoint_count).
 //
@@ -42,6 +43,10 @@ constexpr int kBT = DTG_BWD_THREADS;  // threads per CTA
 constexpr int kFastDeg = 5;  // successor counts up to this take unrolled register paths
 constexpr int kHeadCap = 1024;  // deferred arrived heads per CTA (overflow runs inline)
 constexpr int kB3 = 2;  // R3 slots per thread in flight
+#ifndef DTG_R4_THREADS
+#define DTG_R4_THREADS 192
+#endif
+constexpr int kR4T = DTG_R4_THREADS;  // threads running R4 of step t + 1 beside R1 of step t
 
 __device__ __forceinline__ int findl(const int* off_s, int L, int k) {
   int lo = 0, hi = L - 1;
@@ -96,7 +101,7 @@ __device__ __forceinline__ void t2_merge(T2& A, const T2& B) {
 }
 
 // new slot (layout t+1) of layout-t slot k on link j (rank r)
-__device__ __forceinline__ int map_next(const BView& V, int b, int k, int j, int r,
+__device__ __forceinline__ int map_next(const BView& V, int b, int par, int k, int j, int r,
                                         const int* offT, const int* offN, bool* mover) {
   const DevView& d = V.d;
   const std::size_t bn = static_cast<std::size_t>(b) * d.N;
@@ -104,7 +109,7 @@ __device__ __forceinline__ int map_next(const BView& V, int b, int k, int j, int
   const int na = V.nA_cur[bl + j];
   if (r < na && V.won[bn + k]) {
     *mover = true;
-    return offN[V.choice[bn + k] + 1] - 1;  // tail of the row it won
+    return offN[V.choice[static_cast<std::size_t>(par) * d.B * d.N + bn + k] + 1] - 1;  // tail of the row it won
   }
   *mover = false;
   int dd;
@@ -119,11 +124,11 @@ __device__ __forceinline__ int map_next(const BView& V, int b, int k, int j, int
 }
 
 // adjoint of the new position x1 of slot k (transfer + counting)
-__device__ __forceinline__ double x1_bar_p(const BView& V, int b, int k, int j, int r, double x1,
+__device__ __forceinline__ double x1_bar_p(const BView& V, int b, int par, int k, int j, int r, double x1,
                                            const int* offT, const int* offN, const double* xbn) {
   const DevView& d = V.d;
   bool mover;
-  const int ns = map_next(V, b, k, j, r, offT, offN, &mover);
+  const int ns = map_next(V, b, par, k, j, r, offT, offN, &mover);
   double xb = (mover && !d.tg) ? 0.0 : xbn[ns];
   const double qt = V.qtot[static_cast<std::size_t>(b) * d.L + j];
   if (qt != 0.0) {
@@ -150,7 +155,12 @@ __device__ __forceinline__ void bstamp(const BView& V, int t, int w) {
 // registration as a merge candidate of the chosen row.
 __device__ __forceinline__ void replay_head(const BView& V, int b, int t, int k, int j, int a) {
   const DevView& d = V.d;
-  const std::size_t bn = static_cast<std::size_t>(b) * d.N, bl = static_cast<std::size_t>(b) * d.L;
+  // per-slot head records and candidate counts are kept per step parity: R4 of
+  // step t + 1 reads its own while R1 of step t writes these
+  const std::size_t par = static_cast<std::size_t>(t & 1);
+  const std::size_t bn = par * d.B * d.N + static_cast<std::size_t>(b) * d.N;
+  const std::size_t bl = static_cast<std::size_t>(b) * d.L;
+  const std::size_t blp = par * d.B * d.L + bl;
   const int s0 = d.succ_off[j], deg = (V.dbg & 1) ? 0 : d.succ_off[j + 1] - s0;
   int c = -1;
   if (deg > 0) {
@@ -185,7 +195,7 @@ __device__ __forceinline__ void replay_head(const BView& V, int b, int t, int k,
       c = d.succ[s0 + ed];
       for (int e = 0; e < deg; ++e) lp[e] = (lz[e] + g[e]) * d.kinv;  // logits, as in softmax_stage2
     }
-    const int qq = atomicAdd(&V.ccnt[bl + c], 1);  // round trip overlaps the merge draw
+    const int qq = atomicAdd(&V.ccnt[blp + c], 1);  // round trip overlaps the merge draw
     const std::uint64_t mb = rng_final(rng_prefix2(rng_prefix1(d.seed_merge[b], static_cast<std::uint64_t>(t)),
                                                    static_cast<std::uint64_t>(c)),
                                        static_cast<std::uint64_t>(a));
@@ -263,6 +273,121 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
     }
   grid_sync();
 
+  // R4 of step t4 for scenario b (o4: layout t4's offsets in shared memory;
+  // threads tid4 < nt4 of the CTA take part):
+  // the link-choice VJP per arrived head, the u / kappa / alpha reductions and
+  // the departures reset.  It runs in the same phase as R1 of step t4 - 1
+  // (one grid barrier less per step, and the two phases' dependency chains
+  // overlap): every buffer R4 reads that R1 writes (head records, arrived
+  // list and prefix lengths, candidate counts) is kept per step parity.
+  auto r4 = [&](int b, int t4, const int* o4, int tid4, int nt4) {
+    const int p4 = t4 & 1;
+      const std::size_t bn = static_cast<std::size_t>(b) * N, bl = static_cast<std::size_t>(b) * L;
+      const std::size_t bnp = static_cast<std::size_t>(p4) * d.B * N + bn;  // this step's head records
+      const std::size_t so = sidx(d, t4 % d.S, b);
+      double* vbc = V.vbar + (static_cast<std::size_t>(p4) * d.B * N + bn) * d.maxdeg;
+      const unsigned long long key = V.a0key[p4 * d.B + b];
+      const int a0s = key == ULLONG_MAX ? -1 : static_cast<int>(key & 0xffffffffull);
+      const int nA = V.acount[p4 * d.B + b];
+      for (int q = spread(tid4, lg, nblk); q < nA && !(V.dbg & 512); q += nblk * nt4) {
+        const int s = V.alist[bnp + q];
+        const int c = V.choice[bnp + s];
+        if (c < 0) continue;
+        const int j = d.lnk[so + s];
+        const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
+        const double* lz = d.slogz + (bl + j) * d.maxdeg;
+        const double* lp = V.lpi + (bnp + s) * d.maxdeg;
+        const int ed = V.ched[bnp + s];
+        const double lrow = (V.vac[bl + c] && V.win[bl + c] >= 0) ? V.lbar_row[bn + s] : 0.0;
+        const bool hit = V.vac[bl + c] && V.win[bl + c] >= 0;
+        const double* la0 = V.lbar_a0 + static_cast<std::size_t>(b) * d.maxdeg;
+        if (deg <= kFastDeg) {  // registers, same operation order as two_softmax_vjp
+          double bar[kFastDeg], pi[kFastDeg];
+          {  // pi from the replayed logits: softmax_stage2's operations
+            double yv[kFastDeg];
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e) yv[e] = e < deg ? lp[e] : 0.0;
+            double m2 = yv[0];
+#pragma unroll
+            for (int e = 1; e < kFastDeg; ++e)
+              if (e < deg && m2 < yv[e]) m2 = yv[e];
+            double z2 = 0.0;
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e) {
+              pi[e] = dexp(yv[e] - m2);
+              if (e < deg) z2 += pi[e];
+            }
+#pragma unroll
+            for (int e = 0; e < kFastDeg; ++e) pi[e] = e < deg ? pi[e] / z2 : 0.0;
+          }
+#pragma unroll
+          for (int e = 0; e < kFastDeg; ++e) {
+            const bool on = e < deg;
+            double v = (hit && e == ed) ? lrow : 0.0;
+            if (on && s == a0s) v += la0[e];
+            bar[e] = on ? ((v * 1.0) * 1.0) * (V.vac[bl + d.succ[s0 + e]] ? 1.0 : 0.0) : 0.0;
+          }
+          double dot = 0.0;
+#pragma unroll
+          for (int e = 0; e < kFastDeg; ++e)
+            if (e < deg) dot += bar[e] * pi[e];
+          double gs = 0.0;
+#pragma unroll
+          for (int e = 0; e < kFastDeg; ++e)
+            if (e < deg) {
+              bar[e] = (pi[e] * (bar[e] - dot)) * d.kinv;
+              gs += bar[e];
+            }
+#pragma unroll
+          for (int e = 0; e < kFastDeg; ++e)
+            if (e < deg) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e] - dexp(lz[e]) * gs;
+        } else {
+          double bar[kMaxDeg], pi[kMaxDeg];
+          {  // pi from the replayed logits: softmax_stage2's operations
+            double m2 = lp[0];
+            for (int e = 1; e < deg; ++e)
+              if (m2 < lp[e]) m2 = lp[e];
+            double z2 = 0.0;
+            for (int e = 0; e < deg; ++e) z2 += dexp(lp[e] - m2);
+            for (int e = 0; e < deg; ++e) pi[e] = dexp(lp[e] - m2) / z2;
+          }
+          for (int e = 0; e < deg; ++e) bar[e] = 0.0;
+          if (hit) bar[ed] = lrow;
+          if (s == a0s)
+            for (int e = 0; e < deg; ++e) bar[e] += la0[e];
+          for (int e = 0; e < deg; ++e)
+            bar[e] = ((bar[e] * 1.0) * 1.0) * (V.vac[bl + d.succ[s0 + e]] ? 1.0 : 0.0);
+          two_softmax_vjp(deg, lz, pi, d.kinv, bar);
+          for (int e = 0; e < deg; ++e) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e];
+        }
+      }
+      // warp per link: u, kappa, alpha for step t
+      double* g5 = V.grads + static_cast<std::size_t>(b) * 5 * L;
+      // thread per link (links dealt in 32-lane groups over the CTAs): the
+      // segment sums run in slot order; the parameter loads of the epilogue
+      // are issued together
+      for (int j = spread(tid4, lg, nblk); j < L && !(V.dbg & 1024); j += nblk * nt4) {
+        const int base = o4[j], n = o4[j + 1] - base;
+        const double kap = d.kappa[bl + j];
+        const double g0 = g5[j], g1 = g5[L + j], g3 = g5[3 * L + j];
+        const int na = n ? V.nAb[static_cast<std::size_t>(p4) * d.B * L + bl + j] : 0;
+        double ub, jb;
+        link_sums8(V.cu + bn, V.cg + bn, base, n, ub, jb);
+        if (n) {
+          g5[j] = g0 + (0.0 + ub);
+          g5[L + j] = g1 + (0.0 - jb * static_cast<double>(d.delta_n) / (kap * kap));
+        }
+        double ab = 0.0;
+        for (int r = 0; r < na; ++r) {
+          const int s = base + r;
+          const int ch = V.choice[bnp + s];
+          if (ch >= 0 && V.vac[bl + ch] && V.win[bl + ch] >= 0) ab += 1.0 * V.prio_bar[bn + s];
+        }
+        g5[3 * L + j] = g3 + ab;
+      }
+      for (int i = lg * nt4 + tid4; i < L; i += nblk * nt4) V.dep[bl + i] = 0;
+  };
+
   for (int t = T - 1; t >= 0; --t) {
     const int par = t & 1;
     const int snap_k = ((t + 1) % V.spi == 0) ? (t + 1) / V.spi - 1 : -1;
@@ -278,20 +403,33 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           offN[j] = ogn[j];
         }
         __syncthreads();
+        // R4 of step t + 1 on the first kR4T threads, R1 on the others: the
+        // two phases' dependency chains run side by side
+        const bool with4 = t + 1 < T;
+        const int t1 = with4 ? tid - kR4T : tid, n1 = with4 ? kBT - kR4T : kBT;
+        if (with4 && tid < kR4T) {
+          r4(b, t + 1, offN, tid, kR4T);  // layout t + 1 = step t + 1's
+        } else {
+        auto r1_sync = [&]() {
+          if (with4)
+            asm volatile("bar.sync 2, %0;" ::"r"(kBT - kR4T) : "memory");
+          else
+            __syncthreads();
+        };
         const std::size_t bn = static_cast<std::size_t>(b) * N, bl = static_cast<std::size_t>(b) * L;
         const std::size_t so = sidx(d, t % d.S, b);
         int* nAc = V.nA_cur + bl;  // nA of layout t (parity slot par)
         int* nAw = V.nAb + static_cast<std::size_t>(par) * d.B * L + bl;
         // several slots per thread: queue the arrived heads in shared memory
         // and replay their link choices after the slot loop, one per thread
-        const bool defer = N - lg * kBT > nblk * kBT;
-        if (tid == 0) *hcnt = 0;
-        __syncthreads();
+        const bool defer = N - lg * n1 > nblk * n1;
+        if (t1 == 0) *hcnt = 0;
+        r1_sync();
         // kB3 slots per thread in flight; a slot's follower arrival flag is the
         // next lane's own (lanes are consecutive slots), so only a warp's last
         // lane replays its follower's car-following itself.
-        const int stride1 = nblk * kBT;
-        for (int k0 = lg * kBT + tid; k0 - lane < N; k0 += kB3 * stride1) {
+        const int stride1 = nblk * n1;
+        for (int k0 = lg * n1 + t1; k0 - lane < N; k0 += kB3 * stride1) {
           int kk[kB3], jj[kB3], rr[kB3], nn[kB3];
           double xx[kB3], xp[kB3], xf[kB3];
 #pragma unroll
@@ -357,7 +495,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
             if (r == n - 1) V.tail[bl + j] = x1;
             if (fa) {
               V.won[bn + k] = 0;
-              if (!(V.dbg & 4)) V.alist[bn + qa] = k;
+              if (!(V.dbg & 4)) V.alist[static_cast<std::size_t>(par) * d.B * N + bn + qa] = k;
               if (defer) {
                 const int hi = atomicAdd(hcnt, 1);
                 if (hi < kHeadCap) {
@@ -374,9 +512,10 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           }
         }
         if (defer) {
-          __syncthreads();
+          r1_sync();
           const int nh = min(*hcnt, kHeadCap);
-          for (int i = tid; i < nh; i += kBT) replay_head(V, b, t, hq[i], hq[kHeadCap + i], hq[2 * kHeadCap + i]);
+          for (int i = t1; i < nh; i += n1) replay_head(V, b, t, hq[i], hq[kHeadCap + i], hq[2 * kHeadCap + i]);
+        }
         }
       }
     bstamp(V, t, 1);
@@ -417,7 +556,8 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           const double tx = n_i ? V.tail[bl + i] : d.M;
           const bool vacant = tx > d.jam[bl + i];
           V.vac[bl + i] = vacant;
-          const int cnt = (V.dbg & 8) ? 0 : V.ccnt[bl + i];
+          const int cnt = (V.dbg & 8) ? 0 : V.ccnt[static_cast<std::size_t>(par) * d.B * L + bl + i];
+          V.ccnt[static_cast<std::size_t>(par ^ 1) * d.B * L + bl + i] = 0;  // for R1 of step t - 1
           int w = -1;
           if (vacant && cnt > 0) {
             if (cnt > kBwdCandCap) {
@@ -537,7 +677,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
             const int e = (i - lane) / nAp, q = i - e * nAp;
             T2 x{-INFINITY, -INFINITY, INT_MAX, -1};
             if (q < nA) {
-              const int s = V.alist[bn + q];
+              const int s = V.alist[static_cast<std::size_t>(par) * d.B * N + bn + q];
               const int id = d.aid[so + s];
               const std::uint64_t bits = rng_final(rng_prefix2(h1m, static_cast<std::uint64_t>(d.succ[s0 + e])),
                                                    static_cast<std::uint64_t>(id));
@@ -576,6 +716,10 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
     // ================= R3: merge VJP, A0 rows, position adjoint =================
     if (active)
       for (int b = b0; b < d.B; b += bstep) {
+        if (lg == 0 && tid == 0) {  // for R1 of step t - 1 (R4 of step t + 1 read them last)
+          V.acount[(par ^ 1) * d.B + b] = 0;
+          V.a0key[(par ^ 1) * d.B + b] = ULLONG_MAX;
+        }
         if (!grouped) {
           __syncthreads();
           const int* og = d.off + oidx(d, t % d.S, b);
@@ -594,7 +738,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         for (int i = spread(tid, lg, nblk); i < L && !(V.dbg & 64); i += nblk * kBT) {
           const int w = V.win[bl + i];
           if (w < 0) continue;
-          const int cnt = V.ccnt[bl + i];
+          const int cnt = V.ccnt[static_cast<std::size_t>(par) * d.B * L + bl + i];
           const Cand* cc = V.cands + (bl + i) * kBwdCandCap;
           const double abar_w = xbn[offN[i + 1] - 1] * d.M + 0.0;
           if (cnt <= kFastDeg) {  // registers; two_softmax_vjp's operation order
@@ -706,7 +850,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
                   const int nA = V.acount[par * d.B + b];
                   unsigned long long* keys = V.sort_scratch + (static_cast<std::size_t>(b) * d.maxdeg + e) * N;
                   for (int q = 0; q < nA; ++q) {
-                    const int s = V.alist[bn + q];
+                    const int s = V.alist[static_cast<std::size_t>(par) * d.B * N + bn + q];
                     const unsigned long long kk =
                         (static_cast<unsigned long long>(d.aid[so + s]) << 32) | static_cast<unsigned>(s);
                     int m = q - 1;
@@ -739,7 +883,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
                 const int j = d.lnk[so + ws];
                 const int r = ws - offT[j];
                 bool mover;
-                const int ns = map_next(V, b, ws, j, r, offT, offN, &mover);
+                const int ns = map_next(V, b, par, ws, j, r, offT, offN, &mover);
                 double ab;
                 if (mover) {
                   ab = 0.0 * d.M + 0.0;
@@ -784,14 +928,14 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               const double jam = d.jam[bl + j], dxf = d.dxf[bl + j], len = d.len[j];
               const double x = xx[q];
               const CfPick me = cf_step(x, r == 0 ? d.M : xp[q] - x, jam, dxf, len);
-              const double x1b = x1_bar_p(V, b, k, j, r, me.x1, offT, offN, xbn);
+              const double x1b = x1_bar_p(V, b, par, k, j, r, me.x1, offT, offN, xbn);
               xpb = d.tg ? x1b : (me.cap ? x1b : 0.0);
               const double dxcb = me.cong ? xpb : 0.0;
               dxfb = me.cong ? 0.0 : xpb;
               gapb = me.gap >= 0.0 ? dxcb * 1.0 : 0.0;
               if (lane == 31 && r + 1 < n) {
                 const CfPick fo = cf_step(xf[q], x - xf[q], jam, dxf, len);
-                const double f1b = x1_bar_p(V, b, k + 1, j, r + 1, fo.x1, offT, offN, xbn);
+                const double f1b = x1_bar_p(V, b, par, k + 1, j, r + 1, fo.x1, offT, offN, xbn);
                 const double fpb = d.tg ? f1b : (fo.cap ? f1b : 0.0);
                 const double fcb = fo.cong ? fpb : 0.0;
                 gnext = fo.gap >= 0.0 ? fcb * 1.0 : 0.0;
@@ -813,129 +957,18 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
     bstamp(V, t, 5);
     grid_sync();
     bstamp(V, t, 6);
-    // ================= R4: link-choice VJP, reductions, resets =================
-    if (active)
-      for (int b = b0; b < d.B; b += bstep) {
-        if (!grouped) {
-          __syncthreads();
-          const int* og = d.off + oidx(d, t % d.S, b);
-          for (int j = tid; j <= L; j += kBT) offT[j] = og[j];
-          __syncthreads();
-        }
-        const std::size_t bn = static_cast<std::size_t>(b) * N, bl = static_cast<std::size_t>(b) * L;
-        const std::size_t so = sidx(d, t % d.S, b);
-        double* vbc = V.vbar + (static_cast<std::size_t>(par) * d.B * N + bn) * d.maxdeg;
-        const unsigned long long key = V.a0key[par * d.B + b];
-        const int a0s = key == ULLONG_MAX ? -1 : static_cast<int>(key & 0xffffffffull);
-        const int nA = V.acount[par * d.B + b];
-        for (int q = spread(tid, lg, nblk); q < nA && !(V.dbg & 512); q += nblk * kBT) {
-          const int s = V.alist[bn + q];
-          const int c = V.choice[bn + s];
-          if (c < 0) continue;
-          const int j = d.lnk[so + s];
-          const int s0 = d.succ_off[j], deg = d.succ_off[j + 1] - s0;
-          const double* lz = d.slogz + (bl + j) * d.maxdeg;
-          const double* lp = V.lpi + (bn + s) * d.maxdeg;
-          const int ed = V.ched[bn + s];
-          const double lrow = (V.vac[bl + c] && V.win[bl + c] >= 0) ? V.lbar_row[bn + s] : 0.0;
-          const bool hit = V.vac[bl + c] && V.win[bl + c] >= 0;
-          const double* la0 = V.lbar_a0 + static_cast<std::size_t>(b) * d.maxdeg;
-          if (deg <= kFastDeg) {  // registers, same operation order as two_softmax_vjp
-            double bar[kFastDeg], pi[kFastDeg];
-            {  // pi from the replayed logits: softmax_stage2's operations
-              double yv[kFastDeg];
-#pragma unroll
-              for (int e = 0; e < kFastDeg; ++e) yv[e] = e < deg ? lp[e] : 0.0;
-              double m2 = yv[0];
-#pragma unroll
-              for (int e = 1; e < kFastDeg; ++e)
-                if (e < deg && m2 < yv[e]) m2 = yv[e];
-              double z2 = 0.0;
-#pragma unroll
-              for (int e = 0; e < kFastDeg; ++e) {
-                pi[e] = dexp(yv[e] - m2);
-                if (e < deg) z2 += pi[e];
-              }
-#pragma unroll
-              for (int e = 0; e < kFastDeg; ++e) pi[e] = e < deg ? pi[e] / z2 : 0.0;
-            }
-#pragma unroll
-            for (int e = 0; e < kFastDeg; ++e) {
-              const bool on = e < deg;
-              double v = (hit && e == ed) ? lrow : 0.0;
-              if (on && s == a0s) v += la0[e];
-              bar[e] = on ? ((v * 1.0) * 1.0) * (V.vac[bl + d.succ[s0 + e]] ? 1.0 : 0.0) : 0.0;
-            }
-            double dot = 0.0;
-#pragma unroll
-            for (int e = 0; e < kFastDeg; ++e)
-              if (e < deg) dot += bar[e] * pi[e];
-            double gs = 0.0;
-#pragma unroll
-            for (int e = 0; e < kFastDeg; ++e)
-              if (e < deg) {
-                bar[e] = (pi[e] * (bar[e] - dot)) * d.kinv;
-                gs += bar[e];
-              }
-#pragma unroll
-            for (int e = 0; e < kFastDeg; ++e)
-              if (e < deg) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e] - dexp(lz[e]) * gs;
-          } else {
-            double bar[kMaxDeg], pi[kMaxDeg];
-            {  // pi from the replayed logits: softmax_stage2's operations
-              double m2 = lp[0];
-              for (int e = 1; e < deg; ++e)
-                if (m2 < lp[e]) m2 = lp[e];
-              double z2 = 0.0;
-              for (int e = 0; e < deg; ++e) z2 += dexp(lp[e] - m2);
-              for (int e = 0; e < deg; ++e) pi[e] = dexp(lp[e] - m2) / z2;
-            }
-            for (int e = 0; e < deg; ++e) bar[e] = 0.0;
-            if (hit) bar[ed] = lrow;
-            if (s == a0s)
-              for (int e = 0; e < deg; ++e) bar[e] += la0[e];
-            for (int e = 0; e < deg; ++e)
-              bar[e] = ((bar[e] * 1.0) * 1.0) * (V.vac[bl + d.succ[s0 + e]] ? 1.0 : 0.0);
-            two_softmax_vjp(deg, lz, pi, d.kinv, bar);
-            for (int e = 0; e < deg; ++e) vbc[static_cast<std::size_t>(s) * d.maxdeg + e] = bar[e];
-          }
-        }
-        // warp per link: u, kappa, alpha for step t
-        double* g5 = V.grads + static_cast<std::size_t>(b) * 5 * L;
-        // thread per link (links dealt in 32-lane groups over the CTAs): the
-        // segment sums run in slot order; the parameter loads of the epilogue
-        // are issued together
-        for (int j = spread(tid, lg, nblk); j < L && !(V.dbg & 1024); j += nblk * kBT) {
-          const int base = offT[j], n = offT[j + 1] - base;
-          const double kap = d.kappa[bl + j];
-          const double g0 = g5[j], g1 = g5[L + j], g3 = g5[3 * L + j];
-          const int na = n ? V.nA_cur[bl + j] : 0;
-          double ub, jb;
-          link_sums8(V.cu + bn, V.cg + bn, base, n, ub, jb);
-          if (n) {
-            g5[j] = g0 + (0.0 + ub);
-            g5[L + j] = g1 + (0.0 - jb * static_cast<double>(d.delta_n) / (kap * kap));
-          }
-          double ab = 0.0;
-          for (int r = 0; r < na; ++r) {
-            const int s = base + r;
-            const int ch = V.choice[bn + s];
-            if (ch >= 0 && V.vac[bl + ch] && V.win[bl + ch] >= 0) ab += 1.0 * V.prio_bar[bn + s];
-          }
-          g5[3 * L + j] = g3 + ab;
-        }
-        for (int i = lg * kBT + tid; i < L; i += nblk * kBT) {
-          V.ccnt[bl + i] = 0;
-          V.dep[bl + i] = 0;
-        }
-        if (lg == 0 && tid == 0) {
-          V.acount[(par ^ 1) * d.B + b] = 0;
-          V.a0key[(par ^ 1) * d.B + b] = ULLONG_MAX;
-        }
-      }
-    bstamp(V, t, 7);
-    grid_sync();
+    bstamp(V, t, 7);  // R4 of this step runs with R1 of the next one
   }
+  // R4 of step 0
+  if (T > 0 && active)
+    for (int b = b0; b < d.B; b += bstep) {
+      __syncthreads();
+      const int* og = d.off + oidx(d, 0, b);
+      for (int j = tid; j <= L; j += kBT) offT[j] = og[j];
+      __syncthreads();
+      r4(b, 0, offT, tid, kBT);
+    }
+  grid_sync();
   // deferred preference gradient of step 0
   if (T > 0 && active)
     for (int b = b0; b < d.B; b += bstep) {

@@ -20,14 +20,14 @@ struct BView {
   int* dep;              // [B][L]
   int* win;              // [B][L]
   unsigned char* vac;    // [B][L]
-  int* ccnt;             // [B][L]
+  int* ccnt;             // [2][B][L] per step parity
   Cand* cands;           // [B][L][kBwdCandCap]
   double* mpi;           // [B][L][kBwdCandCap]
   double* mlz;           // [B][L][kBwdCandCap]
-  double* lpi;           // [B][N][maxdeg] link-choice pi of arrived heads
-  int* ched;             // [B][N] index of the chosen successor
-  int* choice;           // [B][N]
-  int* alist;            // [B][N]
+  double* lpi;           // [2][B][N][maxdeg] link-choice logits of arrived heads, per step parity
+  int* ched;             // [2][B][N] index of the chosen successor, per step parity
+  int* choice;           // [2][B][N] per step parity
+  int* alist;            // [2][B][N] per step parity
   int* acount;           // [2][B]
   unsigned long long* a0key;  // [2][B]
   void* a0part;          // [B][bps][maxdeg] per-CTA top-2 partials

@@ -1418,16 +1418,16 @@ static void run_backward_persistent(dtg_ctx* c, cudaStream_t st) {
   ch |= c->btail.ensure(BL);
   ch |= c->bmpi.ensure(BL * dtg::kBwdCandCap);
   ch |= c->bmlz.ensure(BL * dtg::kBwdCandCap);
-  ch |= c->blpi.ensure(BN * MD);
+  ch |= c->blpi.ensure(2 * BN * MD);  // per step parity (R4 of t+1 runs with R1 of t)
   ch |= c->bnA.ensure(2 * BL);
   ch |= c->bnAc.ensure(BL);
   ch |= c->bwon.ensure(BN);
   ch |= c->bdep.ensure(BL);
   ch |= c->bwin.ensure(BL);
-  ch |= c->bccnt.ensure(BL);
-  ch |= c->bched.ensure(BN);
-  ch |= c->bchoice.ensure(BN);
-  ch |= c->balist.ensure(BN);
+  ch |= c->bccnt.ensure(2 * BL);
+  ch |= c->bched.ensure(2 * BN);
+  ch |= c->bchoice.ensure(2 * BN);
+  ch |= c->balist.ensure(2 * BN);
   ch |= c->bacount.ensure(2 * B);
   ch |= c->bvac.ensure(BL);
   ch |= c->bcands.ensure(BL * dtg::kBwdCandCap);
@@ -1438,7 +1438,7 @@ static void run_backward_persistent(dtg_ctx* c, cudaStream_t st) {
   // vbar is shared with the step-graph reverse sweep, whose cached graph
   // (bwd_exec) captured its old pointer: a reallocation must invalidate it
   if (ch) c->drop_graphs();
-  CK(cudaMemsetAsync(c->bccnt.p, 0, BL * 4, st));
+  CK(cudaMemsetAsync(c->bccnt.p, 0, 2 * BL * 4, st));
   CK(cudaMemsetAsync(c->bdep.p, 0, BL * 4, st));
   CK(cudaMemsetAsync(c->bacount.p, 0, 2 * B * 4, st));
   CK(cudaMemsetAsync(c->ba0key.p, 0xff, 2 * B * 8, st));
