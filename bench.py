@@ -635,7 +635,7 @@ def run_throughput(P, torch, sc, p, lk0, ps0, args):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps / 1e3
 
-    for B, mode in ((64, 2), (64, 0), (256, 0)):
+    for B, mode in ((64, 2), (64, 0), (256, 3), (256, 0)):
         eng = P.Engine(sc, n_scenarios=B, max_steps=T_STEPS)
         eng.set_stream(torch.cuda.current_stream().cuda_stream)
         eng.set_mode(mode)
@@ -649,6 +649,16 @@ def run_throughput(P, torch, sc, p, lk0, ps0, args):
             "scenarios": B, **eng.last_schedule,
             "ms_per_batch": s * 1e3, "rtf_aggregate": B * SIM_SECONDS / s,
             "alg_GBps": alg / s / 1e9, "hbm_frac": alg / s / 1e9 / peak}
+        if eng.last_mode // 1000 == 4 and B == 256:
+            # DRAM bytes of the same launch under ncu (profiles/r02/ncu_scn_b256_metrics.csv)
+            dram = ncu_traffic("k_forward_scn")
+            if dram:
+                out[f"c3_dn30_B{B}_mode{mode}"].update({
+                    "alg_bytes_per_step": alg / T_STEPS, "ncu_dram_bytes_per_step": dram / T_STEPS,
+                    "ncu_dram_over_alg": dram / alg,
+                    "layout_floor_bytes_per_step": B * (32 * N + 64 * L),
+                    "note": "alg = SURVEY 16 B/agent (x read + write) + 64 B/link; the compacted layout moves "
+                            "position, id and link of every agent each step: 32 B/agent read + write is its floor"})
         del eng
     # C3 at dn = 1: 1,000,020 agents, 3,600 steps
     sc1 = P.Scenario.grid(GRID_N, LINK_LEN, NET_SEED, VIRT_LEN).configure(VEHICLES, 1, 3600, OBS_S)
