@@ -47,6 +47,10 @@ constexpr int kB3 = 2;  // R3 slots per thread in flight
 #define DTG_R4_THREADS 192
 #endif
 constexpr int kR4T = DTG_R4_THREADS;  // threads running R4 of step t + 1 beside R1 of step t
+#ifndef DTG_M3_THREADS
+#define DTG_M3_THREADS 128
+#endif
+constexpr int kM3T = DTG_M3_THREADS;  // R3 threads for the merge and A[0] rows (the rest: position adjoint)
 
 __device__ __forceinline__ int findl(const int* off_s, int L, int k) {
   int lo = 0, hi = L - 1;
@@ -606,51 +610,6 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
             }
           }
           V.win[bl + i] = w;
-          // deferred: preference gradient of step t+1 (its link-choice VJPs are ready)
-          if (t + 1 < T && !(V.dbg & 16)) {
-            double pb = 0.0;
-            const int e0 = d.pred_off[i], ne = d.pred_off[i + 1] - e0;
-            if (ne <= kFastDeg) {
-              // every predecessor's arrived count and first row load together;
-              // the sum then runs in (predecessor, row) order
-              int pbse[kFastDeg], nap[kFastDeg], pps[kFastDeg];
-              double v0[kFastDeg];
-#pragma unroll
-              for (int q = 0; q < kFastDeg; ++q) {
-                nap[q] = 0;
-                pbse[q] = 0;
-                pps[q] = 0;
-                if (q < ne) {
-                  const int p = d.pred[e0 + q];
-                  pps[q] = d.pred_pos[e0 + q];
-                  pbse[q] = offN[p];
-                  nap[q] = offN[p + 1] == pbse[q] ? 0 : nAn[p];
-                }
-              }
-#pragma unroll
-              for (int q = 0; q < kFastDeg; ++q)
-                v0[q] = nap[q] > 0 ? vbn[static_cast<std::size_t>(pbse[q]) * d.maxdeg + pps[q]] : 0.0;
-#pragma unroll
-              for (int q = 0; q < kFastDeg; ++q)
-                if (nap[q] > 0) {
-                  pb += v0[q] * 1.0;
-                  for (int r = 1; r < nap[q]; ++r)
-                    pb += vbn[static_cast<std::size_t>(pbse[q] + r) * d.maxdeg + pps[q]] * 1.0;
-                }
-            } else {
-              for (int q = 0; q < ne; ++q) {
-                const int p = d.pred[e0 + q];
-                const int pbse = offN[p];
-                if (offN[p + 1] == pbse) continue;
-                const int nap = nAn[p];
-                for (int r = 0; r < nap; ++r)
-                  pb += vbn[static_cast<std::size_t>(pbse + r) * d.maxdeg + d.pred_pos[e0 + q]] * 1.0;
-              }
-            }
-            const double cst = d.cost[bl + i], be = d.beta[bl + i];
-            g5[2 * L + i] += 0.0 + pb / cst;
-            g5[4 * L + i] += 0.0 - pb * be / (cst * cst);
-          }
           (void)sn;
         }
         } else {
@@ -708,6 +667,54 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           }
           asm volatile("bar.sync 1, %0;" ::"r"(kHalf) : "memory");
         }
+        // deferred: the preference gradient of step t+1 (its link-choice VJPs
+        // came from R4 of step t+1 in the phase before), on the A[0] half once
+        // its rows are done: the link half's merge replays are the longer chain
+        if (t + 1 < T && !(V.dbg & 16))
+          for (int i = spread(ta, lg, nblk); i < L; i += nblk * kHalf) {
+            double pb = 0.0;
+            const int e0 = d.pred_off[i], ne = d.pred_off[i + 1] - e0;
+            if (ne <= kFastDeg) {
+              // every predecessor's arrived count and first row load together;
+              // the sum then runs in (predecessor, row) order
+              int pbse[kFastDeg], nap[kFastDeg], pps[kFastDeg];
+              double v0[kFastDeg];
+#pragma unroll
+              for (int q = 0; q < kFastDeg; ++q) {
+                nap[q] = 0;
+                pbse[q] = 0;
+                pps[q] = 0;
+                if (q < ne) {
+                  const int p = d.pred[e0 + q];
+                  pps[q] = d.pred_pos[e0 + q];
+                  pbse[q] = offN[p];
+                  nap[q] = offN[p + 1] == pbse[q] ? 0 : nAn[p];
+                }
+              }
+#pragma unroll
+              for (int q = 0; q < kFastDeg; ++q)
+                v0[q] = nap[q] > 0 ? vbn[static_cast<std::size_t>(pbse[q]) * d.maxdeg + pps[q]] : 0.0;
+#pragma unroll
+              for (int q = 0; q < kFastDeg; ++q)
+                if (nap[q] > 0) {
+                  pb += v0[q] * 1.0;
+                  for (int r = 1; r < nap[q]; ++r)
+                    pb += vbn[static_cast<std::size_t>(pbse[q] + r) * d.maxdeg + pps[q]] * 1.0;
+                }
+            } else {
+              for (int q = 0; q < ne; ++q) {
+                const int p = d.pred[e0 + q];
+                const int pbse = offN[p];
+                if (offN[p + 1] == pbse) continue;
+                const int nap = nAn[p];
+                for (int r = 0; r < nap; ++r)
+                  pb += vbn[static_cast<std::size_t>(pbse + r) * d.maxdeg + d.pred_pos[e0 + q]] * 1.0;
+              }
+            }
+            const double cst = d.cost[bl + i], be = d.beta[bl + i];
+            g5[2 * L + i] += 0.0 + pb / cst;
+            g5[4 * L + i] += 0.0 - pb * be / (cst * cst);
+          }
         }
       }
     bstamp(V, t, 3);
@@ -734,8 +741,10 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         const std::size_t so = sidx(d, t % d.S, b);
         const double* xbn = V.xbar + static_cast<std::size_t>(par ^ 1) * d.B * N + bn;
         double* xbc = V.xbar + static_cast<std::size_t>(par) * d.B * N + bn;
-        // merge rows
-        for (int i = spread(tid, lg, nblk); i < L && !(V.dbg & 64); i += nblk * kBT) {
+        // merge rows and A[0] rows on the first kM3T threads, the position
+        // adjoint on the others: the merge-row chains overlap the slot chains
+        if (tid < kM3T) {
+        for (int i = spread(tid, lg, nblk); i < L && !(V.dbg & 64); i += nblk * kM3T) {
           const int w = V.win[bl + i];
           if (w < 0) continue;
           const int cnt = V.ccnt[static_cast<std::size_t>(par) * d.B * L + bl + i];
@@ -818,11 +827,11 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
         // slots in the interleaved mapping) merges row e's per-CTA partials and
         // writes lbar_a0[e] (0 for rows that take no A[0] routing)
         const unsigned long long key = lg == nblk - 1 ? V.a0key[par * d.B + b] : ULLONG_MAX;
-        if (lg == nblk - 1 && key != ULLONG_MAX && !(V.dbg & 128) && wid < d.maxdeg) {
+        if (lg == nblk - 1 && key != ULLONG_MAX && !(V.dbg & 128))
+        for (int e = wid; e < d.maxdeg; e += kM3T / 32) {
           const int a0s = static_cast<int>(key & 0xffffffffull);
           const int c0 = d.lnk[so + a0s];
           const int s0 = d.succ_off[c0], deg0 = d.succ_off[c0 + 1] - s0;
-          const int e = wid;
           bool routed = false;
           if (e < deg0) {
             const int i = d.succ[s0 + e];
@@ -897,12 +906,14 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
           }
           if (!routed && lane == 0) V.lbar_a0[static_cast<std::size_t>(b) * d.maxdeg + e] = 0.0;
         }
+        } else {
         // position adjoint of layout t: kB3 slots per thread in flight; the
         // follower's headway term is the follower lane's own gap adjoint
         // (lanes are consecutive slots), so only a warp's last lane evaluates
         // its follower's x1 adjoint itself.
-        const int stride3 = nblk * kBT;
-        for (int k0 = lg * kBT + tid; k0 - lane < N && !(V.dbg & 256); k0 += kB3 * stride3) {
+        const int t3 = tid - kM3T, n3 = kBT - kM3T;
+        const int stride3 = nblk * n3;
+        for (int k0 = lg * n3 + t3; k0 - lane < N && !(V.dbg & 256); k0 += kB3 * stride3) {
           int kk[kB3], jj[kB3], rr[kB3], nn[kB3];
           double xx[kB3], xp[kB3], xf[kB3];
 #pragma unroll
@@ -952,6 +963,7 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
               V.cg[bn + k] = gapb;
             }
           }
+        }
         }
       }
     bstamp(V, t, 5);
