@@ -301,11 +301,11 @@ def test_sioux_falls_transfer_events_against_reference(dn):
     assert np.array_equal(tr.transfers, d["events"])
 
 
-@pytest.mark.parametrize("mode", [0, 1, 3])
+@pytest.mark.parametrize("mode", [0, 1, 3, 4])
 def test_c3_transfer_events_every_schedule_against_port(port, mode):
     """C3 (1,000,020 vehicles, dn=30, 1 h), 8 draws batched: the recorded
     events equal the link changes of the port's per-step states, on the fused
-    grid, the cluster and the step-graph schedules."""
+    grid, the cluster, the step-graph and the scenario-resident schedules."""
     T, B = 120, 8
     sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 30, T, 300)
     p = sc.sample_parameters(3)

@@ -148,9 +148,10 @@ def test_speculative_head_decisions_are_exact(n, length, veh, dn, T, B, mode):
 
 def test_mode_toggles_on_one_engine_keep_backward_exact():
     """One context, reverse sweeps alternating between the step graph (mode 3)
-    and the persistent kernel (mode 0): the persistent sweep grows the shared
-    vbar buffer, which the cached step-graph sweep captured, so the graph must
-    be rebuilt (stale vbar pointer in bwd_exec)."""
+    and the persistent kernel (mode 0, and after a scenario-resident forward,
+    mode 4): the persistent sweep grows the shared vbar buffer, which the
+    cached step-graph sweep captured, so the graph must be rebuilt (ADVICE r1:
+    stale vbar pointer in bwd_exec)."""
     sc = P.Scenario.grid(6, 300.0, 42, 1000.0).configure(2400, 2, 120, 300)
     p = sc.sample_parameters(3)
     spi, T, B = sc.steps_per_interval, 120, 3
@@ -164,7 +165,7 @@ def test_mode_toggles_on_one_engine_keep_backward_exact():
     for b in range(B):
         e.set_noise(7, 40 + b, b)
     got = []
-    for mode in (3, 0, 3, 0, 3):
+    for mode in (3, 0, 3, 4, 0, 3):
         e.set_mode(mode)
         e.forward(T, spi, checkpoint=True)
         got.append(e.backward(snap_seeds=snap, x_seeds=xs))
