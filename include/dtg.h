@@ -281,6 +281,28 @@ int dtg_gradient_device_loss(dtg_ctx* ctx, double* d_rows);
 int dtg_reduce_draw_rows(dtg_ctx* ctx, int n_draws, const double* d_rows,
                          int mode, double* out);
 
+/* The draw-ordered reduction of dtg_reduce_draw_rows, kept on the device;
+ * only head[2] = (loss, extra) crosses to the host.  dtg_read_reduced_row
+ * copies the whole row [5L+2] of the last reduction. */
+int dtg_reduce_draw_rows_head(dtg_ctx* ctx, int n_draws, const double* d_rows, int mode, double* head);
+int dtg_read_reduced_row(dtg_ctx* ctx, double* out);
+
+/* Device-resident calibrate step (optimization.cpp:10-59, 173-205), bit-
+ * identical to the host loop: raw[4L] = (u, kappa, beta, alpha) in raw space,
+ * BoundedTransform ranges lo[4] / hi[4], AdamW settings.  init uploads raw,
+ * zeroes the moments and sets the context's (u, kappa, beta, alpha) of every
+ * scenario to the realised raw (cost as last set; set parameters first).
+ * step: gradient of the last device reduction (mode 0) / draws through the
+ * transform's derivative, AdamW with bias corrections bc1 = 1 - beta1^t,
+ * bc2 = 1 - beta2^t, and the parameters of the new raw.  mark_best keeps a
+ * device copy of the current raw; read copies raw and / or that copy (either
+ * may be NULL). */
+int dtg_opt_bounded_init(dtg_ctx* ctx, const double* raw, const double* lo, const double* hi, double lr,
+                         double beta1, double beta2, double eps, double weight_decay);
+int dtg_opt_bounded_step(dtg_ctx* ctx, int draws, double bc1, double bc2);
+int dtg_opt_bounded_mark_best(dtg_ctx* ctx);
+int dtg_opt_bounded_read(dtg_ctx* ctx, double* raw, double* best_raw);
+
 /* Measurement hook: run n_steps of the forward (backward != 0: the reverse
  * sweep of the preceding checkpointed forward) without graphs, bracketing
  * every kernel with CUDA events on the context stream.  ms_out[w] receives
@@ -429,7 +451,9 @@ typedef struct {
 
 /* calibrate (optimization.cpp:122-219) with the device iteration: per
  * iteration one batched forward + reverse sweep over the noise draws, MSE
- * loss/seeds and the draw sum on the device, transform + AdamW on the host.
+ * loss/seeds and the draw sum on the device, and the transform + AdamW step
+ * on the device too (dtg_opt_bounded_*, bit-identical to the host loop's
+ * glibc arithmetic): only (loss, extra) crosses to the host per iteration.
  * init_* may be NULL (start from raw 0 = range midpoints, cost 1);
  * init_cost may be NULL alone.  loss_curve has room for max_iterations.
  * Returns DTG_ERR_DIVERGENCE on a non-finite loss. */

@@ -121,6 +121,12 @@ SIGNATURES = [
     ("dtg_set_loss_control", i32, [vp, i32, C.c_double]),
     ("dtg_gradient_device_loss", i32, [vp, vp]),
     ("dtg_reduce_draw_rows", i32, [vp, i32, vp, i32, _dp]),
+    ("dtg_reduce_draw_rows_head", i32, [vp, i32, vp, i32, _dp]),
+    ("dtg_read_reduced_row", i32, [vp, _dp]),
+    ("dtg_opt_bounded_init", i32, [vp, _dp, _dp, _dp] + [C.c_double] * 5),
+    ("dtg_opt_bounded_step", i32, [vp, i32, C.c_double, C.c_double]),
+    ("dtg_opt_bounded_mark_best", i32, [vp]),
+    ("dtg_opt_bounded_read", i32, [vp, vp, vp]),
     ("dtg_device_cum", vp, [vp]),
     ("dtg_profile_kernels", i32, [vp, i32, i32, i32, _dp, C.POINTER(C.c_int64)]),
     ("dtg_kernel_name", C.c_char_p, [i32, i32]),

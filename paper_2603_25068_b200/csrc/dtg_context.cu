@@ -18,6 +18,7 @@
 #include "dtg_cluster.h"
 #include "dtg_backward.h"
 #include "dtg_loss.h"
+#include "dtg_device.cuh"
 
 namespace dtg {
 cudaError_t decision_stats_fused(int force, unsigned long long* count);
@@ -231,6 +232,12 @@ struct dtg_ctx {
   DevBuf<int> loss_ids, loss_first, loss_next;
   DevBuf<double> loss_obs, loss_val, loss_extra, rows, red;
   double* h_red = nullptr;
+  // device-resident calibrate step (dtg_opt_bounded_*): raw [4][L], the Adam
+  // moments, the raw of the best iteration
+  DevBuf<double> opt_raw, opt_m, opt_v, opt_best;
+  double opt_lo[4] = {0, 0, 0, 0}, opt_hi[4] = {0, 0, 0, 0};
+  double opt_lr = 0, opt_b1 = 0, opt_b2 = 0, opt_eps = 0, opt_wd = 0;
+  bool opt_ready = false;
   // graphs
   cudaGraphExec_t fwd_exec = nullptr, bwd_exec = nullptr;
   long long fwd_key = -1, bwd_key = -1;
@@ -1724,6 +1731,151 @@ int dtg_reduce_draw_rows(dtg_ctx* c, int n_draws, const double* d_rows, int mode
     CK(cudaMemcpyAsync(c->h_red, c->red.p, R * 8, cudaMemcpyDeviceToHost, st));
     c->sync_check();
     std::memcpy(out, c->h_red, R * 8);
+  });
+}
+
+// ---- device-resident calibrate step -------------------------------------------------
+// The host loop of calibrate (optimization.cpp:173-205) realises (u, kappa,
+// beta, alpha) from raw through BoundedTransform, chains the draw-summed
+// gradient through its derivative and takes an AdamW step (optimization.cpp:
+// 10-59).  The same operations run here on the device, in the same order,
+// with glibc's exp restated (dexp) and IEEE sqrt / division: the raw
+// trajectory is bit-identical to the host's, and an iteration no longer waits
+// for a 100 KB gradient row to cross PCIe and 20k host exponentials.
+namespace {
+struct OptArgs {
+  double lo[4], hi[4];
+  double lr, b1, b2, eps, wd, bc1, bc2, draws;
+  int step;  // 0: realise only
+};
+__device__ __forceinline__ double sigmoid_branchy_d(double r) {
+  return r >= 0.0 ? 1.0 / (1.0 + dtg::dexp(-r)) : dtg::dexp(r) / (1.0 + dtg::dexp(r));
+}
+__global__ void k_opt_bounded(double* raw, double* m, double* v, const double* red, OptArgs a, double* params,
+                              int L, int B) {
+  const std::size_t n = static_cast<std::size_t>(4) * L;
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const int q = static_cast<int>(i / L), l = static_cast<int>(i % L);
+    const double lo = a.lo[q], hi = a.hi[q];
+    double r = raw[i];
+    if (a.step) {
+      const double s = sigmoid_branchy_d(r);
+      const double g = red[i] / a.draws * ((hi - lo) * s * (1.0 - s));  // rg = red / draws * dvalue(raw)
+      const double mi = a.b1 * m[i] + (1.0 - a.b1) * g;
+      const double vi = a.b2 * v[i] + (1.0 - a.b2) * g * g;
+      m[i] = mi;
+      v[i] = vi;
+      const double mhat = mi / a.bc1;
+      const double vhat = vi / a.bc2;
+      r -= a.lr * (mhat / (sqrt(vhat) + a.eps) + a.wd * r);
+      raw[i] = r;
+    }
+    const double p = lo + (hi - lo) * sigmoid_branchy_d(r);  // BoundedTransform::value
+    for (int b = 0; b < B; ++b) params[(static_cast<std::size_t>(q) * B + b) * L + l] = p;
+  }
+}
+void launch_opt(dtg_ctx* c, int step, int draws, double bc1, double bc2) {
+  OptArgs a{};
+  for (int q = 0; q < 4; ++q) {
+    a.lo[q] = c->opt_lo[q];
+    a.hi[q] = c->opt_hi[q];
+  }
+  a.lr = c->opt_lr;
+  a.b1 = c->opt_b1;
+  a.b2 = c->opt_b2;
+  a.eps = c->opt_eps;
+  a.wd = c->opt_wd;
+  a.bc1 = bc1;
+  a.bc2 = bc2;
+  a.draws = static_cast<double>(draws);
+  a.step = step;
+  const int n = 4 * c->L;
+  k_opt_bounded<<<(n + 255) / 256, 256, 0, c->stream>>>(c->opt_raw.p, c->opt_m.p, c->opt_v.p, c->red.p, a,
+                                                         c->params.p, c->L, c->B);
+  CK(cudaGetLastError());
+}
+}  // namespace
+
+int dtg_opt_bounded_init(dtg_ctx* c, const double* raw, const double* lo, const double* hi, double lr,
+                         double beta1, double beta2, double eps, double weight_decay) {
+  return guarded(c, [&] {
+    for (int b = 0; b < c->B; ++b)
+      if (!c->have_params[b]) throw std::invalid_argument("set the parameters (incl. cost) first");
+    const std::size_t n = 4 * static_cast<std::size_t>(c->L);
+    c->opt_raw.ensure(n);
+    c->opt_m.ensure(n);
+    c->opt_v.ensure(n);
+    c->opt_best.ensure(n);
+    for (int q = 0; q < 4; ++q) {
+      c->opt_lo[q] = lo[q];
+      c->opt_hi[q] = hi[q];
+    }
+    c->opt_lr = lr;
+    c->opt_b1 = beta1;
+    c->opt_b2 = beta2;
+    c->opt_eps = eps;
+    c->opt_wd = weight_decay;
+    CK(cudaMemcpyAsync(c->opt_raw.p, raw, n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->opt_m.p, 0, n * 8, c->stream));
+    CK(cudaMemsetAsync(c->opt_v.p, 0, n * 8, c->stream));
+    CK(cudaMemcpyAsync(c->opt_best.p, c->opt_raw.p, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    launch_opt(c, 0, 1, 1.0, 1.0);  // the parameters of raw
+    CK(cudaStreamSynchronize(c->stream));  // raw is the caller's
+    c->opt_ready = true;
+  });
+}
+
+int dtg_opt_bounded_step(dtg_ctx* c, int draws, double bc1, double bc2) {
+  return guarded(c, [&] {
+    if (!c->opt_ready) throw std::runtime_error("dtg_opt_bounded_init first");
+    if (draws < 1) throw std::invalid_argument("no noise draws");
+    launch_opt(c, 1, draws, bc1, bc2);
+  });
+}
+
+int dtg_opt_bounded_mark_best(dtg_ctx* c) {
+  return guarded(c, [&] {
+    if (!c->opt_ready) throw std::runtime_error("dtg_opt_bounded_init first");
+    CK(cudaMemcpyAsync(c->opt_best.p, c->opt_raw.p, 4 * static_cast<std::size_t>(c->L) * 8,
+                       cudaMemcpyDeviceToDevice, c->stream));
+  });
+}
+
+int dtg_opt_bounded_read(dtg_ctx* c, double* raw, double* best_raw) {
+  return guarded(c, [&] {
+    if (!c->opt_ready) throw std::runtime_error("dtg_opt_bounded_init first");
+    const std::size_t n = 4 * static_cast<std::size_t>(c->L);
+    if (raw) CK(cudaMemcpyAsync(raw, c->opt_raw.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (best_raw) CK(cudaMemcpyAsync(best_raw, c->opt_best.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int dtg_reduce_draw_rows_head(dtg_ctx* c, int n_draws, const double* d_rows, int mode, double* head) {
+  return guarded(c, [&] {
+    if (mode != 0 && mode != 1) throw std::invalid_argument("reduce mode must be 0 or 1");
+    if (n_draws < 1) throw std::invalid_argument("no noise draws");
+    if (!d_rows && n_draws > c->B)
+      throw std::invalid_argument("internal draw rows hold only B scenarios");
+    const std::size_t R = 5 * static_cast<std::size_t>(c->L) + 2;
+    c->red.ensure(R);
+    if (!c->h_red) CK(cudaMallocHost(&c->h_red, R * 8));
+    cudaStream_t st = c->stream;
+    dtg::launch_reduce_rows(n_draws, c->L, d_rows ? d_rows : c->rows.p, mode, c->red.p, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->h_red + (R - 2), c->red.p + (R - 2), 2 * 8, cudaMemcpyDeviceToHost, st));
+    c->sync_check();
+    head[0] = c->h_red[R - 2];
+    head[1] = c->h_red[R - 1];
+  });
+}
+
+int dtg_read_reduced_row(dtg_ctx* c, double* out) {
+  return guarded(c, [&] {
+    const std::size_t R = 5 * static_cast<std::size_t>(c->L) + 2;
+    if (c->red.n < R) throw std::runtime_error("no reduced row");
+    CK(cudaMemcpy(out, c->red.p, R * 8, cudaMemcpyDeviceToHost));
   });
 }
 

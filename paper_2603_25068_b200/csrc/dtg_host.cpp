@@ -892,12 +892,32 @@ class DeviceLoop {
     return red_;
   }
 
+  /// The same iteration with the parameters already on the device (set by
+  /// dtg_opt_bounded_*): the reduced row stays there, head = (loss, extra).
+  const double* run_head(const RngStream& rng, const std::vector<std::uint64_t>& its, int mode) {
+    for (int b = 0; b < local_; ++b)
+      check(ctx_, dtg_set_noise(ctx_, b, rng.seed(), its[first_ + b]));
+    check(ctx_, dtg_forward(ctx_, s_.horizon_steps, spi_, 1));
+    const bool shared = ex_ && ex_->world > 1;
+    check(ctx_, dtg_gradient_device_loss(ctx_, shared ? ex_->d_local : nullptr));
+    if (shared) ex_->gather();
+    check(ctx_, dtg_reduce_draw_rows_head(ctx_, draws_, shared ? ex_->d_full : nullptr, mode, head_));
+    return head_;
+  }
+
+  /// The whole reduced row of the last run_head.
+  const std::vector<double>& full_row() {
+    check(ctx_, dtg_read_reduced_row(ctx_, red_.data()));
+    return red_;
+  }
+
  private:
   const Scenario& s_;
   int draws_, local_ = 1, first_ = 0, spi_ = 1, N_ = 0, L_ = 0;
   const DrawExchange* ex_;
   dtg_ctx* ctx_ = nullptr;
   std::vector<double> red_;
+  double head_[2] = {0.0, 0.0};
   void* prev_stream_ = nullptr;
   int prev_owned_ = 1;
   bool rebound_ = false;
@@ -974,35 +994,46 @@ CalibrationResult calibrate(const Scenario& s, const CountSeries& obs, const Par
                                        static_cast<int>(obs.link_ids.size()),
                                        obs.link_ids.data(), flat.data()));
   }
-  AdamW adam(4 * L, cfg.adam);
+  // the fixed cost and the starting parameters, then raw, the transforms and
+  // AdamW on the device (dtg_opt_bounded_*: the host loop's operations, bit-
+  // identical); per iteration only (loss, extra) crosses to the host
+  {
+    const LinkParams p0 = realize(raw);
+    check(loop.ctx(), dtg_set_params(loop.ctx(), -1, p0.u.data(), p0.kappa.data(), p0.beta.data(),
+                                     p0.alpha.data(), p0.cost.data()));
+    const double lo[4] = {bounds.u_lo, bounds.kappa_lo, bounds.beta_lo, bounds.alpha_lo};
+    const double hi[4] = {bounds.u_hi, bounds.kappa_hi, bounds.beta_hi, bounds.alpha_hi};
+    check(loop.ctx(), dtg_opt_bounded_init(loop.ctx(), raw.data(), lo, hi, cfg.adam.lr, cfg.adam.beta1,
+                                           cfg.adam.beta2, cfg.adam.eps, cfg.adam.weight_decay));
+  }
   CalibrationResult res;
   res.best_loss = std::numeric_limits<double>::infinity();
   int since_best = 0;
   for (int it = 0; it < cfg.max_iterations; ++it) {
-    const LinkParams params = realize(raw);
-    const auto& red = loop.run(params, rng, iteration_noise(cfg, it, draws), 0);
-    const double loss = red[5 * static_cast<std::size_t>(L)];
+    const double* head = loop.run_head(rng, iteration_noise(cfg, it, draws), 0);
+    const double loss = head[0];
     res.loss_curve.push_back(loss);
     res.iterations = it + 1;
     if (!std::isfinite(loss))
       throw DivergenceError("calibration diverged at iteration " + std::to_string(it) +
-                            " (non-finite " + nan_block_of(red, L) + ")");
+                            " (non-finite " + nan_block_of(loop.full_row(), L) + ")");
     if (loss < res.best_loss) {
       res.best_loss = loss;
-      res.best_params = params;
       res.best_iteration = it;
+      check(loop.ctx(), dtg_opt_bounded_mark_best(loop.ctx()));
       since_best = 0;
     } else if (++since_best >= cfg.patience) {
       break;
     }
-    std::vector<double> rg(4 * static_cast<std::size_t>(L));
-    for (int l = 0; l < L; ++l) {
-      rg[l] = red[l] / draws * tu.dvalue(raw[l]);
-      rg[L + l] = red[L + l] / draws * tk.dvalue(raw[L + l]);
-      rg[2 * L + l] = red[2 * L + l] / draws * tb.dvalue(raw[2 * L + l]);
-      rg[3 * L + l] = red[3 * L + l] / draws * ta.dvalue(raw[3 * L + l]);
-    }
-    adam.step(raw, rg);
+    // AdamW::step's bias corrections for step t = it + 1
+    const double bc1 = 1.0 - std::pow(cfg.adam.beta1, it + 1);
+    const double bc2 = 1.0 - std::pow(cfg.adam.beta2, it + 1);
+    check(loop.ctx(), dtg_opt_bounded_step(loop.ctx(), draws, bc1, bc2));
+  }
+  if (res.best_iteration >= 0) {
+    std::vector<double> best(4 * static_cast<std::size_t>(L));
+    check(loop.ctx(), dtg_opt_bounded_read(loop.ctx(), nullptr, best.data()));
+    res.best_params = realize(best);
   }
   res.wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
   return res;
