@@ -264,6 +264,30 @@ def test_sioux_falls_forward_against_reference(dn):
 
 
 @pytest.mark.parametrize("dn", [4, 1])
+def test_sioux_falls_scenario_resident_forward_against_reference(dn):
+    """The scenario-resident schedule (mode 4, one CTA per scenario) on the
+    reference's own irregular network: counts and final state bit-exact."""
+    from oracle.oracle import fnv1a64_c
+
+    d = _need(f"sf_dn{dn}")
+    T = int(d["meta"][2])
+    sc = sf_scenario(d, T)
+    p = P.LinkParams(*d["params"])
+    lk, ps = sc.seed_agents()
+    e = P.Engine(sc, 1, T)
+    e.set_mode(4)
+    e.set_params(p)
+    e.set_state(lk, ps)
+    e.set_noise(42, 0, 0)
+    e.forward(T, 300 // dn)
+    assert e.last_mode // 1000 == 4
+    cum = e.read_cum(0)
+    assert fnv1a64_c(cum) == int(d["fnv_cum"])
+    fl, fp = e.read_state(0, T)
+    assert np.array_equal(fl, d["link"]) and np.array_equal(fp, d["pos"])
+
+
+@pytest.mark.parametrize("dn", [4, 1])
 def test_sioux_falls_gradient_against_reference(dn):
     """The calibration loss (mse_loss_builder over the physical links) on
     Sioux Falls over the 30-min observation window."""
@@ -343,7 +367,8 @@ def test_c3_dn1_300_steps_against_port(port):
 @pytest.mark.parametrize("B", [64, 256])
 def test_c3_batched_nowcast_draws_against_port(port, B):
     """The batched throughput configuration (B independent C3 nowcasts in one
-    pass: the step graph) — first, middle and last draw against the port."""
+    pass: the step graph at B=64, scenario-resident CTAs at B=256) — first,
+    middle and last draw against the port."""
     sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 30, 120, 300)
     p = sc.sample_parameters(3)
     its = [1000 + b for b in range(B)]
