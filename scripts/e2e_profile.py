@@ -4,6 +4,9 @@ import os, sys, time, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
+from paper_2603_25068_b200 import _lib
+if len(sys.argv) > 1:  # another build (scripts/build_variants.sh)
+    _lib.load_other(sys.argv[1])
 import paper_2603_25068_b200 as P
 from paper_2603_25068_b200._lib import ptr
 
