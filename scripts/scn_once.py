@@ -1,6 +1,9 @@
 """One scenario-resident (mode 4) C3 forward after a warm-up, for ncu: scn_once.py B [T]."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2603_25068_b200 import _lib
+if os.environ.get("DTG_LIB"):  # another build (scripts/build_variants.sh)
+    _lib.load_other(os.environ["DTG_LIB"])
 import paper_2603_25068_b200 as P
 B = int(sys.argv[1]); T = int(sys.argv[2]) if len(sys.argv) > 2 else 120
 sc = P.Scenario.grid(23, 1609.34, 42, 1000.0).configure(1000020, 30, T, 300)
