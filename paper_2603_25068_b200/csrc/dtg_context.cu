@@ -1875,7 +1875,8 @@ int dtg_read_reduced_row(dtg_ctx* c, double* out) {
   return guarded(c, [&] {
     const std::size_t R = 5 * static_cast<std::size_t>(c->L) + 2;
     if (c->red.n < R) throw std::runtime_error("no reduced row");
-    CK(cudaMemcpy(out, c->red.p, R * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(out, c->red.p, R * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 
