@@ -32,6 +32,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef DTG_BAR_BACKOFF
+#define DTG_BAR_BACKOFF 32  // ns between grid-barrier polls: C3 nowcast 1.305 -> 1.295 ms
+#endif
+
 namespace dtg {
 
 namespace {
@@ -240,6 +244,9 @@ __global__ void __launch_bounds__(kBT) k_backward_persistent(BView V) {
       unsigned int v;
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(V.gbar) : "memory");
+#if DTG_BAR_BACKOFF
+            if (v < target) __nanosleep(DTG_BAR_BACKOFF);
+#endif
       } while (v < target);
     }
     __syncthreads();

@@ -36,6 +36,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef DTG_BAR_BACKOFF
+#define DTG_BAR_BACKOFF 32  // ns between grid-barrier polls: C3 nowcast 1.305 -> 1.295 ms
+#endif
+
 namespace dtg {
 
 namespace {
@@ -337,6 +341,9 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ep
     unsigned int v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+#if DTG_BAR_BACKOFF
+            if (v < target) __nanosleep(DTG_BAR_BACKOFF);
+#endif
     } while (v < target);
   }
   __syncthreads();
@@ -786,6 +793,9 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_forward_fused(CView V) {
           unsigned int v;
           do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(V.gbar) : "memory");
+#if DTG_BAR_BACKOFF
+            if (v < target) __nanosleep(DTG_BAR_BACKOFF);
+#endif
           } while (v < target);
         }
         asm volatile("bar.sync 1, 64;" ::: "memory");
