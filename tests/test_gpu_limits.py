@@ -2,7 +2,8 @@
 more than 16 successors is rejected when the context is built; a merge row
 with more than 16 candidates in one step is rejected by the persistent
 kernels (16 register / shared-memory candidate slots) and handled by the step
-graph (32), whose result must equal the C port's."""
+graph and the scenario-resident schedule (32), whose results must equal the C
+port's."""
 import numpy as np
 import pytest
 
@@ -66,16 +67,18 @@ def test_merge_with_17_candidates(port):
     with pytest.raises(P.UnsupportedError, match="candidates"):
         e.forward(T, 1)
         e.sync()
-    # step graph (32 slots): exact, against the port
-    e = P.Engine(sc, 1, T)
-    e.set_mode(3)
-    e.set_params(p)
-    e.set_state(lk, ps)
-    e.set_noise(7, 0, 0)
-    e.forward(T, 1, checkpoint=True)
-    cum = e.read_cum(0)
-    fl, fp = e.read_state(0, T)
+    # step graph and scenario-resident CTAs (32 slots): exact, against the port
     ref = PortScenario(port, frm, to, length, link0=lk, pos0=ps, horizon_steps=T, obs_interval_s=1).forward(p, 7, 0)
-    assert np.array_equal(cum, ref["cum_per_step"])
-    assert np.array_equal(fl, ref["link"]) and np.array_equal(fp, ref["pos"])
-    assert 1 <= (fl == L - 2).sum() <= T  # at most one admission into the merge link per step
+    for mode in (3, 4):
+        e = P.Engine(sc, 1, T)
+        e.set_mode(mode)
+        e.set_params(p)
+        e.set_state(lk, ps)
+        e.set_noise(7, 0, 0)
+        e.forward(T, 1, checkpoint=True)
+        assert e.last_mode // 1000 == mode
+        cum = e.read_cum(0)
+        fl, fp = e.read_state(0, T)
+        assert np.array_equal(cum, ref["cum_per_step"]), mode
+        assert np.array_equal(fl, ref["link"]) and np.array_equal(fp, ref["pos"]), mode
+        assert 1 <= (fl == L - 2).sum() <= T  # at most one admission into the merge link per step
