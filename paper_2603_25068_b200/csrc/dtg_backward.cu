@@ -46,7 +46,10 @@ namespace {
 constexpr int kBT = DTG_BWD_THREADS;  // threads per CTA
 constexpr int kFastDeg = 5;  // successor counts up to this take unrolled register paths
 constexpr int kHeadCap = 1024;  // deferred arrived heads per CTA (overflow runs inline)
-constexpr int kB3 = 2;  // R3 slots per thread in flight
+#ifndef DTG_KB3
+#define DTG_KB3 2
+#endif
+constexpr int kB3 = DTG_KB3;  // R1 / R3 slots per thread in flight
 #ifndef DTG_R4_THREADS
 #define DTG_R4_THREADS 192
 #endif
