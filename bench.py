@@ -635,7 +635,7 @@ def run_throughput(P, torch, sc, p, lk0, ps0, args):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps / 1e3
 
-    for B, mode in ((64, 2), (64, 0), (256, 3), (256, 0)):
+    for B, mode in ((64, 2), (64, 0), (128, 3), (128, 0), (256, 3), (256, 0)):
         eng = P.Engine(sc, n_scenarios=B, max_steps=T_STEPS)
         eng.set_stream(torch.cuda.current_stream().cuda_stream)
         eng.set_mode(mode)

@@ -1101,10 +1101,14 @@ int dtg_forward(dtg_ctx* c, int T, int spi, int checkpoint) {
     // 9.91 vs 7.41; scripts/graph_time.py)
     if (c->mode == 0 && mode == 2 && c->N > dtg::kClusterThreads && 5 * c->B > c->pgrid_max) mode = 3;
     if (!c->persistent && c->mode == 0) mode = 3;
-    // auto: beyond ~1.2 scenarios per SM, one CTA per scenario beats the step
-    // graph (C3 ms/nowcast graph vs mode 4: B=160 17.2 vs 18.6, B=192 21.1 vs
-    // 19.4, B=256 27.9 vs 20.6; scripts/scn_time.py)
-    if (c->mode == 0 && c->persistent && mode == 3 && 5 * c->B > 6 * c->n_sm) mode = 4;
+    // auto: one CTA per scenario beats the step graph from ~0.55 scenarios per
+    // SM (a 768-thread CTA per SM) and beyond ~1.2 (two 384-thread CTAs per
+    // SM); C3 ms/nowcast graph vs mode 4: B=64 8.1 vs 9.0, B=80 9.5 vs 9.5,
+    // B=96 11.2 vs 9.8, B=148 15.8 vs 10.9, B=160 17.2 vs 18.6, B=192 21.1 vs
+    // 19.4, B=256 27.9 vs 20.3 (scripts/scn_time.py)
+    if (c->mode == 0 && c->persistent && mode == 3 &&
+        ((20 * c->B >= 11 * c->n_sm && c->B <= c->n_sm) || 5 * c->B > 6 * c->n_sm))
+      mode = 4;
     if (mode == 4 && !c->scn_ok) mode = 3;  // per-link state exceeds shared memory
     c->last_mode = mode;
     scn = mode == 4;

@@ -134,7 +134,17 @@ __device__ __noinline__ void scn_merge_wide(const DevView& d, int b, int t, int 
   }
 }
 
-__global__ void __launch_bounds__(kScnThreads, 2) k_forward_scn(DevView d, int T, unsigned long long* stamps) {
+#ifndef DTG_SCN_WIDE
+#define DTG_SCN_WIDE 768
+#endif
+constexpr int kScnWide = DTG_SCN_WIDE;  // threads of the one-scenario-per-SM CTA
+
+// kT threads per CTA, kM CTAs per SM: 384 x 2 when the batch fills the SMs
+// twice over, 768 x 1 (twice the threads per scenario) when each scenario has
+// an SM to itself
+template <int kT, int kM>
+__global__ void __launch_bounds__(kT, kM) k_forward_scn(DevView d, int T, unsigned long long* stamps) {
+  constexpr int kScnThreads = kT;
   __shared__ int sm[32];
   __shared__ unsigned long long smin[32];
   __shared__ int cnt[3];  // [0] links with arrived heads, [1] chosen links, [2] most heads on a link (stamps)
@@ -335,9 +345,22 @@ bool forward_scn_ok(int L) {
 
 cudaError_t launch_forward_scn(const DevView& d, int T, unsigned long long* stamps, cudaStream_t st) {
   const std::size_t sm = forward_scn_smem(d.L);
-  cudaError_t e = cudaFuncSetAttribute(k_forward_scn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  const int nb = d.nb ? d.nb : d.B;
+  int dev = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  k_forward_scn<<<d.nb ? d.nb : d.B, kScnThreads, sm, st>>>(d, T, stamps);
+  if (nb <= sms) {  // one scenario per SM: the wide CTA
+    e = cudaFuncSetAttribute(k_forward_scn<kScnWide, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sm));
+    if (e != cudaSuccess) return e;
+    k_forward_scn<kScnWide, 1><<<nb, kScnWide, sm, st>>>(d, T, stamps);
+  } else {
+    e = cudaFuncSetAttribute(k_forward_scn<kScnThreads, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sm));
+    if (e != cudaSuccess) return e;
+    k_forward_scn<kScnThreads, 2><<<nb, kScnThreads, sm, st>>>(d, T, stamps);
+  }
   return cudaGetLastError();
 }
 
