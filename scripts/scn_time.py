@@ -32,7 +32,7 @@ for B in Bs:
         del e
     same = all(np.array_equal(x, y) for x, y in zip(cums[3], cums[4]))
     print(f"B={B}: " + "  ".join(f"mode{m} {v:.2f} ms" for m, v in res.items()) + f"  mode4==mode3 {same}", flush=True)
-for B in (8, 256):
+for B in (8, 128, 256):
     e = P.Engine(sc, B, 120); e.set_stream(st.cuda_stream)
     e.set_params(p); e.set_state(lk, ps)
     for b in range(B): e.set_noise(7, 1000 + b, b)
