@@ -193,3 +193,23 @@ def test_pinned_result_buffers_equal_pageable(B):
             assert np.array_equal(got[b].pos_final, want[b].pos_final)
     with pytest.raises(ValueError):
         P.simulate_forward(sc, p, seed=7, noise_iterations=list(range(B + 1)), out=outs)
+
+
+def test_scenario_resident_falls_back_when_link_state_exceeds_shared_memory():
+    """C2's 12,300 links do not fit one CTA's shared memory: an explicit
+    mode 4 runs the step graph instead, with the same results."""
+    sc = P.Scenario.grid(50, 400.0, 42, 1000.0).configure(100000, 1, 20, 300)
+    p = sc.sample_parameters(3)
+    out = []
+    for mode in (4, 3):
+        e = P.Engine(sc, 2, 20)
+        e.set_mode(mode)
+        e.set_params(p)
+        lk, ps = sc.seed_agents()
+        e.set_state(lk, ps)
+        for b in range(2):
+            e.set_noise(7, b, b)
+        e.forward(20, 20)
+        assert e.last_mode // 1000 == 3
+        out.append([e.read_cum(b) for b in range(2)])
+    assert all(np.array_equal(x, y) for x, y in zip(*out))
